@@ -1,0 +1,245 @@
+// The sum-factorised cell kernel (K1/K2) as a reusable device building block.
+#pragma once
+
+#include "nnmg_kernels.cuh"
+
+namespace nnmg {
+
+// ---------------------------------------------------------------------------
+// K1/K2: the sum-factorised cell kernel.  One thread block per block of CB
+// cells; gather -> interpolate to quadrature points (S sweeps) -> collocation
+// gradient (Dc sweeps) -> quadrature-point physics -> transposed sweeps ->
+// scatter-add.  Reproduces LaplaceOperator.apply (mfoperator.py:108-122) and
+// ElasticityOperator.apply (mfoperator.py:171-202); the gradient D u is formed
+// as Dc (S u), mathematically identical to the reference's D sweeps.
+// ---------------------------------------------------------------------------
+template <int DIM, int P, int NCOMP, int PHYS>
+struct CellKernel {
+  static constexpr int N1 = P + 1;
+  static constexpr int NLOC = ipow(N1, DIM);
+  static constexpr int NPEN = ipow(N1, DIM - 1);
+  static constexpr int CB = cells_per_block<DIM, P, NCOMP>();
+  static constexpr int NG = GeoCount<DIM, PHYS>::value;
+  static constexpr int NTHREADS = NPEN * CB;
+  static constexpr int NBUF = 3;
+  static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * CB * sizeof(double);
+  using PL = Pencil<DIM, N1>;
+
+  __device__ __forceinline__ static double& S(double* sm, int b, int c, int pos, int lane) {
+    return sm[((b * NCOMP + c) * NLOC + pos) * CB + lane];
+  }
+
+  template <int K>
+  __device__ __forceinline__ static void load(double* sm, int b, int pen, int lane, double (&v)[NCOMP][N1]) {
+    const int base = PL::base(K, pen);
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) v[c][i] = S(sm, b, c, base + i * PL::stride(K), lane);
+  }
+  template <int K>
+  __device__ __forceinline__ static void store(double* sm, int b, int pen, int lane, const double (&v)[NCOMP][N1]) {
+    const int base = PL::base(K, pen);
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c)
+#pragma unroll
+      for (int i = 0; i < N1; ++i) S(sm, b, c, base + i * PL::stride(K), lane) = v[c][i];
+  }
+  __device__ __forceinline__ static void op(const double (&M)[kMaxN1][kMaxN1], double (&v)[NCOMP][N1], bool trans) {
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) {
+      double t[N1];
+      if (trans)
+        sweep_t<N1>(M, v[c], t);
+      else
+        sweep<N1>(M, v[c], t);
+#pragma unroll
+      for (int i = 0; i < N1; ++i) v[c][i] = t[i];
+    }
+  }
+
+  // one cell block; the NTHREADS threads tid = 0..NTHREADS-1 of a (sub)group
+  // participate, `sync` synchronises exactly that group.  kNC selects the
+  // read-only (non-coherent) path for the source vector, which is only legal
+  // when no thread of the grid writes it during the kernel.
+  template <bool kNC = true, class Sync>
+  __device__ __forceinline__ static void run(const Tables& tab, const double* __restrict__ src,
+                                             double* __restrict__ dst, const int* __restrict__ idx,
+                                             const double* __restrict__ geo, int64_t blk, double lam,
+                                             double mu, double* sm, int tid, Sync&& sync) {
+    const int lane = tid % CB;
+    const int pen = tid / CB;
+    constexpr int A = 0, GX = 1, GY = 2;
+    double v[NCOMP][N1];
+    int gi[N1];
+    // P1: gather the x-pencil and interpolate along x
+    {
+      const int base = PL::base(0, pen);
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        gi[i] = __ldcs(idx + (blk * NLOC + base + i) * CB + lane);
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? (kNC ? __ldg(src + (int64_t)gi[i] * NCOMP + c) : src[(int64_t)gi[i] * NCOMP + c]) : 0.0;
+      }
+      op(tab.S, v, false);
+      store<0>(sm, A, pen, lane, v);
+    }
+    sync();
+    if constexpr (DIM == 3) {
+      // P2: interpolate along y
+      load<1>(sm, A, pen, lane, v);
+      op(tab.S, v, false);
+      store<1>(sm, A, pen, lane, v);
+      sync();
+    }
+    // P3: interpolate along the last axis -> values at quadrature points
+    constexpr int KL = DIM - 1;
+    double gl[NCOMP][N1];
+    load<KL>(sm, A, pen, lane, v);
+    op(tab.S, v, false);
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) sweep<N1>(tab.Dc, v[c], gl[c]);
+    store<KL>(sm, A, pen, lane, v);
+    sync();
+    // P4: collocation derivatives along x (and y in 3D)
+    {
+      double w[NCOMP][N1];
+      load<0>(sm, A, pen, lane, w);
+      op(tab.Dc, w, false);
+      store<0>(sm, GX, pen, lane, w);
+      if constexpr (DIM == 3) {
+        load<1>(sm, A, pen, lane, w);
+        op(tab.Dc, w, false);
+        store<1>(sm, GY, pen, lane, w);
+      }
+    }
+    sync();
+    // P5: quadrature-point physics on the last-axis pencil
+    {
+      const int base = PL::base(KL, pen);
+      double fl[NCOMP][N1];
+      double fx[NCOMP][N1], fy[NCOMP][N1];
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        const int pos = base + q * PL::stride(KL);
+        double g[NCOMP][DIM], f[NCOMP][DIM];
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) {
+          g[c][0] = S(sm, GX, c, pos, lane);
+          if constexpr (DIM == 3) g[c][1] = S(sm, GY, c, pos, lane);
+          g[c][DIM - 1] = gl[c][q];
+        }
+        qp_flux<DIM, NCOMP, PHYS, CB>(geo + ((blk * (int64_t)NLOC + pos) * NG) * CB + lane, g, f, lam, mu);
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) {
+          fx[c][q] = f[c][0];
+          if constexpr (DIM == 3) fy[c][q] = f[c][1];
+          fl[c][q] = f[c][DIM - 1];
+        }
+      }
+      // last-axis derivative transpose stays in registers
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) {
+        double t[N1];
+        sweep_t<N1>(tab.Dc, fl[c], t);
+#pragma unroll
+        for (int i = 0; i < N1; ++i) fl[c][i] = t[i];
+      }
+      store<KL>(sm, GX, pen, lane, fx);
+      if constexpr (DIM == 3) {
+        store<KL>(sm, GY, pen, lane, fy);
+        store<KL>(sm, A, pen, lane, fl);
+      } else {
+        // 2D: keep the y part in registers (v) for P7
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c)
+#pragma unroll
+          for (int i = 0; i < N1; ++i) v[c][i] = fl[c][i];
+      }
+    }
+    sync();
+    if constexpr (DIM == 3) {
+      // P6: A += Dc^T fx along x
+      {
+        double w[NCOMP][N1], a[NCOMP][N1];
+        load<0>(sm, GX, pen, lane, w);
+        op(tab.Dc, w, true);
+        load<0>(sm, A, pen, lane, a);
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c)
+#pragma unroll
+          for (int i = 0; i < N1; ++i) a[c][i] += w[c][i];
+        store<0>(sm, A, pen, lane, a);
+      }
+      sync();
+      // P7: w = A + Dc^T fy along y, then S^T along y
+      {
+        double w[NCOMP][N1], a[NCOMP][N1];
+        load<1>(sm, GY, pen, lane, w);
+        op(tab.Dc, w, true);
+        load<1>(sm, A, pen, lane, a);
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c)
+#pragma unroll
+          for (int i = 0; i < N1; ++i) a[c][i] += w[c][i];
+        op(tab.S, a, true);
+        store<1>(sm, A, pen, lane, a);
+      }
+      sync();
+      // P8: S^T along z
+      load<2>(sm, A, pen, lane, v);
+      op(tab.S, v, true);
+      store<2>(sm, A, pen, lane, v);
+      sync();
+    } else {
+      // 2D P6: A = Dc^T fx along x
+      {
+        double w[NCOMP][N1];
+        load<0>(sm, GX, pen, lane, w);
+        op(tab.Dc, w, true);
+        store<0>(sm, A, pen, lane, w);
+      }
+      sync();
+      // 2D P7: w = A + (y part in registers), S^T along y
+      {
+        double a[NCOMP][N1];
+        load<1>(sm, A, pen, lane, a);
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c)
+#pragma unroll
+          for (int i = 0; i < N1; ++i) a[c][i] += v[c][i];
+        op(tab.S, a, true);
+        store<1>(sm, A, pen, lane, a);
+      }
+      sync();
+    }
+    // final: S^T along x and scatter-add the x-pencil
+    load<0>(sm, A, pen, lane, v);
+    op(tab.S, v, true);
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      if (gi[i] >= 0) {
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, v[c][i]);
+      }
+    }
+  }
+};
+
+
+template <class F>
+inline void dispatch(int dim, int degree, int ncomp, int physics, F&& f) {
+#define NNMG_CASE(D, P, NC, PH) \
+  if (dim == D && degree == P && ncomp == NC && physics == PH) return f.template operator()<D, P, NC, PH>();
+#define NNMG_DEG(D, P)                 \
+  NNMG_CASE(D, P, 1, kLaplace)         \
+  NNMG_CASE(D, P, D, kElasticity)
+  NNMG_DEG(2, 1) NNMG_DEG(2, 2) NNMG_DEG(2, 3) NNMG_DEG(2, 4)
+  NNMG_DEG(3, 1) NNMG_DEG(3, 2) NNMG_DEG(3, 3) NNMG_DEG(3, 4)
+#undef NNMG_DEG
+#undef NNMG_CASE
+  throw Error{kUnsupported, "unsupported (dim, degree, components, physics) combination"};
+}
+
+
+}  // namespace nnmg

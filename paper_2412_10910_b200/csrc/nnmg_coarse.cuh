@@ -1,0 +1,24 @@
+#pragma once
+
+#include "nnmg_level.cuh"
+
+namespace nnmg {
+
+struct Coarse {
+  Level* level = nullptr;
+  bool dense = false;
+  DevBuf<double> ainv;  // dense inverse (row-major)
+  double reduction = 1e-8;
+  int max_iter = 10000;
+  DevBuf<double> r, z, p, ap, part;
+  DevBuf<int> status;  // iterations, converged, error
+  int nrank = 1, nsub = 1, block = 0;
+  size_t smem = 0;
+};
+
+Coarse* coarse_dense_create(Level* L, const double* inverse);
+Coarse* coarse_cg_create(Level* L, double reduction, int max_iter);
+void coarse_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
+void coarse_status(Coarse& C, int* iterations, int* converged, int* error);
+
+}  // namespace nnmg

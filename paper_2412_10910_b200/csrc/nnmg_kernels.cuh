@@ -1,0 +1,144 @@
+// Device-side building blocks of the sum-factorised cell kernels.
+//
+// Layout conventions:
+//   * cells are processed in blocks of CB consecutive cells; a thread block
+//     of NPEN*CB threads owns one cell block, thread t = pen*CB + lane works on
+//     cell `lane` of the block and on pencil `pen` (a line of N1 tensor-product
+//     points along the current sweep direction);
+//   * index table  idx[blk][l][CB]   int32 scalar DoF, -1 = constrained/padding;
+//   * geometry     geo[blk][q][k][CB] double (k < NG per quadrature point);
+//   * shared memory buffers sm[b][c][pos][CB] (cell fastest => conflict free).
+// Local / quadrature position pos = i0 + N1*i1 + N1^2*i2 (x fastest) as the
+// reference's local DoF order (mesh.py:20-25, mfoperator.py:58-59).
+#pragma once
+
+#include "nnmg_common.cuh"
+
+namespace nnmg {
+
+enum Physics : int { kLaplace = 0, kElasticity = 1 };
+
+template <int DIM, int PHYS>
+struct GeoCount {
+  static constexpr int value = PHYS == kLaplace ? DIM * (DIM + 1) / 2 : DIM * DIM + 1;
+};
+
+template <int DIM, int P, int NCOMP>
+__host__ __device__ constexpr int cells_per_block() {
+  constexpr int N1 = P + 1;
+  constexpr int NLOC = ipow(N1, DIM);
+  constexpr int NPEN = ipow(N1, DIM - 1);
+  return (3 * NCOMP * NLOC * 32 * 8 <= 100 * 1024 && NPEN * 32 <= 1024)   ? 32
+         : (3 * NCOMP * NLOC * 16 * 8 <= 100 * 1024 && NPEN * 16 <= 1024) ? 16
+                                                                            : 8;
+}
+
+template <int DIM, int N1>
+struct Pencil {
+  static constexpr int NLOC = ipow(N1, DIM);
+  static constexpr int NPEN = ipow(N1, DIM - 1);
+  // first position of pencil `pen` along direction k
+  __device__ __forceinline__ static int base(int k, int pen) {
+    if (DIM == 2) return k == 0 ? N1 * pen : pen;
+    if (k == 0) return N1 * pen;
+    if (k == 1) return (pen % N1) + N1 * N1 * (pen / N1);
+    return pen;
+  }
+  __host__ __device__ static constexpr int stride(int k) { return k == 0 ? 1 : (k == 1 ? N1 : N1 * N1); }
+};
+
+// out[q] = sum_i M[q][i] in[i]
+template <int N1>
+__device__ __forceinline__ void sweep(const double (&M)[kMaxN1][kMaxN1], const double* in, double* out) {
+#pragma unroll
+  for (int q = 0; q < N1; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) s = fma(M[q][i], in[i], s);
+    out[q] = s;
+  }
+}
+
+// out[i] = sum_q M[q][i] in[q]
+template <int N1>
+__device__ __forceinline__ void sweep_t(const double (&M)[kMaxN1][kMaxN1], const double* in, double* out) {
+#pragma unroll
+  for (int i = 0; i < N1; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < N1; ++q) s = fma(M[q][i], in[q], s);
+    out[i] = s;
+  }
+}
+
+// Quadrature-point physics.  g[c][j] = d u_c / d xhat_j at the point; returns
+// the reference-coordinate flux f[c][j] that is integrated against d phi/d xhat_j.
+template <int DIM, int NCOMP, int PHYS, int CB>
+__device__ __forceinline__ void qp_flux(const double* __restrict__ geo, const double (&g)[NCOMP][DIM],
+                                        double (&f)[NCOMP][DIM], double lam, double mu) {
+  if constexpr (PHYS == kLaplace) {
+    // G = J^-1 J^-T |det J| w_q, symmetric (mfoperator.py:106, 118)
+    if constexpr (DIM == 3) {
+      const double g00 = __ldcs(geo + 0 * CB), g01 = __ldcs(geo + 1 * CB), g02 = __ldcs(geo + 2 * CB);
+      const double g11 = __ldcs(geo + 3 * CB), g12 = __ldcs(geo + 4 * CB), g22 = __ldcs(geo + 5 * CB);
+      f[0][0] = g00 * g[0][0] + g01 * g[0][1] + g02 * g[0][2];
+      f[0][1] = g01 * g[0][0] + g11 * g[0][1] + g12 * g[0][2];
+      f[0][2] = g02 * g[0][0] + g12 * g[0][1] + g22 * g[0][2];
+    } else {
+      const double g00 = __ldcs(geo + 0 * CB), g01 = __ldcs(geo + 1 * CB), g11 = __ldcs(geo + 2 * CB);
+      f[0][0] = g00 * g[0][0] + g01 * g[0][1];
+      f[0][1] = g01 * g[0][0] + g11 * g[0][1];
+    }
+  } else {
+    // linear elasticity (mfoperator.py:183-191): pg = ghat J^-1, eps = sym(pg),
+    // sigma = 2 mu eps + lam tr(eps) I, flux = sigma J^-T |det J| w_q
+    double K[DIM][DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) K[a][b] = __ldcs(geo + (a * DIM + b) * CB);
+    const double dv = __ldcs(geo + DIM * DIM * CB);
+    double pg[DIM][DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) s = fma(g[a][j], K[j][b], s);
+        pg[a][b] = s;
+      }
+    double tr = 0.0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) tr += pg[a][a];
+    double sig[DIM][DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int b = 0; b < DIM; ++b) sig[a][b] = mu * (pg[a][b] + pg[b][a]) + (a == b ? lam * tr : 0.0);
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < DIM; ++b) s = fma(sig[a][b], K[j][b], s);
+        f[a][j] = s * dv;
+      }
+  }
+}
+
+// Lagrange basis at the Lobatto nodes evaluated at t (fespace.py:42-51)
+template <int N1>
+__device__ __forceinline__ void lagrange_values(const Tables& tab, double t, double* out) {
+#pragma unroll
+  for (int i = 0; i < N1; ++i) {
+    double v = 1.0;
+#pragma unroll
+    for (int j = 0; j < N1; ++j)
+      if (j != i) v *= (t - tab.nodes[j]);
+    out[i] = v / tab.denom[i];
+  }
+}
+
+}  // namespace nnmg

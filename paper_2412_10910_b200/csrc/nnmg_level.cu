@@ -1,0 +1,358 @@
+// K4 geometry precompute, K1/K2 matrix-free apply, K3 diagonal.
+#include "nnmg_level.cuh"
+#include "nnmg_kernels.cuh"
+#include "nnmg_cellkernel.cuh"
+
+#include <algorithm>
+#include <cstring>
+
+namespace nnmg {
+
+// ---------------------------------------------------------------------------
+// K4: per-quadrature-point geometry (mfoperator.py:28-48, 101-106, 163-169)
+// J[a][b] = sum_v dW_v/dxhat_b(q) X_v[a]   (mesh.py:138-143)
+// ---------------------------------------------------------------------------
+template <int DIM, int PHYS>
+__global__ void k_geometry(const double* __restrict__ verts, const int64_t* __restrict__ cells,
+                           int64_t n_cells, int nq1, Tables tab, int cb, double* __restrict__ geo,
+                           int* __restrict__ bad) {
+  constexpr int NV = 1 << DIM;
+  constexpr int NG = GeoCount<DIM, PHYS>::value;
+  const int nq = DIM == 2 ? nq1 * nq1 : nq1 * nq1 * nq1;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_cells * nq) return;
+  const int64_t c = t / nq;
+  const int q = static_cast<int>(t % nq);
+  int qi[3] = {q % nq1, (q / nq1) % nq1, q / (nq1 * nq1)};
+  double xh[3], wq = 1.0;
+  for (int j = 0; j < DIM; ++j) {
+    xh[j] = tab.xq[qi[j]];
+    wq *= tab.w[qi[j]];
+  }
+  double J[DIM][DIM] = {};
+  for (int v = 0; v < NV; ++v) {
+    const double* X = verts + cells[c * NV + v] * DIM;
+    for (int b = 0; b < DIM; ++b) {
+      double gr = 1.0;
+      for (int j = 0; j < DIM; ++j) {
+        const int bit = (v >> j) & 1;
+        if (j == b)
+          gr *= bit ? 1.0 : -1.0;
+        else
+          gr *= bit ? xh[j] : 1.0 - xh[j];
+      }
+      for (int a = 0; a < DIM; ++a) J[a][b] += gr * X[a];
+    }
+  }
+  double det, K[DIM][DIM];
+  if constexpr (DIM == 2) {
+    det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    K[0][0] = J[1][1] / det;
+    K[0][1] = -J[0][1] / det;
+    K[1][0] = -J[1][0] / det;
+    K[1][1] = J[0][0] / det;
+  } else {
+    const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    K[0][0] = c00 / det;
+    K[1][0] = c01 / det;
+    K[2][0] = c02 / det;
+    K[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+    K[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+    K[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+    K[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+    K[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+    K[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+  }
+  if (!(det > 0.0)) atomicOr(bad, 1);
+  const int64_t blk = c / cb, lane = c % cb;
+  double* out = geo + ((blk * nq + q) * NG) * cb + lane;
+  if constexpr (PHYS == kLaplace) {
+    int k = 0;
+    for (int a = 0; a < DIM; ++a)
+      for (int b = a; b < DIM; ++b) {
+        double s = 0.0;
+        for (int j = 0; j < DIM; ++j) s += K[a][j] * K[b][j];
+        out[(k++) * cb] = s * det * wq;
+      }
+  } else {
+    for (int a = 0; a < DIM; ++a)
+      for (int b = 0; b < DIM; ++b) out[(a * DIM + b) * cb] = K[a][b];
+    out[DIM * DIM * cb] = det * wq;
+  }
+}
+
+template <int DIM, int P, int NCOMP, int PHYS>
+__global__ void __launch_bounds__(CellKernel<DIM, P, NCOMP, PHYS>::NTHREADS)
+    k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
+            const double* __restrict__ geo, int64_t b0, double lam, double mu) {
+  extern __shared__ double sm[];
+  CellKernel<DIM, P, NCOMP, PHYS>::template run<true>(tab, src, dst, idx, geo, b0 + blockIdx.x, lam, mu, sm,
+                                                     threadIdx.x, [] __device__() { __syncthreads(); });
+}
+
+// ---------------------------------------------------------------------------
+// K3: exact diagonal.  Thread per (cell, local DoF); sum over quadrature
+// points of w gt^T G gt (Laplace, mfoperator.py:135-150) or
+// dv((lam+mu) pg_a^2 + mu |pg|^2) (elasticity, mfoperator.py:219-238).
+// ---------------------------------------------------------------------------
+template <int DIM, int P, int NCOMP, int PHYS>
+__global__ void k_diagonal(Tables tab, const int* __restrict__ idx, const double* __restrict__ geo, int64_t nblk,
+                           double lam, double mu, double* __restrict__ diag) {
+  using CK = CellKernel<DIM, P, NCOMP, PHYS>;
+  constexpr int N1 = CK::N1, NLOC = CK::NLOC, CB = CK::CB, NG = CK::NG;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nblk * NLOC * CB) return;
+  const int lane = t % CB;
+  const int l = (t / CB) % NLOC;
+  const int64_t blk = t / (CB * NLOC);
+  const int g = idx[(blk * NLOC + l) * CB + lane];
+  if (g < 0) return;
+  const int li[3] = {l % N1, (l / N1) % N1, l / (N1 * N1)};
+  double acc[NCOMP] = {};
+  for (int q = 0; q < NLOC; ++q) {
+    const int qi[3] = {q % N1, (q / N1) % N1, q / (N1 * N1)};
+    double gt[DIM];
+    for (int j = 0; j < DIM; ++j) {
+      double s = 1.0;
+      for (int k = 0; k < DIM; ++k) s *= (k == j ? tab.D[qi[k]][li[k]] : tab.S[qi[k]][li[k]]);
+      gt[j] = s;
+    }
+    const double* G = geo + ((blk * NLOC + q) * NG) * CB + lane;
+    if constexpr (PHYS == kLaplace) {
+      double Gm[DIM][DIM];
+      int k = 0;
+      for (int a = 0; a < DIM; ++a)
+        for (int b = a; b < DIM; ++b) {
+          Gm[a][b] = G[(k++) * CB];
+          Gm[b][a] = Gm[a][b];
+        }
+      double s = 0.0;
+      for (int a = 0; a < DIM; ++a)
+        for (int b = 0; b < DIM; ++b) s += gt[a] * Gm[a][b] * gt[b];
+      acc[0] += s;
+    } else {
+      double pg[DIM];
+      double n2 = 0.0;
+      for (int b = 0; b < DIM; ++b) {
+        double s = 0.0;
+        for (int i = 0; i < DIM; ++i) s += gt[i] * G[(i * DIM + b) * CB];
+        pg[b] = s;
+        n2 += s * s;
+      }
+      const double dv = G[DIM * DIM * CB];
+      for (int a = 0; a < NCOMP; ++a) acc[a] += dv * ((lam + mu) * pg[a] * pg[a] + mu * n2);
+    }
+  }
+  for (int a = 0; a < NCOMP; ++a) atomicAdd(diag + (int64_t)g * NCOMP + a, acc[a]);
+}
+
+__global__ void k_copy_constrained(const int* __restrict__ cd, int64_t n, const double* __restrict__ src,
+                                   double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[cd[i]] = src[cd[i]];
+}
+
+__global__ void k_set_constrained(const int* __restrict__ cd, int64_t n, double val, double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[cd[i]] = val;
+}
+
+__global__ void k_reciprocal(const double* __restrict__ a, double* __restrict__ b, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = 1.0 / a[i];
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+struct CbOf {
+  int* out;
+  template <int D, int P, int NC, int PH>
+  void operator()() { *out = cells_per_block<D, P, NC>(); }
+};
+
+static int cb_of(int dim, int degree, int ncomp, int physics) {
+  int cb = 0;
+  CbOf f{&cb};
+  dispatch(dim, degree, ncomp, physics, f);
+  return cb;
+}
+
+static inline unsigned grid_for(int64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
+Level* level_create(int device, int dim, int degree, int ncomp, int physics, int64_t n_cells,
+                    int64_t n_vertices, const double* vertices, const int64_t* cells, int64_t n_scalar,
+                    const int64_t* cell_dofs, int64_t n_constrained, const int64_t* constrained, double lam,
+                    double mu) {
+  NNMG_REQUIRE(dim == 2 || dim == 3, kInvalidArgument, "dim must be 2 or 3");
+  NNMG_REQUIRE(physics == kLaplace ? ncomp == 1 : ncomp == dim, kInvalidArgument,
+               "Laplace needs 1 component, elasticity dim components");
+  NNMG_REQUIRE(n_cells > 0, kInvalidArgument, "empty mesh");
+  NNMG_REQUIRE(n_scalar * ncomp < (int64_t(1) << 31), kUnsupported, "more than 2^31 DoFs per level");
+  NNMG_CUDA_TRY(cudaSetDevice(device));
+  auto L = new Level();
+  try {
+    L->device = device;
+    L->dim = dim;
+    L->degree = degree;
+    L->ncomp = ncomp;
+    L->physics = physics;
+    L->n1 = degree + 1;
+    L->nloc = ipow(L->n1, dim);
+    L->nq = L->nloc;
+    L->ng = physics == kLaplace ? dim * (dim + 1) / 2 : dim * dim + 1;
+    L->cb = cb_of(dim, degree, ncomp, physics);
+    L->n_cells = n_cells;
+    L->nblk = (n_cells + L->cb - 1) / L->cb;
+    L->n_scalar = n_scalar;
+    L->n_dofs = n_scalar * ncomp;
+    L->lam = lam;
+    L->mu = mu;
+    L->tab = make_tables(degree);
+    // constraints: the kernels support whole-node constraints (every component
+    // of a scalar DoF), which is what dirichlet_constraints produces
+    L->scalar_constrained.assign(n_scalar, 0);
+    std::vector<int> cd(n_constrained);
+    std::vector<int> per_node(n_scalar, 0);
+    for (int64_t i = 0; i < n_constrained; ++i) {
+      const int64_t d = constrained[i];
+      NNMG_REQUIRE(d >= 0 && d < L->n_dofs, kInvalidArgument, "constrained DoF out of range");
+      cd[i] = static_cast<int>(d);
+      per_node[d / ncomp] += 1;
+    }
+    for (int64_t s = 0; s < n_scalar; ++s) {
+      NNMG_REQUIRE(per_node[s] == 0 || per_node[s] == ncomp, kUnsupported,
+                   "partially constrained vector nodes are not supported");
+      L->scalar_constrained[s] = per_node[s] ? 1 : 0;
+    }
+    L->cdofs.upload(cd);
+    // index table in the blocked layout
+    const int nloc = L->nloc, cb = L->cb;
+    std::vector<int> idx(size_t(L->nblk) * nloc * cb, -1);
+    L->cell_dofs_host.resize(size_t(n_cells) * nloc);
+    for (int64_t c = 0; c < n_cells; ++c) {
+      const int64_t blk = c / cb, lane = c % cb;
+      for (int l = 0; l < nloc; ++l) {
+        const int64_t g = cell_dofs[c * nloc + l];
+        NNMG_REQUIRE(g >= 0 && g < n_scalar, kInvalidArgument, "cell_dofs entry out of range");
+        L->cell_dofs_host[c * nloc + l] = static_cast<int>(g);
+        idx[(blk * nloc + l) * cb + lane] = L->scalar_constrained[g] ? -1 : static_cast<int>(g);
+      }
+    }
+    L->idx.upload(idx);
+    // geometry on the device from vertex coordinates
+    DevBuf<double> dverts;
+    DevBuf<int64_t> dcells;
+    dverts.upload(vertices, size_t(n_vertices) * dim);
+    for (int64_t i = 0; i < n_cells * (int64_t(1) << dim); ++i)
+      NNMG_REQUIRE(cells[i] >= 0 && cells[i] < n_vertices, kInvalidArgument, "cell vertex index out of range");
+    dcells.upload(cells, size_t(n_cells) << dim);
+    L->geo.alloc(size_t(L->nblk) * L->nq * L->ng * cb);
+    L->geo.zero();
+    DevBuf<int> bad;
+    bad.alloc(1);
+    bad.zero();
+    const int64_t nt = n_cells * L->nq;
+    const int bs = 256;
+    if (dim == 2 && physics == kLaplace)
+      k_geometry<2, kLaplace><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+    else if (dim == 2)
+      k_geometry<2, kElasticity><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+    else if (physics == kLaplace)
+      k_geometry<3, kLaplace><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+    else
+      k_geometry<3, kElasticity><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+    int hbad = 0;
+    NNMG_CUDA_TRY(cudaMemcpy(&hbad, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+    NNMG_REQUIRE(hbad == 0, kGeometryError, "mesh has non-positive Jacobians");
+    L->diag.alloc(L->n_dofs);
+    L->inv_diag.alloc(L->n_dofs);
+  } catch (...) {
+    delete L;
+    throw;
+  }
+  return L;
+}
+
+struct ApplyLaunch {
+  const Level& L;
+  const double* src;
+  double* dst;
+  int64_t b0, b1;
+  cudaStream_t s;
+  template <int D, int P, int NC, int PH>
+  void operator()() {
+    using CK = CellKernel<D, P, NC, PH>;
+    auto kern = k_apply<D, P, NC, PH>;
+    static bool attr = false;
+    if (!attr) {
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK::SMEM));
+      attr = true;
+    }
+    const int64_t nb = b1 - b0;
+    for (int64_t off = 0; off < nb; off += 0x7fffffff) {
+      const unsigned g = static_cast<unsigned>(std::min<int64_t>(nb - off, 0x7fffffff));
+      kern<<<g, CK::NTHREADS, CK::SMEM, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0 + off, L.lam, L.mu);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+    }
+  }
+};
+
+void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1, cudaStream_t s) {
+  if (b1 <= b0) return;
+  ApplyLaunch f{L, src, dst, b0, b1, s};
+  dispatch(L.dim, L.degree, L.ncomp, L.physics, f);
+}
+
+void launch_copy_constrained(const Level& L, const double* src, double* dst, cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(L.cdofs.n);
+  if (!n) return;
+  k_copy_constrained<<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void level_apply(Level& L, const double* src, double* dst, cudaStream_t s) {
+  NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
+  NNMG_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * L.n_dofs, s));
+  launch_apply_cells(L, src, dst, 0, L.nblk, s);
+  launch_copy_constrained(L, src, dst, s);
+}
+
+struct DiagLaunch {
+  Level& L;
+  cudaStream_t s;
+  template <int D, int P, int NC, int PH>
+  void operator()() {
+    using CK = CellKernel<D, P, NC, PH>;
+    const int64_t nt = L.nblk * CK::NLOC * CK::CB;
+    k_diagonal<D, P, NC, PH><<<grid_for(nt, 128), 128, 0, s>>>(L.tab, L.idx.ptr, L.geo.ptr, L.nblk, L.lam, L.mu,
+                                                                L.diag.ptr);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+  }
+};
+
+void level_compute_diagonal(Level& L, cudaStream_t s) {
+  L.diag.zero(s);
+  DiagLaunch f{L, s};
+  dispatch(L.dim, L.degree, L.ncomp, L.physics, f);
+  const int64_t n = static_cast<int64_t>(L.cdofs.n);
+  if (n) {
+    k_set_constrained<<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, 1.0, L.diag.ptr);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+  }
+  k_reciprocal<<<grid_for(L.n_dofs, 256), 256, 0, s>>>(L.diag.ptr, L.inv_diag.ptr, L.n_dofs);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+  L.diag_ready = true;
+}
+
+}  // namespace nnmg

@@ -1,0 +1,42 @@
+// Level handle: the device-resident state of one multigrid level
+// (replaces the reference _OperatorBase + LaplaceOperator / ElasticityOperator,
+// mfoperator.py:25-252).
+#pragma once
+
+#include "nnmg_common.cuh"
+
+namespace nnmg {
+
+struct Level {
+  int device = 0;
+  int dim = 0, degree = 0, ncomp = 1, physics = 0;
+  int n1 = 0, nloc = 0, nq = 0, ng = 0, cb = 32;
+  int64_t n_cells = 0, nblk = 0, n_scalar = 0, n_dofs = 0;
+  double lam = 0.0, mu = 0.0;
+  Tables tab{};
+  DevBuf<int> idx;       // [nblk][nloc][cb], -1 = constrained or padding
+  DevBuf<double> geo;    // [nblk][nq][ng][cb]
+  DevBuf<int> cdofs;     // constrained full DoFs, sorted
+  DevBuf<double> diag;   // cached exact diagonal (constrained = 1)
+  DevBuf<double> inv_diag;
+  bool diag_ready = false;
+  std::vector<int> cell_dofs_host;  // plain (nc, nloc) copy for transfer setup
+  std::vector<uint8_t> scalar_constrained;  // per scalar DoF
+};
+
+Level* level_create(int device, int dim, int degree, int ncomp, int physics, int64_t n_cells,
+                    int64_t n_vertices, const double* vertices, const int64_t* cells,
+                    int64_t n_scalar, const int64_t* cell_dofs, int64_t n_constrained,
+                    const int64_t* constrained, double lam, double mu);
+
+// v = A u with zero-in / identity-out constraint convention (mfoperator.py:108-122)
+void level_apply(Level& L, const double* src, double* dst, cudaStream_t s);
+// exact diagonal, constrained = 1 (mfoperator.py:92-95, 135-150, 219-238)
+void level_compute_diagonal(Level& L, cudaStream_t s);
+
+// launch the raw cell kernel (no zeroing, no constraint fix-up) over cell blocks [b0, b1)
+void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1,
+                        cudaStream_t s);
+void launch_copy_constrained(const Level& L, const double* src, double* dst, cudaStream_t s);
+
+}  // namespace nnmg

@@ -1,0 +1,574 @@
+// K6 prolongation, K7 restriction (deterministic, two-phase) and the GPU point
+// location that builds the transfer records.
+#include "nnmg_transfer.cuh"
+#include "nnmg_cellkernel.cuh"
+
+#include <algorithm>
+#include <cmath>
+
+namespace nnmg {
+
+static inline unsigned grid_for(int64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
+
+static constexpr int kWarps = 4;  // coarse cells (one per warp) per thread block
+
+// ---------------------------------------------------------------------------
+// K6: u_f[pt] (+)= sum_l u_c[gather[pt,l]] prod_j phi_{l_j}(xhat_j)
+// One warp per owning coarse cell: the cell's coarse values are staged once in
+// shared memory and broadcast while the lanes evaluate the cell's points.
+// Contraction order x, then y, then z as transfer.py:93-95.
+// ---------------------------------------------------------------------------
+template <int DIM, int PC, int NCOMP, int CBC>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_prolongate(Tables tab, const double* __restrict__ uc, double* __restrict__ uf, int accumulate,
+                 const int* __restrict__ cidx, const int* __restrict__ cell_start, const int* __restrict__ pt_dof,
+                 const double* __restrict__ xhat, int64_t ncc) {
+  constexpr int N1 = PC + 1;
+  constexpr int NLOC = ipow(N1, DIM);
+  __shared__ double su[kWarps][NCOMP * NLOC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cell = blockIdx.x * (int64_t)kWarps + warp;
+  if (cell >= ncc) return;
+  const int64_t blk = cell / CBC, cl = cell % CBC;
+  for (int l = lane; l < NLOC; l += 32) {
+    const int g = cidx[(blk * NLOC + l) * CBC + cl];
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] : 0.0;
+  }
+  __syncwarp();
+  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
+  for (int p = p0 + lane; p < p1; p += 32) {
+    double X[DIM][N1];
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, xhat[(int64_t)p * DIM + j], X[j]);
+    const int64_t dof = pt_dof[p];
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) {
+      const double* U = su[warp] + c * NLOC;
+      double val;
+      if constexpr (DIM == 2) {
+        double t[N1];
+#pragma unroll
+        for (int i1 = 0; i1 < N1; ++i1) {
+          double s = 0.0;
+#pragma unroll
+          for (int i0 = 0; i0 < N1; ++i0) s = fma(U[i0 + N1 * i1], X[0][i0], s);
+          t[i1] = s;
+        }
+        val = 0.0;
+#pragma unroll
+        for (int i1 = 0; i1 < N1; ++i1) val = fma(t[i1], X[1][i1], val);
+      } else {
+        double t2[N1];
+#pragma unroll
+        for (int i2 = 0; i2 < N1; ++i2) {
+          double s2 = 0.0;
+#pragma unroll
+          for (int i1 = 0; i1 < N1; ++i1) {
+            double s = 0.0;
+#pragma unroll
+            for (int i0 = 0; i0 < N1; ++i0) s = fma(U[i0 + N1 * i1 + N1 * N1 * i2], X[0][i0], s);
+            s2 = fma(s, X[1][i1], s2);
+          }
+          t2[i2] = s2;
+        }
+        val = 0.0;
+#pragma unroll
+        for (int i2 = 0; i2 < N1; ++i2) val = fma(t2[i2], X[2][i2], val);
+      }
+      double* o = uf + dof * NCOMP + c;
+      if (accumulate)
+        *o += val;
+      else
+        *o = val;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7 phase 1: per owning coarse cell, local vector sum_pt r_f[pt] W_pt where
+// W = phi_{l2}(z)(phi_{l1}(y) phi_{l0}(x)) (transfer.py:104-109, 115).  One
+// warp per cell, lanes own local outputs and sweep the cell's points in fixed
+// order: deterministic, no atomics.
+// ---------------------------------------------------------------------------
+template <int DIM, int PC, int NCOMP>
+__global__ void __launch_bounds__(kWarps * 32)
+    k_restrict_cells(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
+                     const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc,
+                     double* __restrict__ cellbuf) {
+  constexpr int N1 = PC + 1;
+  constexpr int NLOC = ipow(N1, DIM);
+  constexpr int NOUT = NLOC * NCOMP;
+  constexpr int NPL = (NOUT + 31) / 32;
+  __shared__ double sv[kWarps][32][NCOMP];
+  __shared__ double sx[kWarps][32][DIM][N1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cell = blockIdx.x * (int64_t)kWarps + warp;
+  if (cell >= ncc) return;
+  double acc[NPL];
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) acc[k] = 0.0;
+  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
+  for (int start = p0; start < p1; start += 32) {
+    const int p = start + lane;
+    if (p < p1) {
+      const int64_t dof = pt_dof[p];
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) sv[warp][lane][c] = rf[dof * NCOMP + c];
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, xhat[(int64_t)p * DIM + j], sx[warp][lane][j]);
+    }
+    __syncwarp();
+    const int cnt = min(32, p1 - start);
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      const int o = lane + 32 * k;
+      if (o < NOUT) {
+        const int l = o / NCOMP, c = o % NCOMP;
+        const int i0 = l % N1, i1 = (l / N1) % N1, i2 = l / (N1 * N1);
+        double a = acc[k];
+        for (int j = 0; j < cnt; ++j) {
+          double w = sx[warp][j][1][i1] * sx[warp][j][0][i0];
+          if constexpr (DIM == 3) w = sx[warp][j][2][i2] * w;
+          a = fma(sv[warp][j][c], w, a);
+        }
+        acc[k] = a;
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    const int o = lane + 32 * k;
+    if (o < NOUT) cellbuf[cell * NOUT + o] = acc[k];
+  }
+}
+
+// K7 phase 2: r_c[g] = sum over the (cell, l) slots holding g, fixed order
+__global__ void k_restrict_gather(const int* __restrict__ t_off, const int* __restrict__ t_ent,
+                                  const double* __restrict__ cellbuf, int64_t nsc, int ncomp, double* __restrict__ rc) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= nsc) return;
+  const int e0 = t_off[g], e1 = t_off[g + 1];
+  for (int c = 0; c < ncomp; ++c) {
+    double s = 0.0;
+    for (int e = e0; e < e1; ++e) s += cellbuf[(int64_t)t_ent[e] * ncomp + c];
+    rc[g * ncomp + c] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct TransferDispatch {
+  Transfer& T;
+  const double* in;
+  double* out;
+  int mode;  // 0 prolongate, 1 prolongate-accumulate, 2 restrict
+  cudaStream_t s;
+  template <int D, int P, int NC, int PH>
+  void operator()() {
+    constexpr int CBC = cells_per_block<D, P, NC>();
+    const Level& C = *T.coarse;
+    const unsigned g = grid_for(T.ncc, kWarps);
+    if (mode < 2) {
+      k_prolongate<D, P, NC, CBC><<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.cell_start.ptr,
+                                                             T.pt_dof.ptr, T.xhat.ptr, T.ncc);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+    } else {
+      k_restrict_cells<D, P, NC><<<g, kWarps * 32, 0, s>>>(C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
+                                                           T.ncc, T.cellbuf.ptr);
+      NNMG_CHECK_LAUNCH();
+      k_restrict_gather<<<grid_for(C.n_scalar, 256), 256, 0, s>>>(T.t_off.ptr, T.t_ent.ptr, T.cellbuf.ptr,
+                                                                   C.n_scalar, NC, out);
+      NNMG_CHECK_LAUNCH();
+      count_launch(2);
+    }
+  }
+};
+
+Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_t* point_dofs, const int64_t* cells,
+                          const double* xhat) {
+  NNMG_REQUIRE(coarse && fine, kInvalidArgument, "null level handle");
+  NNMG_REQUIRE(coarse->ncomp == fine->ncomp, kInvalidArgument, "component counts of the two levels must match");
+  NNMG_REQUIRE(coarse->dim == fine->dim, kInvalidArgument, "levels must share the dimension");
+  NNMG_REQUIRE(npts < (int64_t(1) << 31), kUnsupported, "too many transfer points");
+  NNMG_CUDA_TRY(cudaSetDevice(coarse->device));
+  auto T = new Transfer();
+  try {
+    T->coarse = coarse;
+    T->fine = fine;
+    T->dim = coarse->dim;
+    T->pc = coarse->degree;
+    T->ncomp = coarse->ncomp;
+    T->npts = npts;
+    T->ncc = coarse->n_cells;
+    const int64_t ncc = coarse->n_cells;
+    std::vector<int> start(ncc + 1, 0);
+    for (int64_t i = 0; i < npts; ++i) {
+      NNMG_REQUIRE(cells[i] >= 0 && cells[i] < ncc, kInvalidArgument, "owning cell out of range");
+      NNMG_REQUIRE(point_dofs[i] >= 0 && point_dofs[i] < fine->n_scalar, kInvalidArgument, "point DoF out of range");
+      start[cells[i] + 1] += 1;
+    }
+    for (int64_t c = 0; c < ncc; ++c) start[c + 1] += start[c];
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    std::vector<int> pd(npts);
+    std::vector<double> xh(size_t(npts) * T->dim);
+    for (int64_t i = 0; i < npts; ++i) {
+      const int k = fill[cells[i]]++;
+      pd[k] = static_cast<int>(point_dofs[i]);
+      for (int j = 0; j < T->dim; ++j) xh[size_t(k) * T->dim + j] = xhat[i * T->dim + j];
+    }
+    T->cell_start.upload(start);
+    T->pt_dof.upload(pd);
+    T->xhat.upload(xh);
+    // transposed coarse map for the restriction gather
+    const int nloc = coarse->nloc;
+    const int64_t nsc = coarse->n_scalar;
+    std::vector<int> off(nsc + 1, 0);
+    for (int64_t e = 0; e < ncc * nloc; ++e) {
+      const int g = coarse->cell_dofs_host[e];
+      if (!coarse->scalar_constrained[g]) off[g + 1] += 1;
+    }
+    for (int64_t g = 0; g < nsc; ++g) off[g + 1] += off[g];
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    std::vector<int> ent(off[nsc]);
+    for (int64_t e = 0; e < ncc * nloc; ++e) {
+      const int g = coarse->cell_dofs_host[e];
+      if (!coarse->scalar_constrained[g]) ent[pos[g]++] = static_cast<int>(e);
+    }
+    T->t_off.upload(off);
+    T->t_ent.upload(ent);
+    T->cellbuf.alloc(size_t(ncc) * nloc * T->ncomp);
+  } catch (...) {
+    delete T;
+    throw;
+  }
+  return T;
+}
+
+void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s) {
+  if (!accumulate) NNMG_CUDA_TRY(cudaMemsetAsync(uf, 0, sizeof(double) * T.fine->n_dofs, s));
+  TransferDispatch f{T, uc, uf, accumulate ? 1 : 0, s};
+  dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
+}
+
+void transfer_restrict(Transfer& T, const double* rf, double* rc, cudaStream_t s) {
+  TransferDispatch f{T, rf, rc, 2, s};
+  dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
+}
+
+// ---------------------------------------------------------------------------
+// Point location
+// ---------------------------------------------------------------------------
+struct BucketGrid {
+  double g0[3], h[3];
+  int nb[3];
+};
+
+template <int DIM>
+__device__ __forceinline__ void forward_map(const double (&X)[1 << DIM][DIM], const double* xh, double* out) {
+  for (int a = 0; a < DIM; ++a) out[a] = 0.0;
+  for (int v = 0; v < (1 << DIM); ++v) {
+    double w = 1.0;
+    for (int j = 0; j < DIM; ++j) w *= ((v >> j) & 1) ? xh[j] : 1.0 - xh[j];
+    for (int a = 0; a < DIM; ++a) out[a] += w * X[v][a];
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ void jacobian(const double (&X)[1 << DIM][DIM], const double* xh, double (&J)[DIM][DIM]) {
+  for (int a = 0; a < DIM; ++a)
+    for (int b = 0; b < DIM; ++b) J[a][b] = 0.0;
+  for (int v = 0; v < (1 << DIM); ++v)
+    for (int b = 0; b < DIM; ++b) {
+      double g = 1.0;
+      for (int j = 0; j < DIM; ++j) {
+        const int bit = (v >> j) & 1;
+        g *= (j == b) ? (bit ? 1.0 : -1.0) : (bit ? xh[j] : 1.0 - xh[j]);
+      }
+      for (int a = 0; a < DIM; ++a) J[a][b] += g * X[v][a];
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ double norm(const double* r) {
+  double s = 0.0;
+  for (int a = 0; a < DIM; ++a) s += r[a] * r[a];
+  return sqrt(s);
+}
+
+// LU with partial pivoting; solves J s = r (returns s in r)
+template <int DIM>
+__device__ __forceinline__ void lu_solve(double (&A)[DIM][DIM], double* r) {
+  int piv[DIM];
+  for (int k = 0; k < DIM; ++k) {
+    int p = k;
+    for (int i = k + 1; i < DIM; ++i)
+      if (fabs(A[i][k]) > fabs(A[p][k])) p = i;
+    piv[k] = p;
+    if (p != k)
+      for (int j = 0; j < DIM; ++j) {
+        const double t = A[k][j];
+        A[k][j] = A[p][j];
+        A[p][j] = t;
+      }
+    const double rinv = 1.0 / A[k][k];
+    for (int i = k + 1; i < DIM; ++i) A[i][k] *= rinv;
+    for (int i = k + 1; i < DIM; ++i)
+      for (int j = k + 1; j < DIM; ++j) A[i][j] -= A[i][k] * A[k][j];
+  }
+  for (int k = 0; k < DIM; ++k)
+    if (piv[k] != k) {
+      const double t = r[k];
+      r[k] = r[piv[k]];
+      r[piv[k]] = t;
+    }
+  for (int k = 0; k < DIM; ++k)
+    for (int i = k + 1; i < DIM; ++i) r[i] -= r[k] * A[i][k];
+  for (int j = DIM - 1; j >= 0; --j) {
+    r[j] /= A[j][j];
+    for (int i = 0; i < j; ++i) r[i] -= r[j] * A[i][j];
+  }
+}
+
+// damped Newton inversion of one multilinear cell map (mesh.py:235-287)
+template <int DIM>
+__device__ bool invert_map(const double (&X)[1 << DIM][DIM], const double* x, double tol, double* xh, double* rnorm) {
+  double res[DIM], f[DIM];
+  for (int j = 0; j < DIM; ++j) xh[j] = 0.5;
+  forward_map<DIM>(X, xh, f);
+  for (int a = 0; a < DIM; ++a) res[a] = f[a] - x[a];
+  double rn = norm<DIM>(res);
+  bool conv = rn <= tol;
+  for (int it = 0; it < 30 && !conv; ++it) {
+    double J[DIM][DIM];
+    jacobian<DIM>(X, xh, J);
+    double det, scale = 0.0;
+    if constexpr (DIM == 2)
+      det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    else
+      det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    for (int a = 0; a < DIM; ++a)
+      for (int b = 0; b < DIM; ++b) scale = fmax(scale, fabs(J[a][b]));
+    scale = (DIM == 2 ? scale * scale : scale * scale * scale) + 1e-300;
+    if (fabs(det) < 1e-14 * scale) break;  // singular: failed
+    double step[DIM];
+    for (int a = 0; a < DIM; ++a) step[a] = res[a];
+    lu_solve<DIM>(J, step);
+    double nx[DIM], nr[DIM];
+    for (int j = 0; j < DIM; ++j) nx[j] = xh[j] - step[j];
+    forward_map<DIM>(X, nx, f);
+    for (int a = 0; a < DIM; ++a) nr[a] = f[a] - x[a];
+    double nn = norm<DIM>(nr);
+    for (int h = 0; h < 8 && nn > rn && nn > tol; ++h) {
+      for (int j = 0; j < DIM; ++j) {
+        step[j] *= 0.5;
+        nx[j] = xh[j] - step[j];
+      }
+      forward_map<DIM>(X, nx, f);
+      for (int a = 0; a < DIM; ++a) nr[a] = f[a] - x[a];
+      nn = norm<DIM>(nr);
+    }
+    for (int j = 0; j < DIM; ++j) xh[j] = nx[j];
+    for (int a = 0; a < DIM; ++a) res[a] = nr[a];
+    rn = nn;
+    conv = nn <= tol;
+  }
+  *rnorm = rn;
+  return conv;
+}
+
+template <int DIM>
+__global__ void k_locate(const double* __restrict__ verts, const int64_t* __restrict__ cells,
+                         const double* __restrict__ blo, const double* __restrict__ bhi,
+                         const int* __restrict__ boff, const int* __restrict__ bcells, BucketGrid grid,
+                         const double* __restrict__ pts, int64_t npts, double eps_geo, double eps_ref,
+                         int64_t* __restrict__ out_cell, double* __restrict__ out_xhat, uint8_t* __restrict__ out_proj,
+                         int* __restrict__ n_missing, unsigned long long* __restrict__ first_missing) {
+  constexpr int NV = 1 << DIM;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= npts) return;
+  double x[DIM];
+  for (int j = 0; j < DIM; ++j) x[j] = pts[p * DIM + j];
+  // bucket of the point (clamped); the padded-box test below decides exactly
+  int b = 0, mult = 1;
+  for (int j = 0; j < DIM; ++j) {
+    const double t = fmin(fmax((x[j] - grid.g0[j]) / grid.h[j], -1.0), grid.nb[j] + 1.0);
+    int bj = static_cast<int>(floor(t));
+    bj = max(0, min(grid.nb[j] - 1, bj));
+    b += bj * mult;
+    mult *= grid.nb[j];
+  }
+  int64_t best_cell = -1, found = -1;
+  double best_dist = 0.0, best_xh[DIM], found_xh[DIM];
+  {
+    for (int e = boff[b]; e < boff[b + 1] && found < 0; ++e) {
+      const int c = bcells[e];
+      bool in = true;
+      for (int j = 0; j < DIM; ++j) in = in && x[j] >= blo[(int64_t)c * DIM + j] && x[j] <= bhi[(int64_t)c * DIM + j];
+      if (!in) continue;
+      double X[NV][DIM];
+      for (int v = 0; v < NV; ++v)
+        for (int a = 0; a < DIM; ++a) X[v][a] = verts[cells[(int64_t)c * NV + v] * DIM + a];
+      double diam = 0.0;
+      for (int u = 0; u < NV; ++u)
+        for (int v = 0; v < NV; ++v) {
+          double s = 0.0;
+          for (int a = 0; a < DIM; ++a) s += (X[u][a] - X[v][a]) * (X[u][a] - X[v][a]);
+          diam = fmax(diam, sqrt(s));
+        }
+      double xh[DIM], rn;
+      const bool conv = invert_map<DIM>(X, x, 1e-12 * diam, xh, &rn);
+      if (!conv) continue;
+      bool inside = rn <= eps_geo;
+      for (int j = 0; j < DIM; ++j) inside = inside && xh[j] >= -eps_ref && xh[j] <= 1.0 + eps_ref;
+      if (inside) {
+        found = c;
+        for (int j = 0; j < DIM; ++j) found_xh[j] = fmin(fmax(xh[j], 0.0), 1.0);
+        break;
+      }
+      double xp[DIM], f[DIM], d[DIM];
+      for (int j = 0; j < DIM; ++j) xp[j] = fmin(fmax(xh[j], 0.0), 1.0);
+      forward_map<DIM>(X, xp, f);
+      for (int a = 0; a < DIM; ++a) d[a] = f[a] - x[a];
+      const double dist = norm<DIM>(d);
+      if (best_cell < 0 || dist < best_dist) {
+        best_cell = c;
+        best_dist = dist;
+        for (int j = 0; j < DIM; ++j) best_xh[j] = xp[j];
+      }
+    }
+  }
+  if (found >= 0) {
+    out_cell[p] = found;
+    for (int j = 0; j < DIM; ++j) out_xhat[p * DIM + j] = found_xh[j];
+    out_proj[p] = 0;
+  } else if (best_cell >= 0) {
+    out_cell[p] = best_cell;
+    for (int j = 0; j < DIM; ++j) out_xhat[p * DIM + j] = best_xh[j];
+    out_proj[p] = 1;
+  } else {
+    out_cell[p] = -1;
+    for (int j = 0; j < DIM; ++j) out_xhat[p * DIM + j] = nan("");
+    out_proj[p] = 0;
+    atomicAdd(n_missing, 1);
+    atomicMin(first_missing, static_cast<unsigned long long>(p));
+  }
+}
+
+LocateResult locate_points(int device, int dim, int64_t nv, const double* vertices, int64_t nc, const int64_t* cells,
+                           int64_t npts, const double* points, double eps_box, double eps_geo, double eps_ref,
+                           int64_t* out_cells, double* out_xhat, uint8_t* out_projected) {
+  NNMG_REQUIRE(dim == 2 || dim == 3, kInvalidArgument, "dim must be 2 or 3");
+  NNMG_REQUIRE(nc > 0, kInvalidArgument, "empty mesh");
+  NNMG_CUDA_TRY(cudaSetDevice(device));
+  LocateResult res;
+  if (npts == 0) return res;
+  const int NV = 1 << dim;
+  // padded boxes (geosearch.py:34-37)
+  std::vector<double> lo(size_t(nc) * dim), hi(size_t(nc) * dim);
+  double g0[3] = {INFINITY, INFINITY, INFINITY}, g1[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t c = 0; c < nc; ++c)
+    for (int j = 0; j < dim; ++j) {
+      double mn = INFINITY, mx = -INFINITY;
+      for (int v = 0; v < NV; ++v) {
+        const int64_t vi = cells[c * NV + v];
+        NNMG_REQUIRE(vi >= 0 && vi < nv, kInvalidArgument, "cell vertex index out of range");
+        mn = std::min(mn, vertices[vi * dim + j]);
+        mx = std::max(mx, vertices[vi * dim + j]);
+      }
+      lo[c * dim + j] = mn - eps_box;
+      hi[c * dim + j] = mx + eps_box;
+      g0[j] = std::min(g0[j], lo[c * dim + j]);
+      g1[j] = std::max(g1[j], hi[c * dim + j]);
+    }
+  BucketGrid grid{};
+  const double per_axis = std::pow(static_cast<double>(nc), 1.0 / dim);
+  int64_t nbt = 1;
+  for (int j = 0; j < 3; ++j) {
+    if (j < dim) {
+      grid.g0[j] = g0[j];
+      grid.nb[j] = std::max(1, static_cast<int>(std::lround(per_axis)));
+      grid.h[j] = (g1[j] - g0[j]) / grid.nb[j];
+      if (!(grid.h[j] > 0.0)) grid.h[j] = 1.0;
+    } else {
+      grid.g0[j] = 0.0;
+      grid.h[j] = 1.0;
+      grid.nb[j] = 1;
+    }
+    nbt *= grid.nb[j];
+  }
+  auto range = [&](int64_t c, int j, int& a, int& b) {
+    a = static_cast<int>(std::floor((lo[c * dim + j] - grid.g0[j]) / grid.h[j]));
+    b = static_cast<int>(std::floor((hi[c * dim + j] - grid.g0[j]) / grid.h[j]));
+    a = std::max(0, std::min(grid.nb[j] - 1, a));
+    b = std::max(0, std::min(grid.nb[j] - 1, b));
+  };
+  std::vector<int> boff(nbt + 1, 0);
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<int> fill;
+    std::vector<int> bc;
+    if (pass == 1) {
+      for (int64_t i = 0; i < nbt; ++i) boff[i + 1] += boff[i];
+      fill.assign(boff.begin(), boff.end() - 1);
+      bc.resize(boff[nbt]);
+    }
+    for (int64_t c = 0; c < nc; ++c) {
+      int a[3] = {0, 0, 0}, b[3] = {0, 0, 0};
+      for (int j = 0; j < dim; ++j) range(c, j, a[j], b[j]);
+      for (int k = a[2]; k <= b[2]; ++k)
+        for (int jj = a[1]; jj <= b[1]; ++jj)
+          for (int i = a[0]; i <= b[0]; ++i) {
+            const int64_t bk = i + grid.nb[0] * (jj + int64_t(grid.nb[1]) * k);
+            if (pass == 0)
+              boff[bk + 1] += 1;
+            else
+              bc[fill[bk]++] = static_cast<int>(c);
+          }
+    }
+    if (pass == 1) {
+      // cells were appended in ascending order: each bucket list is sorted
+      DevBuf<double> dv, dlo, dhi, dpts, dxh;
+      DevBuf<int64_t> dcells, dout;
+      DevBuf<int> dboff, dbc, dmiss;
+      DevBuf<uint8_t> dproj;
+      DevBuf<unsigned long long> dfirst;
+      dv.upload(vertices, size_t(nv) * dim);
+      dcells.upload(cells, size_t(nc) * NV);
+      dlo.upload(lo);
+      dhi.upload(hi);
+      dboff.upload(boff);
+      dbc.upload(bc);
+      dpts.upload(points, size_t(npts) * dim);
+      dout.alloc(npts);
+      dxh.alloc(size_t(npts) * dim);
+      dproj.alloc(npts);
+      dmiss.alloc(1);
+      dmiss.zero();
+      unsigned long long init = ~0ull;
+      dfirst.upload(&init, 1);
+      const int bs = 128;
+      if (dim == 2)
+        k_locate<2><<<grid_for(npts, bs), bs>>>(dv.ptr, dcells.ptr, dlo.ptr, dhi.ptr, dboff.ptr, dbc.ptr, grid,
+                                                 dpts.ptr, npts, eps_geo, eps_ref, dout.ptr, dxh.ptr, dproj.ptr,
+                                                 dmiss.ptr, dfirst.ptr);
+      else
+        k_locate<3><<<grid_for(npts, bs), bs>>>(dv.ptr, dcells.ptr, dlo.ptr, dhi.ptr, dboff.ptr, dbc.ptr, grid,
+                                                 dpts.ptr, npts, eps_geo, eps_ref, dout.ptr, dxh.ptr, dproj.ptr,
+                                                 dmiss.ptr, dfirst.ptr);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+      NNMG_CUDA_TRY(cudaMemcpy(out_cells, dout.ptr, sizeof(int64_t) * npts, cudaMemcpyDeviceToHost));
+      NNMG_CUDA_TRY(cudaMemcpy(out_xhat, dxh.ptr, sizeof(double) * npts * dim, cudaMemcpyDeviceToHost));
+      NNMG_CUDA_TRY(cudaMemcpy(out_projected, dproj.ptr, npts, cudaMemcpyDeviceToHost));
+      unsigned long long fm = 0;
+      NNMG_CUDA_TRY(cudaMemcpy(&res.n_missing, dmiss.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+      NNMG_CUDA_TRY(cudaMemcpy(&fm, dfirst.ptr, sizeof(fm), cudaMemcpyDeviceToHost));
+      res.first_missing = res.n_missing ? static_cast<int64_t>(fm) : -1;
+    }
+  }
+  return res;
+}
+
+}  // namespace nnmg

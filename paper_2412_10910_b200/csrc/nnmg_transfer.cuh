@@ -1,0 +1,43 @@
+// Non-nested transfer handle (replaces TwoLevelTransferNonNested,
+// transfer.py:61-124) and the GPU point location that builds its records
+// (replaces geosearch.locate_points, geosearch.py:163-227).
+#pragma once
+
+#include "nnmg_level.cuh"
+
+namespace nnmg {
+
+struct Transfer {
+  Level* coarse = nullptr;
+  Level* fine = nullptr;
+  int dim = 0, pc = 0, ncomp = 1;
+  int64_t npts = 0, ncc = 0;
+  DevBuf<int> cell_start;   // [ncc+1] CSR of points by owning coarse cell
+  DevBuf<int> pt_dof;       // [npts] fine scalar DoF (sorted by cell, then point order)
+  DevBuf<double> xhat;      // [npts][dim]
+  DevBuf<double> cellbuf;   // [ncc][nloc][ncomp] restriction partial local vectors
+  DevBuf<int> t_off, t_ent; // coarse DoF -> (cell*nloc + l) entries, fixed order
+};
+
+Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_t* point_dofs, const int64_t* cells,
+                          const double* xhat);
+// u_f = P u_c (accumulate: u_f += P u_c) with symmetric constraint masking (transfer.py:31-44, 87-102)
+void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s);
+// r_c = P^T r_f, deterministic two-phase segmented reduction (transfer.py:46-58, 104-124)
+void transfer_restrict(Transfer& T, const double* rf, double* rc, cudaStream_t s);
+
+struct LocateResult {
+  int n_missing = 0;       // points with no candidate / no converged candidate
+  int64_t first_missing = -1;
+};
+
+// GPU point location with the reference's semantics: candidates = cells whose
+// eps_box-padded bounding box contains the point; damped Newton inversion
+// (mesh.py:235-287); first containing candidate in ascending cell order wins;
+// otherwise the converged candidate whose clamped image is nearest (ties to the
+// lowest cell) and the point is flagged projected.
+LocateResult locate_points(int device, int dim, int64_t nv, const double* vertices, int64_t nc, const int64_t* cells,
+                           int64_t npts, const double* points, double eps_box, double eps_geo, double eps_ref,
+                           int64_t* out_cells, double* out_xhat, uint8_t* out_projected);
+
+}  // namespace nnmg

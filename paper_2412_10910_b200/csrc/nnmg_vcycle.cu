@@ -1,0 +1,155 @@
+// Chebyshev-Jacobi smoother sweep and the V-cycle executor
+// (replaces ChebyshevJacobi._sweep, solvers.py:88-108, and
+// MultigridHierarchy._v, multigrid.py:83-113), optionally replayed as one
+// CUDA graph so a whole cycle costs one launch.
+#include "nnmg_vcycle.cuh"
+#include "nnmg_vector.cuh"
+
+#include <algorithm>
+
+namespace nnmg {
+
+void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const double* b, const double* x0,
+                    double* x, double* work, cudaStream_t s) {
+  NNMG_REQUIRE(L.diag_ready, kInvalidArgument, "level diagonal not computed");
+  const int64_t n = L.n_dofs;
+  double* r = work;
+  double* d = work + n;
+  double* t = work + 2 * n;
+  const double theta = (lam_max + lam_min) / 2.0;
+  const double delta = (lam_max - lam_min) / 2.0;
+  const double sigma = theta / delta;
+  if (x0 == nullptr) {
+    cheb_start(n, b, nullptr, nullptr, L.inv_diag.ptr, theta, r, d, x, s);
+  } else {
+    level_apply(L, x0, t, s);
+    cheb_start(n, b, t, x0, L.inv_diag.ptr, theta, r, d, x, s);
+  }
+  double rho_old = 1.0 / sigma;
+  for (int k = 0; k < degree - 1; ++k) {
+    level_apply(L, d, t, s);
+    const double rho = 1.0 / (2.0 * sigma - rho_old);
+    cheb_step(n, t, L.inv_diag.ptr, rho * rho_old, 2.0 * rho / delta, r, d, x, s);
+    rho_old = rho;
+  }
+}
+
+VCycle::~VCycle() {
+  for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+}
+
+VCycle* vcycle_create(int n_levels, Level* const* levels, Transfer* const* transfers, Coarse* coarse,
+                      const double* lam_max, const double* lam_min, const int* degree, int m1, int m2) {
+  NNMG_REQUIRE(n_levels >= 1, kInvalidArgument, "need at least one level");
+  NNMG_REQUIRE(coarse && coarse->level == levels[0], kInvalidArgument, "coarse solver must own level 0");
+  auto V = new VCycle();
+  try {
+    V->m1 = m1;
+    V->m2 = m2;
+    for (int l = 0; l < n_levels; ++l) {
+      NNMG_REQUIRE(levels[l] != nullptr, kInvalidArgument, "null level");
+      V->levels.push_back(levels[l]);
+      V->lam_max.push_back(lam_max[l]);
+      V->lam_min.push_back(lam_min[l]);
+      V->degree.push_back(degree[l]);
+      if (l > 0) {
+        Transfer* T = transfers[l - 1];
+        NNMG_REQUIRE(T && T->coarse == levels[l - 1] && T->fine == levels[l], kInvalidArgument,
+                     "transfer " + std::to_string(l - 1) + " does not connect levels " + std::to_string(l - 1) +
+                         " and " + std::to_string(l));
+        NNMG_REQUIRE(levels[l]->diag_ready, kInvalidArgument, "level diagonal not computed");
+        V->transfers.push_back(T);
+      }
+    }
+    V->coarse = coarse;
+    V->f.resize(n_levels);
+    V->x.resize(n_levels);
+    V->r.resize(n_levels);
+    V->work.resize(n_levels);
+    for (int l = 0; l < n_levels; ++l) {
+      const int64_t n = levels[l]->n_dofs;
+      if (l < n_levels - 1) {
+        V->f[l].alloc(n);
+        V->x[l].alloc(n);
+      }
+      V->r[l].alloc(n);
+      V->work[l].alloc(3 * n);
+    }
+  } catch (...) {
+    delete V;
+    throw;
+  }
+  return V;
+}
+
+static void cycle(VCycle& V, int l, const double* f, double* x, cudaStream_t s) {
+  if (l == 0) {
+    coarse_solve(*V.coarse, f, x, s);
+    return;
+  }
+  Level& L = *V.levels[l];
+  Transfer& T = *V.transfers[l - 1];
+  double* w = V.work[l].ptr;
+  for (int k = 0; k < V.m1; ++k)
+    smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, k == 0 ? nullptr : x, x, w, s);
+  if (V.m1 == 0) NNMG_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * L.n_dofs, s));
+  double* r = V.r[l].ptr;
+  level_apply(L, x, r, s);
+  sub(L.n_dofs, f, r, r, s);
+  transfer_restrict(T, r, V.f[l - 1].ptr, s);
+  cycle(V, l - 1, V.f[l - 1].ptr, V.x[l - 1].ptr, s);
+  transfer_prolongate(T, V.x[l - 1].ptr, x, true, s);
+  for (int k = 0; k < V.m2; ++k) smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s);
+}
+
+void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s) {
+  const int top = static_cast<int>(V.levels.size()) - 1;
+  if (!V.use_graph) {
+    cycle(V, top, f, x, s);
+    return;
+  }
+  NNMG_REQUIRE(s != nullptr, kInvalidArgument, "graph replay needs a non-default stream");
+  V.clock += 1;
+  VCycle::Graph* hit = nullptr;
+  for (auto& g : V.graphs)
+    if (g.f == f && g.x == x && g.s == s) hit = &g;
+  if (!hit) {
+    constexpr size_t kMaxGraphs = 4;
+    if (V.graphs.size() >= kMaxGraphs) {
+      auto oldest = std::min_element(V.graphs.begin(), V.graphs.end(),
+                                     [](const VCycle::Graph& a, const VCycle::Graph& b) { return a.last_use < b.last_use; });
+      cudaGraphExecDestroy(oldest->exec);
+      V.graphs.erase(oldest);
+    }
+    cudaGraph_t g = nullptr;
+    const uint64_t c0 = launch_count();
+    NNMG_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      cycle(V, top, f, x, s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    NNMG_CUDA_TRY(cudaStreamEndCapture(s, &g));
+    V.kernels_per_cycle = static_cast<int64_t>(launch_count() - c0);
+    // capture records launches without executing them
+    count_launch(-static_cast<int>(V.kernels_per_cycle));
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    NNMG_CUDA_TRY(e);
+    V.graphs.push_back(VCycle::Graph{f, x, s, exec, 0});
+    hit = &V.graphs.back();
+  }
+  hit->last_use = V.clock;
+  NNMG_CUDA_TRY(cudaGraphLaunch(hit->exec, s));
+  count_launch(static_cast<int>(V.kernels_per_cycle));
+}
+
+int64_t vcycle_kernels(VCycle& V) {
+  if (V.kernels_per_cycle > 0) return V.kernels_per_cycle;
+  return -1;
+}
+
+}  // namespace nnmg

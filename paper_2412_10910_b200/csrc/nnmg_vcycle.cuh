@@ -1,0 +1,42 @@
+#pragma once
+
+#include "nnmg_coarse.cuh"
+#include "nnmg_level.cuh"
+#include "nnmg_transfer.cuh"
+
+#include <memory>
+
+namespace nnmg {
+
+void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const double* b, const double* x0,
+                    double* x, double* work, cudaStream_t s);
+
+struct VCycle {
+  std::vector<Level*> levels;        // coarsest first
+  std::vector<Transfer*> transfers;  // transfers[l-1] connects l-1 -> l
+  Coarse* coarse = nullptr;
+  std::vector<double> lam_max, lam_min;
+  std::vector<int> degree;
+  int m1 = 1, m2 = 1;
+  // per level: right-hand side and correction (coarse levels), residual, smoother work
+  std::vector<DevBuf<double>> f, x, r, work;
+  bool use_graph = false;
+  struct Graph {
+    const double* f;
+    double* x;
+    cudaStream_t s;
+    cudaGraphExec_t exec;
+    uint64_t last_use;
+  };
+  std::vector<Graph> graphs;  // small LRU keyed by (f, x, stream)
+  uint64_t clock = 0;
+  int64_t kernels_per_cycle = 0;
+  ~VCycle();
+};
+
+VCycle* vcycle_create(int n_levels, Level* const* levels, Transfer* const* transfers, Coarse* coarse,
+                      const double* lam_max, const double* lam_min, const int* degree, int m1, int m2);
+void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s);
+int64_t vcycle_kernels(VCycle& V);
+
+}  // namespace nnmg

@@ -1,0 +1,169 @@
+// K5/K8 vector kernels: fused Chebyshev-Jacobi updates (solvers.py:88-108),
+// CG updates (solvers.py:129-164) and deterministic two-stage dot products.
+#include "nnmg_vector.cuh"
+
+namespace nnmg {
+
+static constexpr int kBS = 256;
+static inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBS - 1) / kBS); }
+
+// r = b - Ax (or b); d = inv_diag*r/theta; x = x0 + d (or d)       (solvers.py:94-100)
+__global__ void k_cheb_start(int64_t n, const double* __restrict__ b, const double* __restrict__ ax,
+                             const double* __restrict__ x0, const double* __restrict__ inv_diag, double theta,
+                             double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double ri = ax ? b[i] - ax[i] : b[i];
+  const double di = inv_diag[i] * ri / theta;
+  r[i] = ri;
+  d[i] = di;
+  x[i] = x0 ? x0[i] + di : di;
+}
+
+// r -= Ad; z = inv_diag r; d = c1 d + c2 z; x += d                 (solvers.py:101-107)
+__global__ void k_cheb_step(int64_t n, const double* __restrict__ ad, const double* __restrict__ inv_diag,
+                            double c1, double c2, double* __restrict__ r, double* __restrict__ d,
+                            double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double ri = r[i] - ad[i];
+  const double z = inv_diag[i] * ri;
+  const double di = c1 * d[i] + c2 * z;
+  r[i] = ri;
+  d[i] = di;
+  x[i] += di;
+}
+
+// y = alpha*x + beta*y  (general axpby; beta==0 ignores y's content)
+__global__ void k_axpby(int64_t n, double alpha, const double* __restrict__ x, double beta, double* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  y[i] = beta == 0.0 ? alpha * x[i] : alpha * x[i] + beta * y[i];
+}
+
+// out = a - b
+__global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] - b[i];
+}
+
+// out = a * b
+__global__ void k_mul(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] * b[i];
+}
+
+// x += alpha p; r -= alpha ap                                      (solvers.py:153-154)
+__global__ void k_cg_update(int64_t n, double alpha, const double* __restrict__ p, const double* __restrict__ ap,
+                            double* __restrict__ x, double* __restrict__ r) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  x[i] = x[i] + alpha * p[i];
+  r[i] = r[i] - alpha * ap[i];
+}
+
+// ---------------------------------------------------------------------------
+// deterministic dots: fixed grid, fixed per-thread order, fixed tree.
+// ---------------------------------------------------------------------------
+static constexpr int kDotBlocks = 296;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+  __syncthreads();
+  return s;
+}
+
+__global__ void k_dot_partial(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                              const double* __restrict__ c, const double* __restrict__ d, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    s0 += a[i] * b[i];
+    if (c) s1 += c[i] * d[i];
+  }
+  s0 = block_sum(s0, sh);
+  s1 = c ? block_sum(s1, sh) : 0.0;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s0;
+    part[gridDim.x + blockIdx.x] = s1;
+  }
+}
+
+__global__ void k_dot_final(const double* __restrict__ part, int nb, double* __restrict__ out, int two) {
+  __shared__ double sh[32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    s0 += part[i];
+    s1 += part[nb + i];
+  }
+  s0 = block_sum(s0, sh);
+  s1 = two ? block_sum(s1, sh) : 0.0;
+  if (threadIdx.x == 0) {
+    out[0] = s0;
+    if (two) out[1] = s1;
+  }
+}
+
+size_t dot_workspace_doubles() { return 2 * kDotBlocks; }
+
+void dot2(int64_t n, const double* a, const double* b, const double* c, const double* d, double* out,
+          double* work, cudaStream_t s) {
+  k_dot_partial<<<kDotBlocks, kBS, 0, s>>>(n, a, b, c, d, work);
+  NNMG_CHECK_LAUNCH();
+  k_dot_final<<<1, kBS, 0, s>>>(work, kDotBlocks, out, c ? 1 : 0);
+  NNMG_CHECK_LAUNCH();
+  count_launch(2);
+}
+
+void cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag, double theta,
+                double* r, double* d, double* x, cudaStream_t s) {
+  if (!n) return;
+  k_cheb_start<<<grid_for(n), kBS, 0, s>>>(n, b, ax, x0, inv_diag, theta, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
+               double* x, cudaStream_t s) {
+  if (!n) return;
+  k_cheb_step<<<grid_for(n), kBS, 0, s>>>(n, ad, inv_diag, c1, c2, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void axpby(int64_t n, double alpha, const double* x, double beta, double* y, cudaStream_t s) {
+  if (!n) return;
+  k_axpby<<<grid_for(n), kBS, 0, s>>>(n, alpha, x, beta, y);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void sub(int64_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+  if (!n) return;
+  k_sub<<<grid_for(n), kBS, 0, s>>>(n, a, b, out);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void mul(int64_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+  if (!n) return;
+  k_mul<<<grid_for(n), kBS, 0, s>>>(n, a, b, out);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void cg_update(int64_t n, double alpha, const double* p, const double* ap, double* x, double* r, cudaStream_t s) {
+  if (!n) return;
+  k_cg_update<<<grid_for(n), kBS, 0, s>>>(n, alpha, p, ap, x, r);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+}  // namespace nnmg

@@ -1,0 +1,20 @@
+#pragma once
+
+#include "nnmg_common.cuh"
+
+namespace nnmg {
+
+size_t dot_workspace_doubles();
+// out[0] = a.b, out[1] = c.d (if c != nullptr); deterministic; out on device
+void dot2(int64_t n, const double* a, const double* b, const double* c, const double* d, double* out, double* work,
+          cudaStream_t s);
+void cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag, double theta,
+                double* r, double* d, double* x, cudaStream_t s);
+void cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
+               double* x, cudaStream_t s);
+void axpby(int64_t n, double alpha, const double* x, double beta, double* y, cudaStream_t s);
+void sub(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
+void mul(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
+void cg_update(int64_t n, double alpha, const double* p, const double* ap, double* x, double* r, cudaStream_t s);
+
+}  // namespace nnmg
