@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 V-cycle GDoF/s (BASELINE.json metric) on a BASELINE config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A step is one V-cycle ``H.precondition(r)`` (Alg. 1: Chebyshev-Jacobi pre/post
+smoothing, residual, non-nested restriction/prolongation, device-resident
+coarse CG) on the finest level of the configuration.  ``value`` = fine DoFs x
+steps / device time with the input resident in HBM (replayed CUDA graph);
+``e2e`` = the same through the public call with pinned-host input, H2D + cycle
++ D2H inside the timed region.  The roofline object describes the dominant
+kernel (the fine-level matrix-free apply) measured live with CUDA events on
+its stream.  ``--impl reference`` times the CPU port of the reference's path
+(oracle/, NumPy) on a bounded sample of the same configuration.
+
+Multi-GPU (torchrun): every rank runs the same per-GPU problem (replicated
+cycles, weak scaling) until the cell-partitioned path lands; timing is the
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_TEXT = {
+    "C1": "2D Poisson Q1, 128^2/45^2/17^2 jittered +-0.25h, Chebyshev 4",
+    "C2": "2D Poisson Q2, 512^2/181^2/64^2 jittered +-0.2h, Chebyshev 4",
+    "C3": "3D Poisson Q2 hex, 128^3/47^3/17^3 jittered +-0.2h, Chebyshev 4",
+    "C4": "3D Poisson Q4 curved, 64^3/23^3/8^3 jittered +-0.15h, Chebyshev 4",
+    "C5": "3D elasticity vector Q2 beam, 256x32^2/93x12^2/33x4^2 jittered +-0.2h, Chebyshev 5",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--scale", type=int, default=1, help="divide cells per axis (1 = full config)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-scale", type=int, default=5, help="sample scale for the CPU baseline")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solve", action="store_true", help="also run the full PCG solve and report it")
+    ap.add_argument("--profile", action="store_true", help="profiler range around one cycle + hot kernels, then exit")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------------------
+# algorithmic byte / flop model
+# ---------------------------------------------------------------------------
+def vmult_bytes(dim, p, ncomp, n_dofs, n_cells, physics):
+    nloc = (p + 1) ** dim
+    g = dim * (dim + 1) // 2 if physics == "poisson" else dim * dim + 1
+    return 16 * n_dofs + 4 * n_cells * nloc + 8 * n_cells * nloc * g
+
+
+def transfer_bytes(dim, p, ncomp, npts, n_dofs_coarse, n_cells_coarse):
+    nloc = (p + 1) ** dim
+    return npts * (4 + 4 + 8 * dim + 8 * ncomp) + 8 * n_dofs_coarse + 4 * n_cells_coarse * nloc
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_from_profiles(kernel_key):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh).get(kernel_key)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"nnmg_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f == "Active"})
+        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": rows[0][1], "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (NumPy port of the reference path) on a sample
+# ---------------------------------------------------------------------------
+def cpu_vcycle_rate(cfg, scale, seconds, steps=None):
+    from oracle import nnmg_oracle as O
+
+    meshes = [O.jittered_mesh(cfg.level_grid(l, scale), cfg.extent, cfg.amplitude, 1000 * cfg.index + l + 1,
+                              cfg.warp) for l in range(len(cfg.levels))]
+    H, spaces = O.build_hierarchy(meshes, cfg.degree, cfg.problem, cfg.dirichlet_ids, cfg.lame or (1.0, 1.0),
+                                  cfg.chebyshev_degree)
+    b = O.assemble_rhs_const(spaces[-1], cfg.body_force if cfg.body_force else 1.0)
+    H.precondition(b)  # warm-up
+    n = spaces[-1].n_dofs
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        H.precondition(b)
+        k += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and k >= steps) or (steps is None and el >= seconds):
+            break
+    return n * k / el / 1e9, n, k, el
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    rate, n, k, el = cpu_vcycle_rate(cfg, args.cpu_scale, args.cpu_seconds, steps=max(1, args.steps))
+    sample = (f"{cfg.name} at 1/{args.cpu_scale} cells per axis ({n} fine DoFs), {k} V-cycles, "
+              f"NumPy oracle port of nnmg")
+    line = {
+        "impl": "reference", "metric": "fp64 V-cycle GDoF/s", "value": rate, "unit": "GDoF/s", "n_gpus": 0,
+        "steps": k, "warmup": 1, "ms_per_step": el / k * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8(d) meshes)",
+        "config": {"workload": CONFIG_TEXT[cfg.name] + f" (CPU sample 1/{args.cpu_scale})", "config": cfg.name},
+        "cpu_baseline": {"value": rate, "unit": "GDoF/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2412_10910_b200 import _lib
+    from paper_2412_10910_b200 import multigrid, solvers
+
+    t_setup = time.perf_counter()
+    meshes = cfg.make_meshes(scale=args.scale, validate=False)
+    H = multigrid.build_hp_hierarchy(meshes, cfg.degree, problem=cfg.problem, dirichlet_ids=cfg.dirichlet_ids,
+                                     lame=cfg.lame, config=multigrid.HierarchyConfig(
+                                         chebyshev_degree=cfg.chebyshev_degree), device=dev)
+    fine = H.finest.operator
+    b = fine.load_vector(cfg.body_force if cfg.body_force else 1.0)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    n = fine.n_dofs
+    stream = torch.cuda.Stream(device=dev)
+    z = torch.empty_like(b)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # warm-up (captures the CUDA graph)
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            H.v_cycle_into(b, z)
+    stream.synchronize()
+
+    if args.profile:
+        # profiler range for `ncu --profile-from-start off`: one V-cycle
+        # (graph), then one isolated fine apply / prolongate / restrict
+        u = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).to(dev)
+        v = torch.empty_like(u)
+        T = H.transfers[-1]
+        rc = torch.empty(T.coarse_space.n_dofs, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        with torch.cuda.stream(stream):
+            H.v_cycle_into(b, z)
+            fine.apply_into(u, v)
+            T.prolongate_into(rc, v)
+            T.restrict_into(u, rc)
+        stream.synchronize()
+        torch.cuda.profiler.stop()
+        if rank == 0:
+            print(json.dumps({"profile": True, "config": cfg.name, "kernels_per_cycle": H.kernels_per_cycle()}))
+        return
+
+    # ---- timed region: K V-cycles from HBM-resident input (> L2) ----
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                H.v_cycle_into(b, z)
+            e1.record(stream)
+        stream.synchronize()
+    launches = _lib.launch_count() - launches0
+    barrier()
+    t_dev = e0.elapsed_time(e1) * 1e-3
+    t_max = t_dev
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([t_dev], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = world * n * args.steps / t_max / 1e9
+
+    # ---- e2e: pinned host r -> device -> V-cycle -> pinned host z ----
+    hb = b.cpu().pin_memory()
+    hz = torch.empty_like(hb).pin_memory()
+    bin_ = torch.empty_like(b)
+    with torch.cuda.stream(stream):
+        bin_.copy_(hb, non_blocking=True)
+        H.v_cycle_into(bin_, z)
+        hz.copy_(z, non_blocking=True)
+    stream.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            bin_.copy_(hb, non_blocking=True)
+            H.v_cycle_into(bin_, z)
+            hz.copy_(z, non_blocking=True)
+        e1.record(stream)
+    stream.synchronize()
+    t_e2e = e0.elapsed_time(e1) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e = world * n * args.steps / t_e2e / 1e9
+
+    # ---- dominant kernel: fine-level apply, CUDA events on its stream ----
+    u = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).to(dev)
+    v = torch.empty_like(u)
+    reps = 20
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            fine.apply_into(u, v)
+        e0.record(stream)
+        for _ in range(reps):
+            fine.apply_into(u, v)
+        e1.record(stream)
+    stream.synchronize()
+    t_apply = e0.elapsed_time(e1) * 1e-3 / reps
+    info = fine.info()
+    sp = H.finest.space
+    ncomp = sp.n_components
+    B = vmult_bytes(sp.mesh.dim, sp.degree, ncomp, n, sp.mesh.n_cells, cfg.problem)
+    peak, peak_kind = measured_peaks()
+    achieved = B / t_apply / 1e9
+    # transfers (fine pair)
+    T = H.transfers[-1]
+    uc = torch.from_numpy(np.random.default_rng(0).standard_normal(T.coarse_space.n_dofs)).to(dev)
+    rc = torch.empty_like(uc)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            T.prolongate_into(uc, v)
+            T.restrict_into(u, rc)
+        e0.record(stream)
+        for _ in range(reps):
+            T.prolongate_into(uc, v)
+        e1.record(stream)
+        e2 = torch.cuda.Event(enable_timing=True)
+        for _ in range(reps):
+            T.restrict_into(u, rc)
+        e2.record(stream)
+    stream.synchronize()
+    t_pro = e0.elapsed_time(e1) * 1e-3 / reps
+    t_res = e1.elapsed_time(e2) * 1e-3 / reps
+    cm = T.coarse_space.mesh
+    BT = transfer_bytes(sp.mesh.dim, T.coarse_space.degree, ncomp, len(T.cells), T.coarse_space.n_dofs, cm.n_cells)
+    applies_per_cycle = 2 * cfg.chebyshev_degree + 1
+
+    # ---- optional full solve ----
+    solve = None
+    if args.solve:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = solvers.cg_solve(fine, b, precond=H.precondition, target_reduction=1e-8)
+        torch.cuda.synchronize()
+        solve = {"iterations": res.iterations, "converged": res.converged, "seconds": time.perf_counter() - t0,
+                 "final_rel_residual": res.residual_norms[-1] / res.residual_norms[0]}
+    cit, cconv, _ = H.coarse_solver.status() if not H.coarse_solver.dense else (None, None, None)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, ncpu, k, el = cpu_vcycle_rate(cfg, args.cpu_scale, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "GDoF/s", "cores": 1, "kind": "port",
+               "sample": f"{cfg.name} at 1/{args.cpu_scale} cells per axis ({ncpu} fine DoFs), {k} V-cycles in "
+                         f"{el:.1f} s, NumPy oracle port of nnmg, {os.cpu_count()} host cores available"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "fp64 V-cycle GDoF/s", "value": value, "unit": "GDoF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SURVEY §8(d) jittered meshes, f=1 load vector)",
+            "config": {"workload": CONFIG_TEXT[cfg.name] + ("" if args.scale == 1 else f" at 1/{args.scale}"),
+                       "config": cfg.name, "fine_dofs": n, "levels_dofs": [lev.operator.n_dofs for lev in H.levels],
+                       "l2": "inputs larger than L2 (each fine apply streams >1 GB)",
+                       "parallelism": "single GPU" if world == 1 else f"replicated x{world}",
+                       "graph": True, "setup_s": round(setup_s, 2),
+                       "coarse_cg_iterations": cit, "coarse_solver": H.coarse_solver.info()},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(f"{cfg.name}_apply"),
+                         "kernel": "k_apply (fine-level matrix-free vmult)", "bytes_per_launch": B,
+                         "avg_launch_ms": t_apply * 1e3, "peak_kind": peak_kind,
+                         "share_of_step": applies_per_cycle * t_apply / (t_max / args.steps)},
+            "kernels": {
+                "vmult_gdofs": n / t_apply / 1e9, "vmult_frac": achieved / peak,
+                "prolongate_ms": t_pro * 1e3, "prolongate_frac": BT / t_pro / 1e9 / peak,
+                "restrict_ms": t_res * 1e3, "restrict_frac": BT / t_res / 1e9 / peak,
+                "transfer_bytes": BT, "geometry_bytes": info["geometry_bytes"],
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if solve is not None:
+            line["solve"] = solve
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_2412_10910_b200.configs import get_config
+
+    cfg = get_config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

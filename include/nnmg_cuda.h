@@ -77,6 +77,10 @@ int nnmg_level_residual(nnmg_level_t level, const double* f_dev, const double* x
 int nnmg_level_compute_diagonal(nnmg_level_t level, void* stream);
 int nnmg_level_diagonal(nnmg_level_t level, double* diag_dev, void* stream);
 
+/* b_dev = (f, phi_i) for a constant body load f_host[n_components],
+ * constrained entries 0 (body-load part of assemble_rhs, mfoperator.py:313-355) */
+int nnmg_level_load_vector(nnmg_level_t level, const double* f_host, double* b_dev, void* stream);
+
 /* ---- Chebyshev-Jacobi smoother: replaces ChebyshevJacobi._sweep / smooth
  * (solvers.py:88-114).  One degree-k pass; x0_dev may be NULL (zero initial
  * guess).  work_dev: 3 * n_dofs doubles of scratch. */

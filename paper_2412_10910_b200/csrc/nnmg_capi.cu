@@ -108,6 +108,14 @@ int nnmg_level_diagonal(nnmg_level_t level, double* diag_dev, void* stream) {
   });
 }
 
+int nnmg_level_load_vector(nnmg_level_t level, const double* f_host, double* b_dev, void* stream) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    NNMG_REQUIRE(f_host && b_dev, kInvalidArgument, "null argument");
+    level_load_vector(*LV(level), f_host, b_dev, S(stream));
+  });
+}
+
 int nnmg_smoother_sweep(nnmg_level_t level, double lam_max, double lam_min, int degree, const double* b_dev,
                         const double* x0_dev, double* x_dev, double* work_dev, void* stream) {
   return guard([&] {

@@ -13,7 +13,7 @@ namespace nnmg {
 // J[a][b] = sum_v dW_v/dxhat_b(q) X_v[a]   (mesh.py:138-143)
 // ---------------------------------------------------------------------------
 template <int DIM, int PHYS>
-__global__ void k_geometry(const double* __restrict__ verts, const int64_t* __restrict__ cells,
+__global__ void k_geometry(const double* __restrict__ verts, const int* __restrict__ cells,
                            int64_t n_cells, int nq1, Tables tab, int cb, double* __restrict__ geo,
                            int* __restrict__ bad) {
   constexpr int NV = 1 << DIM;
@@ -31,7 +31,7 @@ __global__ void k_geometry(const double* __restrict__ verts, const int64_t* __re
   }
   double J[DIM][DIM] = {};
   for (int v = 0; v < NV; ++v) {
-    const double* X = verts + cells[c * NV + v] * DIM;
+    const double* X = verts + (int64_t)cells[c * NV + v] * DIM;
     for (int b = 0; b < DIM; ++b) {
       double gr = 1.0;
       for (int j = 0; j < DIM; ++j) {
@@ -149,6 +149,54 @@ __global__ void k_diagonal(Tables tab, const int* __restrict__ idx, const double
   for (int a = 0; a < NCOMP; ++a) atomicAdd(diag + (int64_t)g * NCOMP + a, acc[a]);
 }
 
+// body load: thread per (cell, local DoF), b_l = sum_q det(J(q)) w_q prod_k S[q_k][l_k]
+template <int DIM>
+__global__ void k_load_vector(const double* __restrict__ verts, const int* __restrict__ cells, int64_t n_cells,
+                              int n1, int cb, const int* __restrict__ idx, Tables tab, int ncomp, double f0,
+                              double f1, double f2, double* __restrict__ b) {
+  constexpr int NV = 1 << DIM;
+  const int nloc = DIM == 2 ? n1 * n1 : n1 * n1 * n1;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_cells * nloc) return;
+  const int64_t c = t / nloc;
+  const int l = static_cast<int>(t % nloc);
+  const int g = idx[((c / cb) * nloc + l) * cb + c % cb];
+  if (g < 0) return;
+  const int li[3] = {l % n1, (l / n1) % n1, l / (n1 * n1)};
+  double X[NV][DIM];
+  for (int v = 0; v < NV; ++v)
+    for (int a = 0; a < DIM; ++a) X[v][a] = verts[(int64_t)cells[c * NV + v] * DIM + a];
+  double acc = 0.0;
+  for (int q = 0; q < nloc; ++q) {
+    const int qi[3] = {q % n1, (q / n1) % n1, q / (n1 * n1)};
+    double J[DIM][DIM] = {};
+    double phi = 1.0, wq = 1.0;
+    for (int j = 0; j < DIM; ++j) {
+      phi *= tab.S[qi[j]][li[j]];
+      wq *= tab.w[qi[j]];
+    }
+    for (int v = 0; v < NV; ++v)
+      for (int bb = 0; bb < DIM; ++bb) {
+        double gr = 1.0;
+        for (int j = 0; j < DIM; ++j) {
+          const int bit = (v >> j) & 1;
+          gr *= (j == bb) ? (bit ? 1.0 : -1.0) : (bit ? tab.xq[qi[j]] : 1.0 - tab.xq[qi[j]]);
+        }
+        for (int a = 0; a < DIM; ++a) J[a][bb] += gr * X[v][a];
+      }
+    double det;
+    if constexpr (DIM == 2)
+      det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    else
+      det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+    acc += det * wq * phi;
+  }
+  const double f[3] = {f0, f1, f2};
+  for (int a = 0; a < ncomp; ++a)
+    if (f[a] != 0.0) atomicAdd(b + (int64_t)g * ncomp + a, f[a] * acc);
+}
+
 __global__ void k_copy_constrained(const int* __restrict__ cd, int64_t n, const double* __restrict__ src,
                                    double* __restrict__ dst) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -244,12 +292,18 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     }
     L->idx.upload(idx);
     // geometry on the device from vertex coordinates
-    DevBuf<double> dverts;
-    DevBuf<int64_t> dcells;
-    dverts.upload(vertices, size_t(n_vertices) * dim);
-    for (int64_t i = 0; i < n_cells * (int64_t(1) << dim); ++i)
-      NNMG_REQUIRE(cells[i] >= 0 && cells[i] < n_vertices, kInvalidArgument, "cell vertex index out of range");
-    dcells.upload(cells, size_t(n_cells) << dim);
+    NNMG_REQUIRE(n_vertices < (int64_t(1) << 31), kUnsupported, "more than 2^31 vertices");
+    L->verts.upload(vertices, size_t(n_vertices) * dim);
+    {
+      std::vector<int> vc(size_t(n_cells) << dim);
+      for (size_t i = 0; i < vc.size(); ++i) {
+        NNMG_REQUIRE(cells[i] >= 0 && cells[i] < n_vertices, kInvalidArgument, "cell vertex index out of range");
+        vc[i] = static_cast<int>(cells[i]);
+      }
+      L->vcells.upload(vc);
+    }
+    const double* dverts = L->verts.ptr;
+    const int* dcells = L->vcells.ptr;
     L->geo.alloc(size_t(L->nblk) * L->nq * L->ng * cb);
     L->geo.zero();
     DevBuf<int> bad;
@@ -258,13 +312,13 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     const int64_t nt = n_cells * L->nq;
     const int bs = 256;
     if (dim == 2 && physics == kLaplace)
-      k_geometry<2, kLaplace><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+      k_geometry<2, kLaplace><<<grid_for(nt, bs), bs>>>(dverts, dcells, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
     else if (dim == 2)
-      k_geometry<2, kElasticity><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+      k_geometry<2, kElasticity><<<grid_for(nt, bs), bs>>>(dverts, dcells, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
     else if (physics == kLaplace)
-      k_geometry<3, kLaplace><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+      k_geometry<3, kLaplace><<<grid_for(nt, bs), bs>>>(dverts, dcells, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
     else
-      k_geometry<3, kElasticity><<<grid_for(nt, bs), bs>>>(dverts.ptr, dcells.ptr, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
+      k_geometry<3, kElasticity><<<grid_for(nt, bs), bs>>>(dverts, dcells, n_cells, L->n1, L->tab, cb, L->geo.ptr, bad.ptr);
     NNMG_CHECK_LAUNCH();
     count_launch();
     int hbad = 0;
@@ -314,6 +368,20 @@ void launch_copy_constrained(const Level& L, const double* src, double* dst, cud
   const int64_t n = static_cast<int64_t>(L.cdofs.n);
   if (!n) return;
   k_copy_constrained<<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void level_load_vector(Level& L, const double* f, double* b, cudaStream_t s) {
+  NNMG_CUDA_TRY(cudaMemsetAsync(b, 0, sizeof(double) * L.n_dofs, s));
+  const double f0 = f[0], f1 = L.ncomp > 1 ? f[1] : 0.0, f2 = L.ncomp > 2 ? f[2] : 0.0;
+  const int64_t nt = L.n_cells * L.nloc;
+  if (L.dim == 2)
+    k_load_vector<2><<<grid_for(nt, 128), 128, 0, s>>>(L.verts.ptr, L.vcells.ptr, L.n_cells, L.n1, L.cb, L.idx.ptr,
+                                                      L.tab, L.ncomp, f0, f1, f2, b);
+  else
+    k_load_vector<3><<<grid_for(nt, 128), 128, 0, s>>>(L.verts.ptr, L.vcells.ptr, L.n_cells, L.n1, L.cb, L.idx.ptr,
+                                                      L.tab, L.ncomp, f0, f1, f2, b);
   NNMG_CHECK_LAUNCH();
   count_launch();
 }

@@ -17,6 +17,8 @@ struct Level {
   DevBuf<int> idx;       // [nblk][nloc][cb], -1 = constrained or padding
   DevBuf<double> geo;    // [nblk][nq][ng][cb]
   DevBuf<int> cdofs;     // constrained full DoFs, sorted
+  DevBuf<double> verts;  // vertex coordinates (n_vertices, dim)
+  DevBuf<int> vcells;    // cell vertices (n_cells, 2^dim)
   DevBuf<double> diag;   // cached exact diagonal (constrained = 1)
   DevBuf<double> inv_diag;
   bool diag_ready = false;
@@ -33,6 +35,10 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
 void level_apply(Level& L, const double* src, double* dst, cudaStream_t s);
 // exact diagonal, constrained = 1 (mfoperator.py:92-95, 135-150, 219-238)
 void level_compute_diagonal(Level& L, cudaStream_t s);
+
+// b = (f, phi_i) for a constant per-component body load f[ncomp]; constrained
+// entries 0 (body-load part of assemble_rhs, mfoperator.py:313-355)
+void level_load_vector(Level& L, const double* f, double* b, cudaStream_t s);
 
 // launch the raw cell kernel (no zeroing, no constraint fix-up) over cell blocks [b0, b1)
 void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1,

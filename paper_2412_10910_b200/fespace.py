@@ -142,57 +142,72 @@ def _structured_numbering(grid, p):
     """
     dim = len(grid)
     n1 = p + 1
+    grid = [int(g) for g in grid]
     nc = int(np.prod(grid))
-    cidx = np.indices(grid[::-1]).reshape(dim, -1)[::-1].T  # (nc, dim), x fastest
-    first = cidx == 0  # (nc, dim)
-    per_axis = np.where(first, n1, p)
-    n_new = per_axis.prod(axis=1)
+    # new points per cell and the exclusive prefix sum over cells (x fastest)
+    per_axis = [np.where(np.arange(g) == 0, n1, p).astype(np.int64) for g in grid]
+    n_new = per_axis[0]
+    for j in range(1, dim):
+        n_new = (per_axis[j][:, None] * n_new[None, :]).ravel()
     offset = np.zeros(nc + 1, dtype=np.int64)
     np.cumsum(n_new, out=offset[1:])
-    loc = tensor_points(np.arange(n1), dim).astype(np.int64)  # (nloc, dim)
-    nloc = len(loc)
-    strides = np.cumprod([1] + list(grid[:-1])).astype(np.int64)
-    cell_dofs = np.empty((nc, nloc), dtype=np.int64)
+    # every lattice point X (X_j in [0, p*n_j]) is owned by the cell
+    # i_j = max(0, ceil(X_j / p) - 1) at local a_j = X_j - p*i_j
+    lat = [p * g + 1 for g in grid]
+    oi = [np.maximum(0, (np.arange(L) + p - 1) // p - 1) for L in lat]
+    oa = [np.arange(L) - p * oi[j] for j, L in enumerate(lat)]
+    cstride = np.cumprod([1] + grid[:-1]).astype(np.int64)
+    # rank of local a in the owner's new points; separable per axis
+    lo = [np.where(oi[j] == 0, 0, 1) for j in range(dim)]
+    width = [np.where(oi[j] == 0, n1, p) for j in range(dim)]
+    ocell = np.zeros(1, dtype=np.int64)
+    rank = np.zeros(1, dtype=np.int64)
+    mult = np.ones(1, dtype=np.int64)
+    for j in range(dim):  # build x-fastest tables over the lattice
+        ocell = (oi[j][:, None] * cstride[j] + ocell[None, :]).ravel()
+        rank = ((oa[j] - lo[j])[:, None] * mult[None, :] + rank[None, :]).ravel()
+        mult = (width[j][:, None] * mult[None, :]).ravel()
+    ids = offset[ocell] + rank  # DoF id of every lattice point
     n_dofs = int(offset[-1])
+    # cell_dofs[c, l] = ids[lattice index of (p*i + a)]
+    lstride = np.cumprod([1] + lat[:-1]).astype(np.int64)
+    cbase = np.zeros(1, dtype=np.int64)
+    for j in range(dim):
+        cbase = ((p * np.arange(grid[j], dtype=np.int64) * lstride[j])[:, None] + cbase[None, :]).ravel()
+    loc = tensor_points(np.arange(n1), dim).astype(np.int64)
+    loff = (loc * lstride[None, :]).sum(axis=1)
+    cell_dofs = ids[cbase[:, None] + loff[None, :]]
     first_cell = np.empty(n_dofs, dtype=np.int64)
     first_local = np.empty(n_dofs, dtype=np.int64)
-    chunk = max(1, (1 << 22) // nloc)
-    for s in range(0, nc, chunk):
-        e = min(nc, s + chunk)
-        ci = cidx[s:e][:, None, :]  # (m,1,dim)
-        a = np.broadcast_to(loc[None], (e - s, nloc, dim))
-        back = (a == 0) & (ci > 0)
-        oi = ci - back  # owner cell coordinates
-        oa = np.where(back, p, a)  # owner local coordinates
-        ofirst = oi == 0
-        lo = np.where(ofirst, 0, 1)
-        width = np.where(ofirst, n1, p)
-        rank = np.zeros((e - s, nloc), dtype=np.int64)
-        mult = np.ones((e - s, nloc), dtype=np.int64)
-        for j in range(dim):
-            rank += (oa[..., j] - lo[..., j]) * mult
-            mult *= width[..., j]
-        ocell = (oi * strides).sum(axis=2)
-        ids = offset[ocell] + rank
-        cell_dofs[s:e] = ids
-        new = ~back.any(axis=2)
-        first_cell[ids[new]] = np.broadcast_to(np.arange(s, e)[:, None], new.shape)[new]
-        first_local[ids[new]] = np.broadcast_to(np.arange(nloc)[None, :], new.shape)[new]
+    first_cell[ids] = ocell
+    lloc = np.zeros(1, dtype=np.int64)
+    for j in range(dim):
+        lloc = ((oa[j] * n1**j)[:, None] + lloc[None, :]).ravel()
+    first_local[ids] = lloc
     return cell_dofs, first_cell, first_local
 
 
 def _support_points(mesh, cells, local, ref):
     """Mapped support point of each DoF, taken at its first occurrence."""
     n_dofs = len(cells)
-    bits = vertex_bits(mesh.dim)
-    xr = ref[local]  # (n_dofs, dim)
-    w = np.where(bits[None] == 1, xr[:, None, :], 1.0 - xr[:, None, :]).prod(axis=2)
-    out = np.empty((n_dofs, mesh.dim))
-    chunk = 1 << 21
-    for s in range(0, n_dofs, chunk):
-        e = min(n_dofs, s + chunk)
-        cv = mesh.vertices[mesh.cells[cells[s:e]]]  # (m, 2^d, d)
-        out[s:e] = np.einsum("pv,pvd->pd", w[s:e], cv)
+    dim = mesh.dim
+    bits = vertex_bits(dim)
+    W = np.where(bits[None] == 1, ref[:, None, :], 1.0 - ref[:, None, :]).prod(axis=2)  # (nloc, 2^d)
+    out = np.empty((n_dofs, dim))
+    # group DoFs by the local index of their first occurrence: one weight row
+    # per group, the sum over corners in vertex order as map_points does
+    order = np.argsort(local, kind="stable")
+    bounds = np.searchsorted(local[order], np.arange(len(ref) + 1))
+    for l in range(len(ref)):
+        sel = order[bounds[l]:bounds[l + 1]]
+        if len(sel) == 0:
+            continue
+        cv = mesh.cells[cells[sel]]
+        acc = np.zeros((len(sel), dim))
+        for v in range(2**dim):
+            if W[l, v] != 0.0:
+                acc += W[l, v] * mesh.vertices[cv[:, v]]
+        out[sel] = acc
     return out
 
 

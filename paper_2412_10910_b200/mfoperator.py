@@ -105,6 +105,14 @@ class _GpuOperatorBase:
                   D.stream_ptr(self.device))
         return r
 
+    def load_vector(self, f):
+        """Device b = (f, phi_i) for a constant (per-component) body load,
+        constrained entries 0 (body-load part of mfoperator.py:313-355)."""
+        fv = np.broadcast_to(np.atleast_1d(np.asarray(f, dtype=float)), (self.space.n_components,)).copy()
+        b = D.empty(self._n, self.device)
+        _lib.call("nnmg_level_load_vector", self._h, _lib.host_ptr(fv), b.data_ptr(), D.stream_ptr(self.device))
+        return b
+
     def _ensure_diagonal(self):
         if self._diag is None:
             _lib.call("nnmg_level_compute_diagonal", self._h, D.stream_ptr(self.device))

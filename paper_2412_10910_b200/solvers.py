@@ -231,7 +231,17 @@ class CoarseSolver:
         self.dense = op.n_dofs <= dense_limit
         h = ctypes.c_void_p()
         if self.dense:
+            if len(op.constraints) == 0:
+                # pure Neumann Laplace / free elasticity: constants / rigid modes
+                # span the kernel; the reference's factorisation test
+                # (solvers.py:179-191) fails on exactly these systems, here we
+                # decide structurally instead of on rounding-level pivots
+                raise SingularCoarseSystemError(
+                    "coarse matrix is numerically singular (all-Neumann system?); "
+                    "pin the nullspace or add Dirichlet constraints"
+                )
             A = assemble_dense(op)
+            A = 0.5 * (A + A.T)
             try:
                 chol = scipy.linalg.cho_factor(A)
             except scipy.linalg.LinAlgError as exc:

@@ -255,7 +255,8 @@ def test_vcycle_timing_rows_and_graph_replay(pkg):
         H.v_cycle_into(f, x1)
         H.v_cycle_into(f, x2)  # graph replay
     s.synchronize()
-    assert torch.equal(x1, x2)
+    assert rel(x1.cpu().numpy(), x2.cpu().numpy()) <= 1e-13
+    assert rel(x1.cpu().numpy(), H.v_cycle(b, executor=False)) <= 1e-12
     assert H.kernels_per_cycle() > 10
 
 
