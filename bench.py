@@ -235,10 +235,14 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         torch.cuda.profiler.start()
         with torch.cuda.stream(stream):
+            torch.cuda.nvtx.range_push("vcycle")
             H.v_cycle_into(b, z)
+            torch.cuda.nvtx.range_pop()
+            torch.cuda.nvtx.range_push("hot")
             fine.apply_into(u, v)
             T.prolongate_into(rc, v)
             T.restrict_into(u, rc)
+            torch.cuda.nvtx.range_pop()
         stream.synchronize()
         torch.cuda.profiler.stop()
         if rank == 0:

@@ -62,15 +62,19 @@ struct CellKernel {
   // participate, `sync` synchronises exactly that group.  kNC selects the
   // read-only (non-coherent) path for the source vector, which is only legal
   // when no thread of the grid writes it during the kernel.
-  template <bool kNC = true, class Sync>
-  __device__ __forceinline__ static void run(const Tables& tab, const double* __restrict__ src,
-                                             double* __restrict__ dst, const int* __restrict__ idx,
-                                             const double* __restrict__ geo, int64_t blk, double lam,
-                                             double mu, double* sm, int tid, Sync&& sync) {
+  // `src(i)` yields source entry i (a plain vector, or a fused expression such
+  // as z + beta p inside the coarse CG).  Returns this thread's share of the
+  // cell energy sum_l u_l (A_K u)_l over its x-pencil (zero-in applied), so
+  // that p.Ap can be formed without waiting for the scatter to complete.
+  template <class Src, class Sync>
+  __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
+                                               const int* __restrict__ idx, const double* __restrict__ geo,
+                                               int64_t blk, double lam, double mu, double* sm, int tid,
+                                               Sync&& sync) {
     const int lane = tid % CB;
     const int pen = tid / CB;
     constexpr int A = 0, GX = 1, GY = 2;
-    double v[NCOMP][N1];
+    double v[NCOMP][N1], u0[NCOMP][N1];
     int gi[N1];
     // P1: gather the x-pencil and interpolate along x
     {
@@ -79,7 +83,10 @@ struct CellKernel {
       for (int i = 0; i < N1; ++i) {
         gi[i] = __ldcs(idx + (blk * NLOC + base + i) * CB + lane);
 #pragma unroll
-        for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? (kNC ? __ldg(src + (int64_t)gi[i] * NCOMP + c) : src[(int64_t)gi[i] * NCOMP + c]) : 0.0;
+        for (int c = 0; c < NCOMP; ++c) {
+          v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
+          u0[c][i] = v[c][i];
+        }
       }
       op(tab.S, v, false);
       store<0>(sm, A, pen, lane, v);
@@ -216,14 +223,25 @@ struct CellKernel {
     // final: S^T along x and scatter-add the x-pencil
     load<0>(sm, A, pen, lane, v);
     op(tab.S, v, true);
+    double energy = 0.0;
 #pragma unroll
     for (int i = 0; i < N1; ++i) {
       if (gi[i] >= 0) {
 #pragma unroll
-        for (int c = 0; c < NCOMP; ++c) atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, v[c][i]);
+        for (int c = 0; c < NCOMP; ++c) {
+          atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, v[c][i]);
+          energy = fma(u0[c][i], v[c][i], energy);
+        }
       }
     }
+    return energy;
   }
+};
+
+// read-only source vector (never written during the kernel)
+struct PlainSrc {
+  const double* __restrict__ s;
+  __device__ __forceinline__ double operator()(int64_t i) const { return __ldg(s + i); }
 };
 
 

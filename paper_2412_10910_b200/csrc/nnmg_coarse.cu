@@ -3,11 +3,17 @@
 // * dense: x = A^-1 b with the inverse precomputed on the host from a Cholesky
 //   factorisation (n <= dense_limit), one warp per row;
 // * CG-Jacobi: the reference's cg_solve(op, b, precond=inv_diag, 1e-8, 1e4)
-//   (solvers.py:129-164) as ONE persistent kernel on one thread-block cluster.
-//   The matrix-free apply runs on NSUB sub-groups per CTA (named barriers), the
-//   vector phases on each CTA's contiguous DoF range, dot products reduce per
-//   CTA and then in fixed rank order so every CTA takes identical decisions;
-//   cluster barriers separate the phases.  No host round trip per iteration.
+//   (solvers.py:129-164) as ONE persistent cooperative kernel.  Per iteration
+//   two grid barriers instead of four:
+//     phase A  p_k = z + beta p_{k-1} is formed on the fly inside the cell
+//              gather (owners also store it), Ap_k accumulates by scatter, and
+//              p.Ap is summed from the per-cell energies p_K.(A_K p_K) plus
+//              the constrained rows (identical to p.Ap in exact arithmetic);
+//     barrier; phase B  alpha, x += alpha p, r -= alpha Ap, z = D^-1 r, r.r,
+//              r.z partial sums, zero the other Ap buffer;
+//     barrier; every CTA reduces the partials in the same fixed order, tests
+//              ||r|| <= tol ||r0|| and forms beta.
+//   Double-buffered p and Ap make the on-the-fly formulation race free.
 #include "nnmg_coarse.cuh"
 #include "nnmg_cellkernel.cuh"
 
@@ -43,17 +49,22 @@ struct CgArgs {
   int64_t n;
   const double* b;
   double* x;
-  double *r, *z, *p, *ap;
-  double* part;  // [3][nrank]
+  double *r, *z;
+  double* p[2];
+  double* ap[2];
+  double* part;  // [3][grid]
   double reduction;
   int max_iter;
   int* status;  // iterations, converged, error
-  int nsub;
 };
 
-__device__ __forceinline__ void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
+// p = z + beta p_old, evaluated identically by gathers and owners
+struct CgSrc {
+  const double* z;
+  const double* p_old;
+  double beta;
+  __device__ __forceinline__ double operator()(int64_t i) const { return fma(beta, p_old[i], z[i]); }
+};
 
 // block-wide fixed-order sum of two values; result valid in every thread
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
@@ -78,18 +89,43 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
   b = sb;
 }
 
+// sum of part[0..n) (and part2) in one fixed order, identical in every CTA
+__device__ __forceinline__ void grid_sum2(const double* part, const double* part2, int n, double& a, double& b,
+                                          double* sh) {
+  if (threadIdx.x < 32) {
+    double sa = 0.0, sb = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) {
+      sa += __ldcg(part + i);
+      if (part2) sb += __ldcg(part2 + i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_down_sync(0xffffffffu, sa, o);
+      sb += __shfl_down_sync(0xffffffffu, sb, o);
+    }
+    if (threadIdx.x == 0) {
+      sh[0] = sa;
+      sh[1] = sb;
+    }
+  }
+  __syncthreads();
+  a = sh[0];
+  b = sh[1];
+  __syncthreads();
+}
+
 template <int D, int P, int NC, int PH>
-__global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
+__global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_cg(CgArgs a) {
   using CK = CellKernel<D, P, NC, PH>;
   extern __shared__ double sm[];
-  __shared__ double red[64];
-  cg::cluster_group cl = cg::this_cluster();
-  const int rank = static_cast<int>(cl.block_rank()), nrank = static_cast<int>(cl.num_blocks());
+  __shared__ double red[2 * 32 + 2];
+  cg::grid_group grid = cg::this_grid();
+  const int rank = blockIdx.x, nrank = gridDim.x;
   const int tid = threadIdx.x, nth = blockDim.x;
   const int64_t i0 = a.n * rank / nrank, i1 = a.n * (rank + 1) / nrank;
-  double* part_rr = a.part;
-  double* part_rz = a.part + nrank;
-  double* part_pap = a.part + 2 * nrank;
+  double* part_e = a.part;
+  double* part_rr = a.part + nrank;
+  double* part_rz = a.part + 2 * nrank;
 
   double srr = 0.0, srz = 0.0;
   for (int64_t i = i0 + tid; i < i1; i += nth) {
@@ -98,8 +134,9 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
     a.x[i] = 0.0;
     a.r[i] = bi;
     a.z[i] = zi;
-    a.p[i] = zi;
-    a.ap[i] = 0.0;
+    a.p[1][i] = 0.0;
+    a.ap[1][i] = 0.0;
+    a.ap[0][i] = 0.0;
     srr += bi * bi;
     srz += bi * zi;
   }
@@ -108,12 +145,9 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
     part_rr[rank] = srr;
     part_rz[rank] = srz;
   }
-  cl.sync();
-  double rr = 0.0, rz = 0.0;
-  for (int k = 0; k < nrank; ++k) {
-    rr += part_rr[k];
-    rz += part_rz[k];
-  }
+  grid.sync();
+  double rr, rz;
+  grid_sum2(part_rr, part_rz, nrank, rr, rz, red + 64);
   const double norm0 = sqrt(rr);
   if (norm0 == 0.0) {
     if (rank == 0 && tid == 0) {
@@ -124,35 +158,28 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
     return;
   }
   const double target = a.reduction * norm0;
-  const int sub = tid / CK::NTHREADS, stid = tid % CK::NTHREADS;
-  const size_t sub_doubles = CK::SMEM / sizeof(double);
+  double beta = 0.0;
   for (int it = 1; it <= a.max_iter; ++it) {
-    // Ap = A p (zero-in / identity-out)
-    if (sub < a.nsub) {
-      double* smem = sm + sub * sub_doubles;
-      const int bar = sub + 1;
-      const int64_t stride = (int64_t)nrank * a.nsub;
-      for (int64_t blk = (int64_t)rank * a.nsub + sub; blk < a.nblk; blk += stride) {
-        if (a.nsub == 1)
-          CK::template run<false>(a.tab, a.p, a.ap, a.idx, a.geo, blk, a.lam, a.mu, smem, stid,
-                                  [] __device__() { __syncthreads(); });
-        else
-          CK::template run<false>(a.tab, a.p, a.ap, a.idx, a.geo, blk, a.lam, a.mu, smem, stid,
-                                  [bar] __device__() { named_sync(bar, CK::NTHREADS); });
-      }
-    }
+    const int cur = it & 1, prv = cur ^ 1;
+    const CgSrc src{a.z, a.p[prv], beta};
+    // phase A: Ap = A p with p formed on the fly; cell energies
+    double e = 0.0;
+    for (int64_t blk = rank; blk < a.nblk; blk += nrank)
+      e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm, tid,
+                   [] __device__() { __syncthreads(); });
+    for (int64_t i = i0 + tid; i < i1; i += nth) a.p[cur][i] = src(i);
     for (int64_t k = (int64_t)rank * nth + tid; k < a.ncons; k += (int64_t)nrank * nth) {
       const int c = a.cdofs[k];
-      a.ap[c] = a.p[c];
+      const double pc = src(c);
+      a.ap[cur][c] = pc;
+      e = fma(pc, pc, e);
     }
-    cl.sync();
-    double spap = 0.0, dummy = 0.0;
-    for (int64_t i = i0 + tid; i < i1; i += nth) spap += a.p[i] * a.ap[i];
-    block_sum2(spap, dummy, red);
-    if (tid == 0) part_pap[rank] = spap;
-    cl.sync();
-    double pap = 0.0;
-    for (int k = 0; k < nrank; ++k) pap += part_pap[k];
+    double dummy = 0.0;
+    block_sum2(e, dummy, red);
+    if (tid == 0) part_e[rank] = e;
+    grid.sync();
+    double pap, unused;
+    grid_sum2(part_e, nullptr, nrank, pap, unused, red + 64);
     if (!(pap > 0.0)) {
       if (rank == 0 && tid == 0) {
         a.status[0] = it;
@@ -162,15 +189,16 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
       return;
     }
     const double alpha = rz / pap;
+    // phase B
     srr = 0.0;
     srz = 0.0;
     for (int64_t i = i0 + tid; i < i1; i += nth) {
-      a.x[i] = a.x[i] + alpha * a.p[i];
-      const double ri = a.r[i] - alpha * a.ap[i];
+      a.x[i] = a.x[i] + alpha * a.p[cur][i];
+      const double ri = a.r[i] - alpha * a.ap[cur][i];
       const double zi = a.inv_diag[i] * ri;
       a.r[i] = ri;
       a.z[i] = zi;
-      a.ap[i] = 0.0;
+      a.ap[prv][i] = 0.0;
       srr += ri * ri;
       srz += ri * zi;
     }
@@ -179,13 +207,9 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
       part_rr[rank] = srr;
       part_rz[rank] = srz;
     }
-    cl.sync();
-    rr = 0.0;
-    double rz_new = 0.0;
-    for (int k = 0; k < nrank; ++k) {
-      rr += part_rr[k];
-      rz_new += part_rz[k];
-    }
+    grid.sync();
+    double rz_new;
+    grid_sum2(part_rr, part_rz, nrank, rr, rz_new, red + 64);
     if (sqrt(rr) <= target) {
       if (rank == 0 && tid == 0) {
         a.status[0] = it;
@@ -194,10 +218,8 @@ __global__ void __launch_bounds__(1024) k_coarse_cg(CgArgs a) {
       }
       return;
     }
-    const double beta = rz_new / rz;
+    beta = rz_new / rz;
     rz = rz_new;
-    for (int64_t i = i0 + tid; i < i1; i += nth) a.p[i] = a.z[i] + beta * a.p[i];
-    cl.sync();
   }
   if (rank == 0 && tid == 0) {
     a.status[0] = a.max_iter;
@@ -218,36 +240,19 @@ struct CgLaunch {
     auto kern = k_coarse_cg<D, P, NC, PH>;
     Level& L = *C.level;
     if (configure_only) {
-      int nsub = 1;
-      if (CK::NTHREADS % 32 == 0) {
-        nsub = std::max(1, std::min({15, 1024 / CK::NTHREADS, int((200 * 1024) / CK::SMEM)}));
-      }
-      C.nsub = nsub;
-      C.block = nsub * CK::NTHREADS;
-      C.smem = nsub * CK::SMEM;
+      C.block = CK::NTHREADS;
+      C.smem = CK::SMEM;
+      C.nsub = 1;
       NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      C.nrank = 0;
-      for (int cs : {16, 8, 4, 2, 1}) {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = cs;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(cs);
-        cfg.blockDim = dim3(C.block);
-        cfg.dynamicSmemBytes = C.smem;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int nclusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0) {
-          C.nrank = cs;
-          break;
-        }
-        cudaGetLastError();
-      }
-      NNMG_REQUIRE(C.nrank > 0, kCudaError, "no thread-block cluster configuration fits the coarse solver");
+      int per_sm = 0, nsm = 0, dev = 0;
+      NNMG_CUDA_TRY(cudaGetDevice(&dev));
+      NNMG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C.block, C.smem));
+      NNMG_REQUIRE(per_sm > 0, kCudaError, "coarse CG kernel does not fit on an SM");
+      // one CTA per cell block (single apply round), capped by co-residency
+      const int64_t want = std::max<int64_t>(1, L.nblk);
+      C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
+      C.part.alloc(3 * size_t(C.nrank));
       return;
     }
     CgArgs a;
@@ -265,26 +270,16 @@ struct CgLaunch {
     a.x = x;
     a.r = C.r.ptr;
     a.z = C.z.ptr;
-    a.p = C.p.ptr;
-    a.ap = C.ap.ptr;
+    a.p[0] = C.p.ptr;
+    a.p[1] = C.p.ptr + L.n_dofs;
+    a.ap[0] = C.ap.ptr;
+    a.ap[1] = C.ap.ptr + L.n_dofs;
     a.part = C.part.ptr;
     a.reduction = C.reduction;
     a.max_iter = C.max_iter;
     a.status = C.status.ptr;
-    a.nsub = C.nsub;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C.nrank;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(C.nrank);
-    cfg.blockDim = dim3(C.block);
-    cfg.dynamicSmemBytes = C.smem;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    NNMG_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
+    void* params[] = {&a};
+    NNMG_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(C.nrank), dim3(C.block), params, C.smem, s));
     count_launch();
   }
 };
@@ -313,9 +308,8 @@ Coarse* coarse_cg_create(Level* L, double reduction, int max_iter) {
     C->max_iter = max_iter;
     C->r.alloc(L->n_dofs);
     C->z.alloc(L->n_dofs);
-    C->p.alloc(L->n_dofs);
-    C->ap.alloc(L->n_dofs);
-    C->part.alloc(3 * 16);
+    C->p.alloc(2 * L->n_dofs);
+    C->ap.alloc(2 * L->n_dofs);
     C->status.alloc(3);
     C->status.zero();
     CgLaunch f{*C, nullptr, nullptr, 0, true};

@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(CellKernel<DIM, P, NCOMP, PHYS>::NTHREADS)
     k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
             const double* __restrict__ geo, int64_t b0, double lam, double mu) {
   extern __shared__ double sm[];
-  CellKernel<DIM, P, NCOMP, PHYS>::template run<true>(tab, src, dst, idx, geo, b0 + blockIdx.x, lam, mu, sm,
-                                                     threadIdx.x, [] __device__() { __syncthreads(); });
+  CellKernel<DIM, P, NCOMP, PHYS>::run(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x, lam, mu, sm, threadIdx.x,
+                                       [] __device__() { __syncthreads(); });
 }
 
 // ---------------------------------------------------------------------------

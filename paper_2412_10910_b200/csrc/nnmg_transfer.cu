@@ -2,6 +2,7 @@
 // location that builds the transfer records.
 #include "nnmg_transfer.cuh"
 #include "nnmg_cellkernel.cuh"
+#include "nnmg_transfer_kernels.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -10,152 +11,7 @@ namespace nnmg {
 
 static inline unsigned grid_for(int64_t n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
-static constexpr int kWarps = 4;  // coarse cells (one per warp) per thread block
-
-// ---------------------------------------------------------------------------
-// K6: u_f[pt] (+)= sum_l u_c[gather[pt,l]] prod_j phi_{l_j}(xhat_j)
-// One warp per owning coarse cell: the cell's coarse values are staged once in
-// shared memory and broadcast while the lanes evaluate the cell's points.
-// Contraction order x, then y, then z as transfer.py:93-95.
-// ---------------------------------------------------------------------------
-template <int DIM, int PC, int NCOMP, int CBC>
-__global__ void __launch_bounds__(kWarps * 32)
-    k_prolongate(Tables tab, const double* __restrict__ uc, double* __restrict__ uf, int accumulate,
-                 const int* __restrict__ cidx, const int* __restrict__ cell_start, const int* __restrict__ pt_dof,
-                 const double* __restrict__ xhat, int64_t ncc) {
-  constexpr int N1 = PC + 1;
-  constexpr int NLOC = ipow(N1, DIM);
-  __shared__ double su[kWarps][NCOMP * NLOC];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t cell = blockIdx.x * (int64_t)kWarps + warp;
-  if (cell >= ncc) return;
-  const int64_t blk = cell / CBC, cl = cell % CBC;
-  for (int l = lane; l < NLOC; l += 32) {
-    const int g = cidx[(blk * NLOC + l) * CBC + cl];
-#pragma unroll
-    for (int c = 0; c < NCOMP; ++c) su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] : 0.0;
-  }
-  __syncwarp();
-  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
-  for (int p = p0 + lane; p < p1; p += 32) {
-    double X[DIM][N1];
-#pragma unroll
-    for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, xhat[(int64_t)p * DIM + j], X[j]);
-    const int64_t dof = pt_dof[p];
-#pragma unroll
-    for (int c = 0; c < NCOMP; ++c) {
-      const double* U = su[warp] + c * NLOC;
-      double val;
-      if constexpr (DIM == 2) {
-        double t[N1];
-#pragma unroll
-        for (int i1 = 0; i1 < N1; ++i1) {
-          double s = 0.0;
-#pragma unroll
-          for (int i0 = 0; i0 < N1; ++i0) s = fma(U[i0 + N1 * i1], X[0][i0], s);
-          t[i1] = s;
-        }
-        val = 0.0;
-#pragma unroll
-        for (int i1 = 0; i1 < N1; ++i1) val = fma(t[i1], X[1][i1], val);
-      } else {
-        double t2[N1];
-#pragma unroll
-        for (int i2 = 0; i2 < N1; ++i2) {
-          double s2 = 0.0;
-#pragma unroll
-          for (int i1 = 0; i1 < N1; ++i1) {
-            double s = 0.0;
-#pragma unroll
-            for (int i0 = 0; i0 < N1; ++i0) s = fma(U[i0 + N1 * i1 + N1 * N1 * i2], X[0][i0], s);
-            s2 = fma(s, X[1][i1], s2);
-          }
-          t2[i2] = s2;
-        }
-        val = 0.0;
-#pragma unroll
-        for (int i2 = 0; i2 < N1; ++i2) val = fma(t2[i2], X[2][i2], val);
-      }
-      double* o = uf + dof * NCOMP + c;
-      if (accumulate)
-        *o += val;
-      else
-        *o = val;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K7 phase 1: per owning coarse cell, local vector sum_pt r_f[pt] W_pt where
-// W = phi_{l2}(z)(phi_{l1}(y) phi_{l0}(x)) (transfer.py:104-109, 115).  One
-// warp per cell, lanes own local outputs and sweep the cell's points in fixed
-// order: deterministic, no atomics.
-// ---------------------------------------------------------------------------
-template <int DIM, int PC, int NCOMP>
-__global__ void __launch_bounds__(kWarps * 32)
-    k_restrict_cells(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
-                     const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc,
-                     double* __restrict__ cellbuf) {
-  constexpr int N1 = PC + 1;
-  constexpr int NLOC = ipow(N1, DIM);
-  constexpr int NOUT = NLOC * NCOMP;
-  constexpr int NPL = (NOUT + 31) / 32;
-  __shared__ double sv[kWarps][32][NCOMP];
-  __shared__ double sx[kWarps][32][DIM][N1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t cell = blockIdx.x * (int64_t)kWarps + warp;
-  if (cell >= ncc) return;
-  double acc[NPL];
-#pragma unroll
-  for (int k = 0; k < NPL; ++k) acc[k] = 0.0;
-  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
-  for (int start = p0; start < p1; start += 32) {
-    const int p = start + lane;
-    if (p < p1) {
-      const int64_t dof = pt_dof[p];
-#pragma unroll
-      for (int c = 0; c < NCOMP; ++c) sv[warp][lane][c] = rf[dof * NCOMP + c];
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, xhat[(int64_t)p * DIM + j], sx[warp][lane][j]);
-    }
-    __syncwarp();
-    const int cnt = min(32, p1 - start);
-#pragma unroll
-    for (int k = 0; k < NPL; ++k) {
-      const int o = lane + 32 * k;
-      if (o < NOUT) {
-        const int l = o / NCOMP, c = o % NCOMP;
-        const int i0 = l % N1, i1 = (l / N1) % N1, i2 = l / (N1 * N1);
-        double a = acc[k];
-        for (int j = 0; j < cnt; ++j) {
-          double w = sx[warp][j][1][i1] * sx[warp][j][0][i0];
-          if constexpr (DIM == 3) w = sx[warp][j][2][i2] * w;
-          a = fma(sv[warp][j][c], w, a);
-        }
-        acc[k] = a;
-      }
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int k = 0; k < NPL; ++k) {
-    const int o = lane + 32 * k;
-    if (o < NOUT) cellbuf[cell * NOUT + o] = acc[k];
-  }
-}
-
-// K7 phase 2: r_c[g] = sum over the (cell, l) slots holding g, fixed order
-__global__ void k_restrict_gather(const int* __restrict__ t_off, const int* __restrict__ t_ent,
-                                  const double* __restrict__ cellbuf, int64_t nsc, int ncomp, double* __restrict__ rc) {
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= nsc) return;
-  const int e0 = t_off[g], e1 = t_off[g + 1];
-  for (int c = 0; c < ncomp; ++c) {
-    double s = 0.0;
-    for (int e = e0; e < e1; ++e) s += cellbuf[(int64_t)t_ent[e] * ncomp + c];
-    rc[g * ncomp + c] = s;
-  }
-}
+static constexpr int kWarps = kTransferWarps;
 
 // ---------------------------------------------------------------------------
 struct TransferDispatch {
