@@ -66,7 +66,8 @@ struct CellKernel {
   // as z + beta p inside the coarse CG).  Returns this thread's share of the
   // cell energy sum_l u_l (A_K u)_l over its x-pencil (zero-in applied), so
   // that p.Ap can be formed without waiting for the scatter to complete.
-  template <class Src, class Sync>
+  // kRes: idx/geo point at a shared-memory copy of this block's tables
+  template <bool kRes = false, class Src, class Sync>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
@@ -74,6 +75,10 @@ struct CellKernel {
     const int lane = tid % CB;
     const int pen = tid / CB;
     constexpr int A = 0, GX = 1, GY = 2;
+    // the block's geometry chunk (85% of the bytes) is consumed only in phase
+    // 5: start streaming it into L2 now so it overlaps gathers and sweeps
+    constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
+    if (!kRes && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
     double v[NCOMP][N1], u0[NCOMP][N1];
     int gi[N1];
     // P1: gather the x-pencil and interpolate along x
@@ -81,7 +86,7 @@ struct CellKernel {
       const int base = PL::base(0, pen);
 #pragma unroll
       for (int i = 0; i < N1; ++i) {
-        gi[i] = __ldcs(idx + (blk * NLOC + base + i) * CB + lane);
+        gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * CB + lane);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
@@ -136,7 +141,7 @@ struct CellKernel {
           if constexpr (DIM == 3) g[c][1] = S(sm, GY, c, pos, lane);
           g[c][DIM - 1] = gl[c][q];
         }
-        qp_flux<DIM, NCOMP, PHYS, CB>(geo + ((blk * (int64_t)NLOC + pos) * NG) * CB + lane, g, f, lam, mu);
+        qp_flux<DIM, NCOMP, PHYS, CB, !kRes>(geo +((blk * (int64_t)NLOC + pos) * NG) * CB + lane, g, f, lam, mu);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           fx[c][q] = f[c][0];

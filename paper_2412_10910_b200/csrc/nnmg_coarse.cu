@@ -114,7 +114,9 @@ __device__ __forceinline__ void grid_sum2(const double* part, const double* part
   __syncthreads();
 }
 
-template <int D, int P, int NC, int PH>
+// RES: one cell block per CTA whose index table and geometry stay resident in
+// shared memory for the whole solve (they do not change between iterations)
+template <int D, int P, int NC, int PH, bool RES>
 __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_cg(CgArgs a) {
   using CK = CellKernel<D, P, NC, PH>;
   extern __shared__ double sm[];
@@ -122,6 +124,15 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
   cg::grid_group grid = cg::this_grid();
   const int rank = blockIdx.x, nrank = gridDim.x;
   const int tid = threadIdx.x, nth = blockDim.x;
+  constexpr int64_t kGeoChunk = int64_t(CK::NLOC) * CK::NG * CK::CB;
+  constexpr int64_t kIdxChunk = int64_t(CK::NLOC) * CK::CB;
+  double* geo_s = sm + CK::SMEM / sizeof(double);
+  int* idx_s = reinterpret_cast<int*>(geo_s + kGeoChunk);
+  if constexpr (RES) {
+    for (int64_t k = tid; k < kGeoChunk; k += nth) geo_s[k] = a.geo[rank * kGeoChunk + k];
+    for (int64_t k = tid; k < kIdxChunk; k += nth) idx_s[k] = a.idx[rank * kIdxChunk + k];
+    __syncthreads();
+  }
   const int64_t i0 = a.n * rank / nrank, i1 = a.n * (rank + 1) / nrank;
   double* part_e = a.part;
   double* part_rr = a.part + nrank;
@@ -164,9 +175,14 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
     const CgSrc src{a.z, a.p[prv], beta};
     // phase A: Ap = A p with p formed on the fly; cell energies
     double e = 0.0;
-    for (int64_t blk = rank; blk < a.nblk; blk += nrank)
-      e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm, tid,
-                   [] __device__() { __syncthreads(); });
+    if constexpr (RES) {
+      e = CK::template run<true>(a.tab, src, a.ap[cur], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
+                                 [] __device__() { __syncthreads(); });
+    } else {
+      for (int64_t blk = rank; blk < a.nblk; blk += nrank)
+        e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm, tid,
+                     [] __device__() { __syncthreads(); });
+    }
     for (int64_t i = i0 + tid; i < i1; i += nth) a.p[cur][i] = src(i);
     for (int64_t k = (int64_t)rank * nth + tid; k < a.ncons; k += (int64_t)nrank * nth) {
       const int c = a.cdofs[k];
@@ -237,24 +253,43 @@ struct CgLaunch {
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
-    auto kern = k_coarse_cg<D, P, NC, PH>;
     Level& L = *C.level;
     if (configure_only) {
       C.block = CK::NTHREADS;
-      C.smem = CK::SMEM;
       C.nsub = 1;
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
-      int per_sm = 0, nsm = 0, dev = 0;
+      int nsm = 0, dev = 0;
       NNMG_CUDA_TRY(cudaGetDevice(&dev));
       NNMG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C.block, C.smem));
-      NNMG_REQUIRE(per_sm > 0, kCudaError, "coarse CG kernel does not fit on an SM");
-      // one CTA per cell block (single apply round), capped by co-residency
-      const int64_t want = std::max<int64_t>(1, L.nblk);
-      C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
+      // resident variant: one CTA per cell block with its tables in smem
+      const size_t res_smem =
+          CK::SMEM + size_t(CK::NLOC) * CK::NG * CK::CB * sizeof(double) + size_t(CK::NLOC) * CK::CB * sizeof(int);
+      C.resident = false;
+      if (res_smem <= 200 * 1024) {
+        auto kr = k_coarse_cg<D, P, NC, PH, true>;
+        NNMG_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        int per_sm = 0;
+        NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kr, C.block, res_smem));
+        if (per_sm > 0 && L.nblk <= int64_t(per_sm) * nsm) {
+          C.resident = true;
+          C.smem = res_smem;
+          C.nrank = static_cast<int>(L.nblk);
+        }
+      }
+      if (!C.resident) {
+        auto kern = k_coarse_cg<D, P, NC, PH, false>;
+        C.smem = CK::SMEM;
+        NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+        int per_sm = 0;
+        NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C.block, C.smem));
+        NNMG_REQUIRE(per_sm > 0, kCudaError, "coarse CG kernel does not fit on an SM");
+        // one CTA per cell block (single apply round), capped by co-residency
+        const int64_t want = std::max<int64_t>(1, L.nblk);
+        C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
+      }
       C.part.alloc(3 * size_t(C.nrank));
       return;
     }
+    auto kern = C.resident ? k_coarse_cg<D, P, NC, PH, true> : k_coarse_cg<D, P, NC, PH, false>;
     CgArgs a;
     a.tab = L.tab;
     a.idx = L.idx.ptr;

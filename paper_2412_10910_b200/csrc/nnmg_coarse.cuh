@@ -13,6 +13,7 @@ struct Coarse {
   DevBuf<double> r, z, p, ap, part;
   DevBuf<int> status;  // iterations, converged, error
   int nrank = 1, nsub = 1, block = 0;
+  bool resident = false;  // cell-block tables kept in shared memory
   size_t smem = 0;
 };
 

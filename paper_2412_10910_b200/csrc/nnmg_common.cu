@@ -105,6 +105,7 @@ Tables make_tables(int degree) {
       if (j != i) d *= (nd[i] - nd[j]);
     den[i] = d;
     t.denom[i] = static_cast<double>(d);
+    t.rdenom[i] = static_cast<double>(1.0L / d);
   }
   for (int a = 0; a < n1; ++a) {
     for (int i = 0; i < n1; ++i) {

@@ -117,6 +117,7 @@ struct Tables {
   double xq[kMaxN1];          // Gauss points on [0,1]
   double nodes[kMaxN1];       // Lobatto nodes on [0,1]
   double denom[kMaxN1];       // prod_{j!=i} (node_i - node_j)
+  double rdenom[kMaxN1];      // 1 / denom (multiplications instead of fp64 divisions)
 };
 
 Tables make_tables(int degree);

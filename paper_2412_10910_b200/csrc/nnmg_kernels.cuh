@@ -47,6 +47,12 @@ struct Pencil {
   __host__ __device__ static constexpr int stride(int k) { return k == 0 ? 1 : (k == 1 ? N1 : N1 * N1); }
 };
 
+// TMA bulk prefetch of a contiguous global range into L2 (sm_90+):
+// one instruction, no registers or shared memory held.  bytes % 16 == 0.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // out[q] = sum_i M[q][i] in[i]
 template <int N1>
 __device__ __forceinline__ void sweep(const double (&M)[kMaxN1][kMaxN1], const double* in, double* out) {
@@ -71,11 +77,22 @@ __device__ __forceinline__ void sweep_t(const double (&M)[kMaxN1][kMaxN1], const
   }
 }
 
+// streaming (evict-first) global load, or a plain load when the data was made
+// resident in shared memory (generic pointer)
+template <bool kStream, class T>
+__device__ __forceinline__ T ld_geo(const T* p) {
+  if constexpr (kStream)
+    return __ldcs(p);
+  else
+    return *p;
+}
+
 // Quadrature-point physics.  g[c][j] = d u_c / d xhat_j at the point; returns
 // the reference-coordinate flux f[c][j] that is integrated against d phi/d xhat_j.
-template <int DIM, int NCOMP, int PHYS, int CB>
+template <int DIM, int NCOMP, int PHYS, int CB, bool kStream = true>
 __device__ __forceinline__ void qp_flux(const double* __restrict__ geo, const double (&g)[NCOMP][DIM],
                                         double (&f)[NCOMP][DIM], double lam, double mu) {
+#define __ldcs(p) ld_geo<kStream>(p)
   if constexpr (PHYS == kLaplace) {
     // G = J^-1 J^-T |det J| w_q, symmetric (mfoperator.py:106, 118)
     if constexpr (DIM == 3) {
@@ -126,18 +143,24 @@ __device__ __forceinline__ void qp_flux(const double* __restrict__ geo, const do
         f[a][j] = s * dv;
       }
   }
+#undef __ldcs
 }
 
-// Lagrange basis at the Lobatto nodes evaluated at t (fespace.py:42-51)
+// Lagrange basis at the Lobatto nodes evaluated at t (fespace.py:42-51); the
+// reference divides by prod(node_i - node_j), here we multiply by the
+// precomputed reciprocal (fp64 division is a long instruction sequence)
 template <int N1>
 __device__ __forceinline__ void lagrange_values(const Tables& tab, double t, double* out) {
+  double d[N1];
+#pragma unroll
+  for (int j = 0; j < N1; ++j) d[j] = t - tab.nodes[j];
 #pragma unroll
   for (int i = 0; i < N1; ++i) {
-    double v = 1.0;
+    double v = tab.rdenom[i];
 #pragma unroll
     for (int j = 0; j < N1; ++j)
-      if (j != i) v *= (t - tab.nodes[j]);
-    out[i] = v / tab.denom[i];
+      if (j != i) v *= d[j];
+    out[i] = v;
   }
 }
 
