@@ -37,6 +37,8 @@ __global__ void k_dense_solve(const double* __restrict__ ainv, const double* __r
   if (lane == 0) x[row] = s;
 }
 
+struct Slot;
+
 struct CgArgs {
   Tables tab;
   const int* idx;
@@ -52,19 +54,74 @@ struct CgArgs {
   double *r, *z;
   double* p[2];
   double* ap[2];
-  double* part;  // [3][grid]
+  Slot* slots;   // [2][grid] barrier-with-payload banks
+  unsigned long long* solve_epoch;
   double reduction;
   int max_iter;
   int* status;  // iterations, converged, error
 };
 
-// p = z + beta p_old, evaluated identically by gathers and owners
+// p = z + beta p_old, evaluated identically by gathers and owners; the
+// operands were written by other CTAs in the previous phase: read them from L2
 struct CgSrc {
   const double* z;
   const double* p_old;
   double beta;
-  __device__ __forceinline__ double operator()(int64_t i) const { return fma(beta, p_old[i], z[i]); }
+  __device__ __forceinline__ double operator()(int64_t i) const { return fma(beta, __ldcg(p_old + i), __ldcg(z + i)); }
 };
+
+// Barrier with payload: every CTA publishes two partial sums and an epoch in
+// its slot; every CTA polls all slots and sums them in one fixed order, so all
+// CTAs leave with bitwise identical totals.  Two slot banks alternate so a
+// slot is never overwritten before every CTA has read it.
+struct Slot {
+  double v[2];
+  unsigned long long epoch;
+  unsigned long long pad;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void exchange(Slot* bank, int rank, int nrank, unsigned long long epoch, double& a,
+                                         double& b, double* sh) {
+  __syncthreads();  // all of this CTA's writes precede the publish
+  if (threadIdx.x == 0) {
+    bank[rank].v[0] = a;
+    bank[rank].v[1] = b;
+    __threadfence();
+    st_release(&bank[rank].epoch, epoch);
+  }
+  if (threadIdx.x < 32) {
+    double sa = 0.0, sb = 0.0;
+    for (int i = threadIdx.x; i < nrank; i += 32) {
+      while (ld_acquire(&bank[i].epoch) < epoch) {
+      }
+      sa += __ldcg(&bank[i].v[0]);
+      sb += __ldcg(&bank[i].v[1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_down_sync(0xffffffffu, sa, o);
+      sb += __shfl_down_sync(0xffffffffu, sb, o);
+    }
+    if (threadIdx.x == 0) {
+      sh[0] = sa;
+      sh[1] = sb;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  a = sh[0];
+  b = sh[1];
+}
 
 // block-wide fixed-order sum of two values; result valid in every thread
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
@@ -134,9 +191,7 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
     __syncthreads();
   }
   const int64_t i0 = a.n * rank / nrank, i1 = a.n * (rank + 1) / nrank;
-  double* part_e = a.part;
-  double* part_rr = a.part + nrank;
-  double* part_rz = a.part + 2 * nrank;
+  unsigned long long ep = __ldcg(a.solve_epoch);  // epochs of this solve start after the last one
 
   double srr = 0.0, srz = 0.0;
   for (int64_t i = i0 + tid; i < i1; i += nth) {
@@ -152,95 +207,80 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
     srz += bi * zi;
   }
   block_sum2(srr, srz, red);
-  if (tid == 0) {
-    part_rr[rank] = srr;
-    part_rz[rank] = srz;
-  }
-  grid.sync();
-  double rr, rz;
-  grid_sum2(part_rr, part_rz, nrank, rr, rz, red + 64);
+  ++ep;
+  double rr = srr, rz = srz;
+  exchange(a.slots + (ep & 1) * nrank, rank, nrank, ep, rr, rz, red + 64);
   const double norm0 = sqrt(rr);
+  int status_it = 0, status_conv = 0, status_err = 0;
   if (norm0 == 0.0) {
-    if (rank == 0 && tid == 0) {
-      a.status[0] = 0;
-      a.status[1] = 1;
-      a.status[2] = 0;
-    }
-    return;
-  }
-  const double target = a.reduction * norm0;
-  double beta = 0.0;
-  for (int it = 1; it <= a.max_iter; ++it) {
-    const int cur = it & 1, prv = cur ^ 1;
-    const CgSrc src{a.z, a.p[prv], beta};
-    // phase A: Ap = A p with p formed on the fly; cell energies
-    double e = 0.0;
-    if constexpr (RES) {
-      e = CK::template run<true>(a.tab, src, a.ap[cur], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
-                                 [] __device__() { __syncthreads(); });
-    } else {
-      for (int64_t blk = rank; blk < a.nblk; blk += nrank)
-        e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm, tid,
-                     [] __device__() { __syncthreads(); });
-    }
-    for (int64_t i = i0 + tid; i < i1; i += nth) a.p[cur][i] = src(i);
-    for (int64_t k = (int64_t)rank * nth + tid; k < a.ncons; k += (int64_t)nrank * nth) {
-      const int c = a.cdofs[k];
-      const double pc = src(c);
-      a.ap[cur][c] = pc;
-      e = fma(pc, pc, e);
-    }
-    double dummy = 0.0;
-    block_sum2(e, dummy, red);
-    if (tid == 0) part_e[rank] = e;
-    grid.sync();
-    double pap, unused;
-    grid_sum2(part_e, nullptr, nrank, pap, unused, red + 64);
-    if (!(pap > 0.0)) {
-      if (rank == 0 && tid == 0) {
-        a.status[0] = it;
-        a.status[1] = 0;
-        a.status[2] = 1;
+    status_conv = 1;
+  } else {
+    const double target = a.reduction * norm0;
+    double beta = 0.0;
+    status_it = a.max_iter;
+    for (int it = 1; it <= a.max_iter; ++it) {
+      const int cur = it & 1, prv = cur ^ 1;
+      const CgSrc src{a.z, a.p[prv], beta};
+      // phase A: Ap = A p with p formed on the fly; cell energies
+      double e = 0.0;
+      if constexpr (RES) {
+        e = CK::template run<true>(a.tab, src, a.ap[cur], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
+                                   [] __device__() { __syncthreads(); });
+      } else {
+        for (int64_t blk = rank; blk < a.nblk; blk += nrank)
+          e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm, tid,
+                       [] __device__() { __syncthreads(); });
       }
-      return;
-    }
-    const double alpha = rz / pap;
-    // phase B
-    srr = 0.0;
-    srz = 0.0;
-    for (int64_t i = i0 + tid; i < i1; i += nth) {
-      a.x[i] = a.x[i] + alpha * a.p[cur][i];
-      const double ri = a.r[i] - alpha * a.ap[cur][i];
-      const double zi = a.inv_diag[i] * ri;
-      a.r[i] = ri;
-      a.z[i] = zi;
-      a.ap[prv][i] = 0.0;
-      srr += ri * ri;
-      srz += ri * zi;
-    }
-    block_sum2(srr, srz, red);
-    if (tid == 0) {
-      part_rr[rank] = srr;
-      part_rz[rank] = srz;
-    }
-    grid.sync();
-    double rz_new;
-    grid_sum2(part_rr, part_rz, nrank, rr, rz_new, red + 64);
-    if (sqrt(rr) <= target) {
-      if (rank == 0 && tid == 0) {
-        a.status[0] = it;
-        a.status[1] = 1;
-        a.status[2] = 0;
+      for (int64_t i = i0 + tid; i < i1; i += nth) a.p[cur][i] = src(i);
+      for (int64_t k = (int64_t)rank * nth + tid; k < a.ncons; k += (int64_t)nrank * nth) {
+        const int c = a.cdofs[k];
+        const double pc = src(c);
+        a.ap[cur][c] = pc;
+        e = fma(pc, pc, e);
       }
-      return;
+      double dummy = 0.0;
+      block_sum2(e, dummy, red);
+      ++ep;
+      exchange(a.slots + (ep & 1) * nrank, rank, nrank, ep, e, dummy, red + 64);
+      const double pap = e;
+      if (!(pap > 0.0)) {
+        status_it = it;
+        status_err = 1;
+        break;
+      }
+      const double alpha = rz / pap;
+      // phase B
+      srr = 0.0;
+      srz = 0.0;
+      for (int64_t i = i0 + tid; i < i1; i += nth) {
+        a.x[i] = a.x[i] + alpha * a.p[cur][i];
+        const double ri = a.r[i] - alpha * __ldcg(a.ap[cur] + i);
+        const double zi = a.inv_diag[i] * ri;
+        a.r[i] = ri;
+        a.z[i] = zi;
+        a.ap[prv][i] = 0.0;
+        srr += ri * ri;
+        srz += ri * zi;
+      }
+      block_sum2(srr, srz, red);
+      ++ep;
+      double rz_new = srz;
+      rr = srr;
+      exchange(a.slots + (ep & 1) * nrank, rank, nrank, ep, rr, rz_new, red + 64);
+      if (sqrt(rr) <= target) {
+        status_it = it;
+        status_conv = 1;
+        break;
+      }
+      beta = rz_new / rz;
+      rz = rz_new;
     }
-    beta = rz_new / rz;
-    rz = rz_new;
   }
   if (rank == 0 && tid == 0) {
-    a.status[0] = a.max_iter;
-    a.status[1] = 0;
-    a.status[2] = 0;
+    a.status[0] = status_it;
+    a.status[1] = status_conv;
+    a.status[2] = status_err;
+    *a.solve_epoch = ep;  // every CTA has read the base epoch (first exchange)
   }
 }
 
@@ -286,7 +326,11 @@ struct CgLaunch {
         const int64_t want = std::max<int64_t>(1, L.nblk);
         C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
       }
-      C.part.alloc(3 * size_t(C.nrank));
+      C.part.alloc(2 * 4 * size_t(C.nrank));  // 2 banks of 32-byte slots
+      C.part.zero();
+      C.epoch.alloc(1);
+      C.epoch.zero();
+      NNMG_CUDA_TRY(cudaDeviceSynchronize());
       return;
     }
     auto kern = C.resident ? k_coarse_cg<D, P, NC, PH, true> : k_coarse_cg<D, P, NC, PH, false>;
@@ -309,7 +353,8 @@ struct CgLaunch {
     a.p[1] = C.p.ptr + L.n_dofs;
     a.ap[0] = C.ap.ptr;
     a.ap[1] = C.ap.ptr + L.n_dofs;
-    a.part = C.part.ptr;
+    a.slots = reinterpret_cast<Slot*>(C.part.ptr);
+    a.solve_epoch = reinterpret_cast<unsigned long long*>(C.epoch.ptr);
     a.reduction = C.reduction;
     a.max_iter = C.max_iter;
     a.status = C.status.ptr;

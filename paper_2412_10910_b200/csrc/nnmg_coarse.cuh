@@ -11,6 +11,7 @@ struct Coarse {
   double reduction = 1e-8;
   int max_iter = 10000;
   DevBuf<double> r, z, p, ap, part;
+  DevBuf<unsigned long long> epoch;  // last barrier epoch used (persists across solves)
   DevBuf<int> status;  // iterations, converged, error
   int nrank = 1, nsub = 1, block = 0;
   bool resident = false;  // cell-block tables kept in shared memory
