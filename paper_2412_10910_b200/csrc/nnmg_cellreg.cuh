@@ -1,0 +1,134 @@
+// Register-resident cell kernel (one thread per cell) for low orders.
+//
+// The pencil kernel (nnmg_cellkernel.cuh) exchanges every intermediate through
+// shared memory; ncu shows it L1/shared-pipe bound on 3D Q2 (l1tex 96% busy,
+// DRAM 70%).  For NLOC <= 27 a whole cell fits in registers: the thread
+// gathers its cell, runs all sum-factorisation sweeps in registers, visits the
+// quadrature points slice by slice (gradients by collocation, flux, and the
+// transposed derivative sweeps accumulated immediately), and scatters.  No
+// shared memory, no block barriers; loads of the index table and geometry are
+// coalesced across the warp (32 consecutive cells = one cell block of the
+// blocked layout).
+#pragma once
+
+#include "nnmg_kernels.cuh"
+
+namespace nnmg {
+
+template <int DIM, int P>
+struct CellReg {
+  static constexpr int N1 = P + 1;
+  static constexpr int NLOC = ipow(N1, DIM);
+  static constexpr int CB = 32;
+  static constexpr int NG = DIM * (DIM + 1) / 2;
+  static constexpr bool kSupported = NLOC <= 27;
+
+  __host__ __device__ static constexpr int at(int i0, int i1, int i2) { return i0 + N1 * (i1 + N1 * i2); }
+
+  // in-register sweep along axis K with matrix M (trans: M^T)
+  template <int K, bool TRANS>
+  __device__ __forceinline__ static void sweep_axis(const double (&M)[kMaxN1][kMaxN1], double (&v)[NLOC]) {
+    constexpr int S0 = K == 0 ? 1 : (K == 1 ? N1 : N1 * N1);
+    constexpr int NL = NLOC / N1;  // lines along axis K
+#pragma unroll
+    for (int line = 0; line < NL; ++line) {
+      // base position of the line: enumerate the other axes
+      int base;
+      if constexpr (K == 0)
+        base = line * N1;
+      else if constexpr (K == 1)
+        base = (line % N1) + (line / N1) * N1 * N1;
+      else
+        base = line;
+      double in[N1], out[N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) in[i] = v[base + i * S0];
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < N1; ++i) s = fma(TRANS ? M[i][q] : M[q][i], in[i], s);
+        out[q] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < N1; ++i) v[base + i * S0] = out[i];
+    }
+  }
+
+  // Laplace only.  Returns the thread's cell energy sum_l u_l (A_K u)_l.
+  template <bool kStream, bool kEnergy, class Src>
+  __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
+                                               const int* __restrict__ idx, const double* __restrict__ geo,
+                                               int64_t blk, int lane) {
+    double v[NLOC];
+    const int* ib = idx + blk * NLOC * CB + lane;
+#pragma unroll
+    for (int l = 0; l < NLOC; ++l) {
+      const int g = ld_geo<kStream>(ib + l * CB);
+      v[l] = g >= 0 ? src((int64_t)g) : 0.0;
+    }
+    double u0[kEnergy ? NLOC : 1];
+    if constexpr (kEnergy) {
+#pragma unroll
+      for (int l = 0; l < NLOC; ++l) u0[l] = v[l];
+    }
+    // values at the Gauss points
+    sweep_axis<0, false>(tab.S, v);
+    sweep_axis<1, false>(tab.S, v);
+    if constexpr (DIM == 3) sweep_axis<2, false>(tab.S, v);
+    double w[NLOC];
+#pragma unroll
+    for (int l = 0; l < NLOC; ++l) w[l] = 0.0;
+    const double* g0 = geo + blk * (int64_t)NLOC * NG * CB + lane;
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) {
+      const int qx = q % N1, qy = (q / N1) % N1, qz = DIM == 3 ? q / (N1 * N1) : 0;
+      double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+      for (int r = 0; r < N1; ++r) {
+        gx = fma(tab.Dc[qx][r], v[at(r, qy, qz)], gx);
+        gy = fma(tab.Dc[qy][r], v[at(qx, r, qz)], gy);
+        if constexpr (DIM == 3) gz = fma(tab.Dc[qz][r], v[at(qx, qy, r)], gz);
+      }
+      const double* G = g0 + q * NG * CB;
+      double fx, fy, fz = 0.0;
+      if constexpr (DIM == 3) {
+        const double g00 = ld_geo<kStream>(G + 0 * CB), g01 = ld_geo<kStream>(G + 1 * CB);
+        const double g02 = ld_geo<kStream>(G + 2 * CB), g11 = ld_geo<kStream>(G + 3 * CB);
+        const double g12 = ld_geo<kStream>(G + 4 * CB), g22 = ld_geo<kStream>(G + 5 * CB);
+        fx = g00 * gx + g01 * gy + g02 * gz;
+        fy = g01 * gx + g11 * gy + g12 * gz;
+        fz = g02 * gx + g12 * gy + g22 * gz;
+      } else {
+        const double g00 = ld_geo<kStream>(G + 0 * CB), g01 = ld_geo<kStream>(G + 1 * CB);
+        const double g11 = ld_geo<kStream>(G + 2 * CB);
+        fx = g00 * gx + g01 * gy;
+        fy = g01 * gx + g11 * gy;
+      }
+      // transposed collocation derivatives, accumulated at once
+#pragma unroll
+      for (int r = 0; r < N1; ++r) {
+        w[at(r, qy, qz)] = fma(tab.Dc[qx][r], fx, w[at(r, qy, qz)]);
+        w[at(qx, r, qz)] = fma(tab.Dc[qy][r], fy, w[at(qx, r, qz)]);
+        if constexpr (DIM == 3) w[at(qx, qy, r)] = fma(tab.Dc[qz][r], fz, w[at(qx, qy, r)]);
+      }
+    }
+    // back to the nodal basis: S^T sweeps
+    if constexpr (DIM == 3) sweep_axis<2, true>(tab.S, w);
+    sweep_axis<1, true>(tab.S, w);
+    sweep_axis<0, true>(tab.S, w);
+    double energy = 0.0;
+#pragma unroll
+    for (int l = 0; l < NLOC; ++l) {
+      // the index table is re-read (L1/L2 hit) rather than kept live
+      const int g = kStream ? __ldg(ib + l * CB) : ib[l * CB];
+      if (g >= 0) {
+        atomicAdd(dst + g, w[l]);
+        if constexpr (kEnergy) energy = fma(u0[l], w[l], energy);
+      }
+    }
+    return energy;
+  }
+};
+
+}  // namespace nnmg

@@ -16,8 +16,10 @@
 //   Double-buffered p and Ap make the on-the-fly formulation race free.
 #include "nnmg_coarse.cuh"
 #include "nnmg_cellkernel.cuh"
+#include "nnmg_cellreg.cuh"
 
 #include <cooperative_groups.h>
+#include <string>
 
 namespace cg = cooperative_groups;
 
@@ -55,6 +57,9 @@ struct CgArgs {
   double* p[2];
   double* ap[2];
   Slot* slots;   // [2][grid] barrier-with-payload banks
+  Slot* result;  // [2] root-broadcast results
+  int barrier;   // 0 grid.sync, 1 all-to-all, 2 root
+  unsigned long long* trace;  // optional per-phase %globaltimer samples (rank 0)
   unsigned long long* solve_epoch;
   double reduction;
   int max_iter;
@@ -88,6 +93,51 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// centralised variant: CTA 0 gathers the partials in fixed order and
+// publishes one result; the other CTAs poll a single flag
+__device__ __forceinline__ void exchange_root(Slot* bank, Slot* result, int rank, int nrank, unsigned long long epoch,
+                                              double& a, double& b, double* sh) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bank[rank].v[0] = a;
+    bank[rank].v[1] = b;
+    __threadfence();
+    st_release(&bank[rank].epoch, epoch);
+  }
+  if (rank == 0 && threadIdx.x < 32) {
+    double sa = 0.0, sb = 0.0;
+    for (int i = threadIdx.x; i < nrank; i += 32) {
+      while (ld_acquire(&bank[i].epoch) < epoch) {
+      }
+      sa += __ldcg(&bank[i].v[0]);
+      sb += __ldcg(&bank[i].v[1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_down_sync(0xffffffffu, sa, o);
+      sb += __shfl_down_sync(0xffffffffu, sb, o);
+    }
+    if (threadIdx.x == 0) {
+      Slot* r = result + (epoch & 1);
+      r->v[0] = sa;
+      r->v[1] = sb;
+      __threadfence();
+      st_release(&r->epoch, epoch);
+    }
+  }
+  if (threadIdx.x == 0) {
+    Slot* r = result + (epoch & 1);
+    while (ld_acquire(&r->epoch) < epoch) {
+    }
+    sh[0] = __ldcg(&r->v[0]);
+    sh[1] = __ldcg(&r->v[1]);
+    __threadfence();
+  }
+  __syncthreads();
+  a = sh[0];
+  b = sh[1];
 }
 
 __device__ __forceinline__ void exchange(Slot* bank, int rank, int nrank, unsigned long long epoch, double& a,
@@ -173,9 +223,62 @@ __device__ __forceinline__ void grid_sum2(const double* part, const double* part
 
 // RES: one cell block per CTA whose index table and geometry stay resident in
 // shared memory for the whole solve (they do not change between iterations)
-template <int D, int P, int NC, int PH, bool RES>
-__global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_cg(CgArgs a) {
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// barrier + fixed-order sum of two per-CTA partials; kind 0: cooperative
+// grid.sync, 1: all-to-all slot polling, 2: root gathers and broadcasts
+__device__ __forceinline__ void barrier_sum(int kind, Slot* slots, Slot* result, int rank, int nrank,
+                                            unsigned long long& ep, double& x, double& y, double* red) {
+  ++ep;
+  Slot* bank = slots + (ep & 1) * nrank;
+  if (kind == 1) {
+    exchange(bank, rank, nrank, ep, x, y, red);
+  } else if (kind == 2) {
+    exchange_root(bank, result, rank, nrank, ep, x, y, red);
+  } else {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bank[rank].v[0] = x;
+      bank[rank].v[1] = y;
+    }
+    cg::this_grid().sync();
+    if (threadIdx.x < 32) {
+      double sa = 0.0, sb = 0.0;
+      for (int i = threadIdx.x; i < nrank; i += 32) {
+        sa += __ldcg(&bank[i].v[0]);
+        sb += __ldcg(&bank[i].v[1]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_down_sync(0xffffffffu, sa, o);
+        sb += __shfl_down_sync(0xffffffffu, sb, o);
+      }
+      if (threadIdx.x == 0) {
+        red[0] = sa;
+        red[1] = sb;
+      }
+    }
+    __syncthreads();
+    x = red[0];
+    y = red[1];
+    __syncthreads();
+  }
+}
+
+// MODE 0: pencil cell kernel, tables from L2; 1: pencil, tables resident in
+// shared memory (RES); 2: register-resident thread-per-cell kernel, one warp
+// per cell block (Laplace, NLOC <= 27)
+constexpr int kCgRegThreads = 256;
+
+template <int D, int P, int NC, int PH, int MODE>
+__global__ void __launch_bounds__(MODE == 2 ? kCgRegThreads : CellKernel<D, P, NC, PH>::NTHREADS)
+    k_coarse_cg(CgArgs a) {
   using CK = CellKernel<D, P, NC, PH>;
+  constexpr bool RES = MODE == 1;
   extern __shared__ double sm[];
   __shared__ double red[2 * 32 + 2];
   cg::grid_group grid = cg::this_grid();
@@ -191,6 +294,7 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
     __syncthreads();
   }
   const int64_t i0 = a.n * rank / nrank, i1 = a.n * (rank + 1) / nrank;
+  unsigned long long* trace = (a.trace && rank == 0 && tid == 0) ? a.trace : nullptr;
   unsigned long long ep = __ldcg(a.solve_epoch);  // epochs of this solve start after the last one
 
   double srr = 0.0, srz = 0.0;
@@ -207,9 +311,8 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
     srz += bi * zi;
   }
   block_sum2(srr, srz, red);
-  ++ep;
   double rr = srr, rz = srz;
-  exchange(a.slots + (ep & 1) * nrank, rank, nrank, ep, rr, rz, red + 64);
+  barrier_sum(a.barrier, a.slots, a.result, rank, nrank, ep, rr, rz, red + 64);
   const double norm0 = sqrt(rr);
   int status_it = 0, status_conv = 0, status_err = 0;
   if (norm0 == 0.0) {
@@ -221,9 +324,16 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
     for (int it = 1; it <= a.max_iter; ++it) {
       const int cur = it & 1, prv = cur ^ 1;
       const CgSrc src{a.z, a.p[prv], beta};
+      if (trace) trace[it * 8 + 0] = gtimer();
       // phase A: Ap = A p with p formed on the fly; cell energies
       double e = 0.0;
-      if constexpr (RES) {
+      if constexpr (MODE == 2) {
+        if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported) {
+          const int nw = nth >> 5, w = tid >> 5;
+          for (int64_t blk = (int64_t)rank * nw + w; blk < a.nblk; blk += (int64_t)nrank * nw)
+            e += CellReg<D, P>::template run<false, true>(a.tab, src, a.ap[cur], a.idx, a.geo, blk, tid & 31);
+        }
+      } else if constexpr (RES) {
         e = CK::template run<true>(a.tab, src, a.ap[cur], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
                                    [] __device__() { __syncthreads(); });
       } else {
@@ -240,8 +350,9 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
       }
       double dummy = 0.0;
       block_sum2(e, dummy, red);
-      ++ep;
-      exchange(a.slots + (ep & 1) * nrank, rank, nrank, ep, e, dummy, red + 64);
+      if (trace) trace[it * 8 + 1] = gtimer();
+      barrier_sum(a.barrier, a.slots, a.result, rank, nrank, ep, e, dummy, red + 64);
+      if (trace) trace[it * 8 + 2] = gtimer();
       const double pap = e;
       if (!(pap > 0.0)) {
         status_it = it;
@@ -252,21 +363,41 @@ __global__ void __launch_bounds__(CellKernel<D, P, NC, PH>::NTHREADS) k_coarse_c
       // phase B
       srr = 0.0;
       srz = 0.0;
-      for (int64_t i = i0 + tid; i < i1; i += nth) {
-        a.x[i] = a.x[i] + alpha * a.p[cur][i];
-        const double ri = a.r[i] - alpha * __ldcg(a.ap[cur] + i);
-        const double zi = a.inv_diag[i] * ri;
-        a.r[i] = ri;
-        a.z[i] = zi;
-        a.ap[prv][i] = 0.0;
-        srr += ri * ri;
-        srz += ri * zi;
+      // batched by 4 so that four elements' loads are in flight per thread
+      for (int64_t i = i0 + tid; i < i1; i += 4 * (int64_t)nth) {
+        double xv[4], pv[4], rv[4], av[4], dv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = i + k * (int64_t)nth;
+          if (j < i1) {
+            xv[k] = a.x[j];
+            pv[k] = a.p[cur][j];
+            rv[k] = a.r[j];
+            av[k] = __ldcg(a.ap[cur] + j);
+            dv[k] = a.inv_diag[j];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = i + k * (int64_t)nth;
+          if (j < i1) {
+            a.x[j] = xv[k] + alpha * pv[k];
+            const double ri = rv[k] - alpha * av[k];
+            const double zi = dv[k] * ri;
+            a.r[j] = ri;
+            a.z[j] = zi;
+            a.ap[prv][j] = 0.0;
+            srr += ri * ri;
+            srz += ri * zi;
+          }
+        }
       }
       block_sum2(srr, srz, red);
-      ++ep;
       double rz_new = srz;
       rr = srr;
-      exchange(a.slots + (ep & 1) * nrank, rank, nrank, ep, rr, rz_new, red + 64);
+      if (trace) trace[it * 8 + 3] = gtimer();
+      barrier_sum(a.barrier, a.slots, a.result, rank, nrank, ep, rr, rz_new, red + 64);
+      if (trace) trace[it * 8 + 4] = gtimer();
       if (sqrt(rr) <= target) {
         status_it = it;
         status_conv = 1;
@@ -300,23 +431,43 @@ struct CgLaunch {
       int nsm = 0, dev = 0;
       NNMG_CUDA_TRY(cudaGetDevice(&dev));
       NNMG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      // register variant (Laplace, low order): 8 cell blocks per CTA
+      C.resident = false;
+      C.mode = -1;
+      const char* ek = getenv("NNMG_APPLY_KERNEL");
+      const bool allow_reg = !(ek && std::string(ek) == "pencil");
+      if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported) {
+        if (allow_reg) {
+          auto kg = k_coarse_cg<D, P, NC, PH, 2>;
+          int per_sm = 0;
+          NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kg, kCgRegThreads, 0));
+          if (per_sm > 0) {
+            C.mode = 2;
+            C.block = kCgRegThreads;
+            C.smem = 0;
+            const int64_t want = std::max<int64_t>(1, (L.nblk + kCgRegThreads / 32 - 1) / (kCgRegThreads / 32));
+            C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
+          }
+        }
+      }
       // resident variant: one CTA per cell block with its tables in smem
       const size_t res_smem =
           CK::SMEM + size_t(CK::NLOC) * CK::NG * CK::CB * sizeof(double) + size_t(CK::NLOC) * CK::CB * sizeof(int);
-      C.resident = false;
-      if (res_smem <= 200 * 1024) {
-        auto kr = k_coarse_cg<D, P, NC, PH, true>;
+      if (C.mode < 0 && res_smem <= 200 * 1024) {
+        auto kr = k_coarse_cg<D, P, NC, PH, 1>;
         NNMG_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         int per_sm = 0;
         NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kr, C.block, res_smem));
         if (per_sm > 0 && L.nblk <= int64_t(per_sm) * nsm) {
           C.resident = true;
+          C.mode = 1;
           C.smem = res_smem;
           C.nrank = static_cast<int>(L.nblk);
         }
       }
-      if (!C.resident) {
-        auto kern = k_coarse_cg<D, P, NC, PH, false>;
+      if (C.mode < 0) {
+        C.mode = 0;
+        auto kern = k_coarse_cg<D, P, NC, PH, 0>;
         C.smem = CK::SMEM;
         NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
         int per_sm = 0;
@@ -326,14 +477,20 @@ struct CgLaunch {
         const int64_t want = std::max<int64_t>(1, L.nblk);
         C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
       }
-      C.part.alloc(2 * 4 * size_t(C.nrank));  // 2 banks of 32-byte slots
+      C.part.alloc(4 * (2 * size_t(C.nrank) + 2));  // 2 banks of 32-byte slots + 2 result slots
+      if (const char* e = getenv("NNMG_COARSE_BARRIER")) C.barrier = atoi(e);
+      if (getenv("NNMG_COARSE_TRACE")) {
+        C.trace.alloc(8 * 64);
+        C.trace.zero();
+      }
       C.part.zero();
       C.epoch.alloc(1);
       C.epoch.zero();
       NNMG_CUDA_TRY(cudaDeviceSynchronize());
       return;
     }
-    auto kern = C.resident ? k_coarse_cg<D, P, NC, PH, true> : k_coarse_cg<D, P, NC, PH, false>;
+    auto kern = C.mode == 2 ? k_coarse_cg<D, P, NC, PH, 2>
+                            : (C.mode == 1 ? k_coarse_cg<D, P, NC, PH, 1> : k_coarse_cg<D, P, NC, PH, 0>);
     CgArgs a;
     a.tab = L.tab;
     a.idx = L.idx.ptr;
@@ -354,6 +511,9 @@ struct CgLaunch {
     a.ap[0] = C.ap.ptr;
     a.ap[1] = C.ap.ptr + L.n_dofs;
     a.slots = reinterpret_cast<Slot*>(C.part.ptr);
+    a.result = reinterpret_cast<Slot*>(C.part.ptr) + 2 * C.nrank;
+    a.barrier = C.barrier;
+    a.trace = C.trace.n ? C.trace.ptr : nullptr;
     a.solve_epoch = reinterpret_cast<unsigned long long*>(C.epoch.ptr);
     a.reduction = C.reduction;
     a.max_iter = C.max_iter;
@@ -419,6 +579,27 @@ void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
   *iterations = st[0];
   *converged = st[1];
   *error = st[2];
+  if (C.trace.n) {
+    std::vector<unsigned long long> t(C.trace.n);
+    NNMG_CUDA_TRY(cudaMemcpy(t.data(), C.trace.ptr, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    const int n = std::min(st[0], 63);
+    double ph[4] = {0, 0, 0, 0}, tot = 0;
+    int cnt = 0;
+    for (int it = 2; it < n; ++it) {
+      const unsigned long long* r = &t[it * 8];
+      ph[0] += double(r[1] - r[0]);
+      ph[1] += double(r[2] - r[1]);
+      ph[2] += double(r[3] - r[2]);
+      ph[3] += double(r[4] - r[3]);
+      tot += double(t[(it + 1) * 8] - r[0]);
+      ++cnt;
+    }
+    if (cnt)
+      fprintf(stderr,
+              "[nnmg coarse trace] barrier=%d ctas=%d resident=%d per-iteration ns: applyA %.0f barrierA %.0f "
+              "phaseB %.0f barrierB %.0f total %.0f\n",
+              C.barrier, C.nrank, int(C.resident), ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt, tot / cnt);
+  }
 }
 
 }  // namespace nnmg

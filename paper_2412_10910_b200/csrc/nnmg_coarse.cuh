@@ -15,6 +15,9 @@ struct Coarse {
   DevBuf<int> status;  // iterations, converged, error
   int nrank = 1, nsub = 1, block = 0;
   bool resident = false;  // cell-block tables kept in shared memory
+  int mode = 0;           // 0 pencil, 1 pencil resident, 2 register kernel
+  int barrier = 0;        // 0 grid.sync, 1 all-to-all slots, 2 root broadcast (NNMG_COARSE_BARRIER)
+  DevBuf<unsigned long long> trace;  // NNMG_COARSE_TRACE: per-phase timestamps of CTA 0
   size_t smem = 0;
 };
 

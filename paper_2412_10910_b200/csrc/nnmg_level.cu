@@ -2,6 +2,7 @@
 #include "nnmg_level.cuh"
 #include "nnmg_kernels.cuh"
 #include "nnmg_cellkernel.cuh"
+#include "nnmg_cellreg.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -260,6 +261,12 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     L->lam = lam;
     L->mu = mu;
     L->tab = make_tables(degree);
+    {
+      const char* e = getenv("NNMG_APPLY_KERNEL");
+      L->reg_kernel = !(e && std::string(e) == "pencil");
+      const char* m = getenv("NNMG_REG_MINB");
+      L->reg_minb = m ? atoi(m) : 1;
+    }
     // constraints: the kernels support whole-node constraints (every component
     // of a scalar DoF), which is what dirichlet_constraints produces
     L->scalar_constrained.assign(n_scalar, 0);
@@ -333,6 +340,16 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
   return L;
 }
 
+// one warp per cell block, one thread per cell (register-resident kernel)
+template <int D, int P, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const double* __restrict__ src, double* __restrict__ dst,
+                                                   const int* __restrict__ idx, const double* __restrict__ geo,
+                                                   int64_t b0, int64_t b1) {
+  const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (blk >= b1) return;
+  CellReg<D, P>::template run<true, false>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
+}
+
 struct ApplyLaunch {
   const Level& L;
   const double* src;
@@ -342,6 +359,20 @@ struct ApplyLaunch {
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
+    if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported) {
+      if (L.reg_kernel) {
+        const int64_t nb = b1 - b0;
+        constexpr int kWarpsPerCta = 4;
+        const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
+        if (L.reg_minb >= 4)
+          k_apply_reg<D, P, 4><<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
+        else
+          k_apply_reg<D, P, 1><<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
+        NNMG_CHECK_LAUNCH();
+        count_launch();
+        return;
+      }
+    }
     auto kern = k_apply<D, P, NC, PH>;
     static bool attr = false;
     if (!attr) {

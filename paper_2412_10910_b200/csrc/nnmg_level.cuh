@@ -22,6 +22,8 @@ struct Level {
   DevBuf<double> diag;   // cached exact diagonal (constrained = 1)
   DevBuf<double> inv_diag;
   bool diag_ready = false;
+  bool reg_kernel = true;  // register-resident thread-per-cell apply where supported
+  int reg_minb = 1;        // min CTAs/SM launch bound of that kernel (4 caps registers at 128: spills)
   std::vector<int> cell_dofs_host;  // plain (nc, nloc) copy for transfer setup
   std::vector<uint8_t> scalar_constrained;  // per scalar DoF
 };
