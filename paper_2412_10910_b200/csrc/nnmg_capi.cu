@@ -85,9 +85,9 @@ int nnmg_level_apply(nnmg_level_t level, const double* src, double* dst, void* s
 int nnmg_level_residual(nnmg_level_t level, const double* f, const double* x, double* r, void* stream) {
   return guard([&] {
     REQUIRE_HANDLE(level);
-    NNMG_REQUIRE(r != f, kInvalidArgument, "residual output must not alias f");
-    level_apply(*LV(level), x, r, S(stream));
-    sub(LV(level)->n_dofs, f, r, r, S(stream));
+    NNMG_REQUIRE(r != f && r != x, kInvalidArgument, "residual output must not alias f or x");
+    NNMG_CUDA_TRY(cudaMemcpyAsync(r, f, sizeof(double) * LV(level)->n_dofs, cudaMemcpyDeviceToDevice, S(stream)));
+    level_apply_sub(*LV(level), x, r, S(stream));
   });
 }
 

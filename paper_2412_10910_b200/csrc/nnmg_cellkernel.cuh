@@ -67,7 +67,8 @@ struct CellKernel {
   // cell energy sum_l u_l (A_K u)_l over its x-pencil (zero-in applied), so
   // that p.Ap can be formed without waiting for the scatter to complete.
   // kRes: idx/geo point at a shared-memory copy of this block's tables
-  template <bool kRes = false, class Src, class Sync>
+  // kNeg: scatter -A_K u (dst -= A u, used to update residuals in place)
+  template <bool kRes = false, bool kNeg = false, class Src, class Sync>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
@@ -234,7 +235,7 @@ struct CellKernel {
       if (gi[i] >= 0) {
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
-          atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, v[c][i]);
+          atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, kNeg ? -v[c][i] : v[c][i]);
           energy = fma(u0[c][i], v[c][i], energy);
         }
       }

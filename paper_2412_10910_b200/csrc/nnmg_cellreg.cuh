@@ -56,7 +56,7 @@ struct CellReg {
   }
 
   // Laplace only.  Returns the thread's cell energy sum_l u_l (A_K u)_l.
-  template <bool kStream, bool kEnergy, class Src>
+  template <bool kStream, bool kEnergy, bool kNeg = false, class Src>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, int lane) {
@@ -123,7 +123,7 @@ struct CellReg {
       // the index table is re-read (L1/L2 hit) rather than kept live
       const int g = kStream ? __ldg(ib + l * CB) : ib[l * CB];
       if (g >= 0) {
-        atomicAdd(dst + g, w[l]);
+        atomicAdd(dst + g, kNeg ? -w[l] : w[l]);
         if constexpr (kEnergy) energy = fma(u0[l], w[l], energy);
       }
     }

@@ -434,8 +434,11 @@ struct CgLaunch {
       // register variant (Laplace, low order): 8 cell blocks per CTA
       C.resident = false;
       C.mode = -1;
-      const char* ek = getenv("NNMG_APPLY_KERNEL");
-      const bool allow_reg = !(ek && std::string(ek) == "pencil");
+      // measured on B200 (C2/C3 coarse): the pencil kernel spreads a cell over
+      // N1^(d-1) threads and wins on this latency-bound level; the register
+      // kernel only on request
+      const char* ek = getenv("NNMG_COARSE_MODE");
+      const bool allow_reg = ek && std::string(ek) == "2";
       if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported) {
         if (allow_reg) {
           auto kg = k_coarse_cg<D, P, NC, PH, 2>;

@@ -85,13 +85,14 @@ __global__ void k_geometry(const double* __restrict__ verts, const int* __restri
   }
 }
 
-template <int DIM, int P, int NCOMP, int PHYS>
+template <int DIM, int P, int NCOMP, int PHYS, bool NEG>
 __global__ void __launch_bounds__(CellKernel<DIM, P, NCOMP, PHYS>::NTHREADS)
     k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
             const double* __restrict__ geo, int64_t b0, double lam, double mu) {
   extern __shared__ double sm[];
-  CellKernel<DIM, P, NCOMP, PHYS>::run(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x, lam, mu, sm, threadIdx.x,
-                                       [] __device__() { __syncthreads(); });
+  CellKernel<DIM, P, NCOMP, PHYS>::template run<false, NEG>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x, lam,
+                                                            mu, sm, threadIdx.x,
+                                                            [] __device__() { __syncthreads(); });
 }
 
 // ---------------------------------------------------------------------------
@@ -341,13 +342,13 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
 }
 
 // one warp per cell block, one thread per cell (register-resident kernel)
-template <int D, int P, int MINB>
+template <int D, int P, int MINB, bool NEG>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const double* __restrict__ src, double* __restrict__ dst,
                                                    const int* __restrict__ idx, const double* __restrict__ geo,
                                                    int64_t b0, int64_t b1) {
   const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= b1) return;
-  CellReg<D, P>::template run<true, false>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
+  CellReg<D, P>::template run<true, false, NEG>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
 }
 
 struct ApplyLaunch {
@@ -356,6 +357,7 @@ struct ApplyLaunch {
   double* dst;
   int64_t b0, b1;
   cudaStream_t s;
+  bool neg;
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
@@ -364,19 +366,21 @@ struct ApplyLaunch {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
-        if (L.reg_minb >= 4)
-          k_apply_reg<D, P, 4><<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
-        else
-          k_apply_reg<D, P, 1><<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
+        auto kr = neg ? (L.reg_minb >= 4 ? k_apply_reg<D, P, 4, true> : k_apply_reg<D, P, 1, true>)
+                      : (L.reg_minb >= 4 ? k_apply_reg<D, P, 4, false> : k_apply_reg<D, P, 1, false>);
+        kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;
       }
     }
-    auto kern = k_apply<D, P, NC, PH>;
+    auto kern = neg ? k_apply<D, P, NC, PH, true> : k_apply<D, P, NC, PH, false>;
     static bool attr = false;
     if (!attr) {
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK::SMEM));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)CK::SMEM));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)CK::SMEM));
       attr = true;
     }
     const int64_t nb = b1 - b0;
@@ -389,10 +393,28 @@ struct ApplyLaunch {
   }
 };
 
-void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1, cudaStream_t s) {
+void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1, cudaStream_t s,
+                        bool negate) {
   if (b1 <= b0) return;
-  ApplyLaunch f{L, src, dst, b0, b1, s};
+  ApplyLaunch f{L, src, dst, b0, b1, s, negate};
   dispatch(L.dim, L.degree, L.ncomp, L.physics, f);
+}
+
+__global__ void k_sub_constrained(const int* __restrict__ cd, int64_t n, const double* __restrict__ src,
+                                  double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[cd[i]] -= src[cd[i]];
+}
+
+void level_apply_sub(Level& L, const double* src, double* dst, cudaStream_t s) {
+  NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
+  launch_apply_cells(L, src, dst, 0, L.nblk, s, true);
+  const int64_t n = static_cast<int64_t>(L.cdofs.n);
+  if (n) {
+    k_sub_constrained<<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+  }
 }
 
 void launch_copy_constrained(const Level& L, const double* src, double* dst, cudaStream_t s) {
@@ -420,7 +442,7 @@ void level_load_vector(Level& L, const double* f, double* b, cudaStream_t s) {
 void level_apply(Level& L, const double* src, double* dst, cudaStream_t s) {
   NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
   NNMG_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * L.n_dofs, s));
-  launch_apply_cells(L, src, dst, 0, L.nblk, s);
+  launch_apply_cells(L, src, dst, 0, L.nblk, s, false);
   launch_copy_constrained(L, src, dst, s);
 }
 

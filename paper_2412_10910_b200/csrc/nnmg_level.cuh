@@ -44,7 +44,9 @@ void level_load_vector(Level& L, const double* f, double* b, cudaStream_t s);
 
 // launch the raw cell kernel (no zeroing, no constraint fix-up) over cell blocks [b0, b1)
 void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1,
-                        cudaStream_t s);
+                        cudaStream_t s, bool negate = false);
+// dst -= A src (constrained rows: dst[c] -= src[c]); no zeroing pass
+void level_apply_sub(Level& L, const double* src, double* dst, cudaStream_t s);
 void launch_copy_constrained(const Level& L, const double* src, double* dst, cudaStream_t s);
 
 }  // namespace nnmg

@@ -15,21 +15,23 @@ void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const 
   const int64_t n = L.n_dofs;
   double* r = work;
   double* d = work + n;
-  double* t = work + 2 * n;
   const double theta = (lam_max + lam_min) / 2.0;
   const double delta = (lam_max - lam_min) / 2.0;
   const double sigma = theta / delta;
+  // residual form: the apply scatters -A(.) straight into r (no zeroing pass,
+  // no separate A d vector); same recurrence as solvers.py:94-107
   if (x0 == nullptr) {
-    cheb_start(n, b, nullptr, nullptr, L.inv_diag.ptr, theta, r, d, x, s);
+    cheb_init(n, b, nullptr, L.inv_diag.ptr, theta, r, d, x, s);
   } else {
-    level_apply(L, x0, t, s);
-    cheb_start(n, b, t, x0, L.inv_diag.ptr, theta, r, d, x, s);
+    NNMG_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    level_apply_sub(L, x0, r, s);
+    cheb_init(n, b, x0, L.inv_diag.ptr, theta, r, d, x, s);
   }
   double rho_old = 1.0 / sigma;
   for (int k = 0; k < degree - 1; ++k) {
-    level_apply(L, d, t, s);
+    level_apply_sub(L, d, r, s);
     const double rho = 1.0 / (2.0 * sigma - rho_old);
-    cheb_step(n, t, L.inv_diag.ptr, rho * rho_old, 2.0 * rho / delta, r, d, x, s);
+    cheb_update(n, L.inv_diag.ptr, rho * rho_old, 2.0 * rho / delta, r, d, x, s);
     rho_old = rho;
   }
 }
@@ -94,8 +96,8 @@ static void cycle(VCycle& V, int l, const double* f, double* x, cudaStream_t s) 
     smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, k == 0 ? nullptr : x, x, w, s);
   if (V.m1 == 0) NNMG_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * L.n_dofs, s));
   double* r = V.r[l].ptr;
-  level_apply(L, x, r, s);
-  sub(L.n_dofs, f, r, r, s);
+  NNMG_CUDA_TRY(cudaMemcpyAsync(r, f, sizeof(double) * L.n_dofs, cudaMemcpyDeviceToDevice, s));
+  level_apply_sub(L, x, r, s);
   transfer_restrict(T, r, V.f[l - 1].ptr, s);
   cycle(V, l - 1, V.f[l - 1].ptr, V.x[l - 1].ptr, s);
   transfer_prolongate(T, V.x[l - 1].ptr, x, true, s);

@@ -34,6 +34,52 @@ __global__ void k_cheb_step(int64_t n, const double* __restrict__ ad, const doub
   x[i] += di;
 }
 
+// In-place residual form: the apply scatters -A d straight into r.
+// x0 == nullptr: r = b, d = inv_diag*b/theta, x = d
+// otherwise r already holds b - A x0: d = inv_diag*r/theta, x = x0 + d
+__global__ void k_cheb_init(int64_t n, const double* __restrict__ b, const double* x0,
+                            const double* __restrict__ inv_diag, double theta, double* __restrict__ r,
+                            double* __restrict__ d, double* x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ri;
+  if (x0) {
+    ri = r[i];
+  } else {
+    ri = b[i];
+    r[i] = ri;
+  }
+  const double di = inv_diag[i] * ri / theta;
+  d[i] = di;
+  x[i] = x0 ? x0[i] + di : di;
+}
+
+// r already holds r - A d: d = c1 d + c2 inv_diag r; x += d
+__global__ void k_cheb_update(int64_t n, const double* __restrict__ inv_diag, double c1, double c2,
+                              const double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = c1 * d[i] + c2 * (inv_diag[i] * r[i]);
+  d[i] = di;
+  x[i] += di;
+}
+
+void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_diag, double theta, double* r,
+               double* d, double* x, cudaStream_t s) {
+  if (!n) return;
+  k_cheb_init<<<grid_for(n), kBS, 0, s>>>(n, b, x0, inv_diag, theta, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,
+                 cudaStream_t s) {
+  if (!n) return;
+  k_cheb_update<<<grid_for(n), kBS, 0, s>>>(n, inv_diag, c1, c2, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
 // y = alpha*x + beta*y  (general axpby; beta==0 ignores y's content)
 __global__ void k_axpby(int64_t n, double alpha, const double* __restrict__ x, double beta, double* __restrict__ y) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
