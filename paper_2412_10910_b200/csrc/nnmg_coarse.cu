@@ -459,6 +459,8 @@ struct CgLaunch {
       if (C.mode < 0 && res_smem <= 200 * 1024) {
         auto kr = k_coarse_cg<D, P, NC, PH, 1>;
         NNMG_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
+        NNMG_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           cudaSharedmemCarveoutMaxShared));
         int per_sm = 0;
         NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kr, C.block, res_smem));
         if (per_sm > 0 && L.nblk <= int64_t(per_sm) * nsm) {
