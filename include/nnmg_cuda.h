@@ -87,6 +87,15 @@ int nnmg_level_load_vector(nnmg_level_t level, const double* f_host, double* b_d
 int nnmg_smoother_sweep(nnmg_level_t level, double lam_max, double lam_min, int degree, const double* b_dev,
                         const double* x0_dev, double* x_dev, double* work_dev, void* stream);
 
+/* fused Chebyshev vector updates for externally applied operators (the
+ * distributed smoother): start  r = b - Ax (ax may be NULL: r = b),
+ * d = inv_diag*r/theta, x = x0 + d (x0 may be NULL);  step  r -= Ad,
+ * d = c1 d + c2 inv_diag r, x += d   (solvers.py:94-107) */
+int nnmg_cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag,
+                    double theta, double* r, double* d, double* x, void* stream);
+int nnmg_cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
+                   double* x, void* stream);
+
 /* ---- vector kernels used by cg_solve (solvers.py:129-164) ---------------- */
 /* out_dev[0] = a.b, out_dev[1] = c.d (c may be NULL); deterministic.
  * work_dev: nnmg_dot_workspace() doubles */

@@ -49,6 +49,9 @@ _SIGNATURES = {
     "nnmg_level_diagonal": [_handle, c_void_p, c_void_p],
     "nnmg_level_load_vector": [_handle, c_void_p, c_void_p, c_void_p],
     "nnmg_smoother_sweep": [_handle, c_double, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "nnmg_cheb_start": [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p, c_void_p,
+                        c_void_p],
+    "nnmg_cheb_step": [c_int64, c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_dot_workspace": [],
     "nnmg_dot2": [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_axpby": [c_int64, c_double, c_void_p, c_double, c_void_p, c_void_p],

@@ -125,6 +125,16 @@ int nnmg_smoother_sweep(nnmg_level_t level, double lam_max, double lam_min, int 
   });
 }
 
+int nnmg_cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag,
+                    double theta, double* r, double* d, double* x, void* stream) {
+  return guard([&] { cheb_start(n, b, ax, x0, inv_diag, theta, r, d, x, S(stream)); });
+}
+
+int nnmg_cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
+                   double* x, void* stream) {
+  return guard([&] { cheb_step(n, ad, inv_diag, c1, c2, r, d, x, S(stream)); });
+}
+
 int nnmg_dot_workspace(void) { return static_cast<int>(dot_workspace_doubles()); }
 
 int nnmg_dot2(int64_t n, const double* a, const double* b, const double* c, const double* d, double* out,
