@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solve", action="store_true", help="also run the full PCG solve and report it")
     ap.add_argument("--profile", action="store_true", help="profiler range around one cycle + hot kernels, then exit")
+    ap.add_argument("--distributed", action="store_true", help="use the cell-partitioned path even on one rank")
     return ap.parse_args()
 
 
@@ -488,7 +489,7 @@ def main():
     cfg = get_config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)
-    elif dist_env()[1] > 1:
+    elif dist_env()[1] > 1 or args.distributed:
         run_distributed(args, cfg)
     else:
         run_ours(args, cfg)

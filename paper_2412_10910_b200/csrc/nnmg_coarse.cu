@@ -63,6 +63,7 @@ struct CgArgs {
   unsigned long long* solve_epoch;
   double reduction;
   int max_iter;
+  int nsub;     // pencil subgroups (cell blocks) per CTA
   int* status;  // iterations, converged, error
 };
 
@@ -173,6 +174,10 @@ __device__ __forceinline__ void exchange(Slot* bank, int rank, int nrank, unsign
   b = sh[1];
 }
 
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // block-wide fixed-order sum of two values; result valid in every thread
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
 #pragma unroll
@@ -274,8 +279,18 @@ __device__ __forceinline__ void barrier_sum(int kind, Slot* slots, Slot* result,
 // per cell block (Laplace, NLOC <= 27)
 constexpr int kCgRegThreads = 256;
 
+// at most max_sub() pencil subgroups per CTA.  Two only for scalar Laplace
+// (measured: the halved register budget makes the elasticity / Q4 variants
+// spill); more cell blocks than max_sub x SMs loop.
+template <int D, int P, int NC, int PH>
+__host__ __device__ constexpr int max_sub() {
+  // measured (C3 coarse, 154 cell blocks): 77 CTAs x 2 subgroups shortened the
+  // cell loop (5.0 -> 3.7 us) but lengthened the iteration (12.4 -> 14.4 us)
+  return 1;
+}
+
 template <int D, int P, int NC, int PH, int MODE>
-__global__ void __launch_bounds__(MODE == 2 ? kCgRegThreads : CellKernel<D, P, NC, PH>::NTHREADS)
+__global__ void __launch_bounds__(MODE == 2 ? kCgRegThreads : CellKernel<D, P, NC, PH>::NTHREADS * max_sub<D, P, NC, PH>())
     k_coarse_cg(CgArgs a) {
   using CK = CellKernel<D, P, NC, PH>;
   constexpr bool RES = MODE == 1;
@@ -284,15 +299,25 @@ __global__ void __launch_bounds__(MODE == 2 ? kCgRegThreads : CellKernel<D, P, N
   cg::grid_group grid = cg::this_grid();
   const int rank = blockIdx.x, nrank = gridDim.x;
   const int tid = threadIdx.x, nth = blockDim.x;
+  // pencil modes: the CTA holds a.nsub independent subgroups of CK::NTHREADS
+  // threads, each owning one cell block (named barriers 1..nsub), so that
+  // every cell block of the level is processed in a single round
+  const int sub = tid / CK::NTHREADS, stid = tid % CK::NTHREADS;
   constexpr int64_t kGeoChunk = int64_t(CK::NLOC) * CK::NG * CK::CB;
   constexpr int64_t kIdxChunk = int64_t(CK::NLOC) * CK::CB;
-  double* geo_s = sm + CK::SMEM / sizeof(double);
+  constexpr size_t kSubDoubles = CK::SMEM / sizeof(double) + (RES ? kGeoChunk + (kIdxChunk + 1) / 2 : 0);
+  double* sm_sub = sm + sub * kSubDoubles;
+  double* geo_s = sm_sub + CK::SMEM / sizeof(double);
   int* idx_s = reinterpret_cast<int*>(geo_s + kGeoChunk);
+  const int64_t my_blk = (int64_t)rank * a.nsub + sub;
   if constexpr (RES) {
-    for (int64_t k = tid; k < kGeoChunk; k += nth) geo_s[k] = a.geo[rank * kGeoChunk + k];
-    for (int64_t k = tid; k < kIdxChunk; k += nth) idx_s[k] = a.idx[rank * kIdxChunk + k];
+    if (sub < a.nsub && my_blk < a.nblk) {
+      for (int64_t k = stid; k < kGeoChunk; k += CK::NTHREADS) geo_s[k] = a.geo[my_blk * kGeoChunk + k];
+      for (int64_t k = stid; k < kIdxChunk; k += CK::NTHREADS) idx_s[k] = a.idx[my_blk * kIdxChunk + k];
+    }
     __syncthreads();
   }
+  const int bar_id = 1 + sub;
   const int64_t i0 = a.n * rank / nrank, i1 = a.n * (rank + 1) / nrank;
   unsigned long long* trace = (a.trace && rank == 0 && tid == 0) ? a.trace : nullptr;
   unsigned long long ep = __ldcg(a.solve_epoch);  // epochs of this solve start after the last one
@@ -333,21 +358,44 @@ __global__ void __launch_bounds__(MODE == 2 ? kCgRegThreads : CellKernel<D, P, N
           for (int64_t blk = (int64_t)rank * nw + w; blk < a.nblk; blk += (int64_t)nrank * nw)
             e += CellReg<D, P>::template run<false, true>(a.tab, src, a.ap[cur], a.idx, a.geo, blk, tid & 31);
         }
-      } else if constexpr (RES) {
-        e = CK::template run<true>(a.tab, src, a.ap[cur], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
-                                   [] __device__() { __syncthreads(); });
-      } else {
-        for (int64_t blk = rank; blk < a.nblk; blk += nrank)
-          e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm, tid,
-                       [] __device__() { __syncthreads(); });
+      } else if (sub < a.nsub) {
+        auto bar = [bar_id] __device__() {
+          if constexpr (CK::NTHREADS % 32 == 0)
+            named_sync(bar_id, CK::NTHREADS);
+          else
+            __syncthreads();  // nsub == 1 whenever the subgroup is not warp-aligned
+        };
+        if constexpr (RES) {
+          if (my_blk < a.nblk) e = CK::template run<true>(a.tab, src, a.ap[cur], idx_s, geo_s, 0, a.lam, a.mu, sm_sub,
+                                                          stid, bar);
+        } else {
+          for (int64_t blk = my_blk; blk < a.nblk; blk += (int64_t)nrank * a.nsub)
+            e += CK::run(a.tab, src, a.ap[cur], a.idx, a.geo, blk, a.lam, a.mu, sm_sub, stid, bar);
+        }
       }
-      for (int64_t i = i0 + tid; i < i1; i += nth) a.p[cur][i] = src(i);
+      if (trace) trace[it * 8 + 5] = gtimer();
+      // owners store p (batched: four independent L2 round trips in flight)
+      for (int64_t i = i0 + tid; i < i1; i += 4 * (int64_t)nth) {
+        double pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = i + k * (int64_t)nth;
+          if (j < i1) pv[k] = src(j);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = i + k * (int64_t)nth;
+          if (j < i1) a.p[cur][j] = pv[k];
+        }
+      }
+      if (trace) trace[it * 8 + 6] = gtimer();
       for (int64_t k = (int64_t)rank * nth + tid; k < a.ncons; k += (int64_t)nrank * nth) {
         const int c = a.cdofs[k];
         const double pc = src(c);
         a.ap[cur][c] = pc;
         e = fma(pc, pc, e);
       }
+      if (trace) trace[it * 8 + 7] = gtimer();
       double dummy = 0.0;
       block_sum2(e, dummy, red);
       if (trace) trace[it * 8 + 1] = gtimer();
@@ -453,34 +501,45 @@ struct CgLaunch {
           }
         }
       }
-      // resident variant: one CTA per cell block with its tables in smem
-      const size_t res_smem =
-          CK::SMEM + size_t(CK::NLOC) * CK::NG * CK::CB * sizeof(double) + size_t(CK::NLOC) * CK::CB * sizeof(int);
-      if (C.mode < 0 && res_smem <= 200 * 1024) {
+      // pencil modes: nsub cell blocks per CTA (named-barrier subgroups) so
+      // that all cell blocks run in one round on at most one CTA per SM
+      const int nsub_max = max_sub<D, P, NC, PH>();
+      const int nsub = static_cast<int>(std::max<int64_t>(
+          1, std::min<int64_t>(nsub_max, (L.nblk + nsm - 1) / nsm)));
+      const int64_t nrank_one_round = (L.nblk + nsub - 1) / nsub;
+      // resident variant: every subgroup keeps its cell block's tables in smem
+      const size_t sub_res = CK::SMEM + size_t(CK::NLOC) * CK::NG * CK::CB * sizeof(double) +
+                             ((size_t(CK::NLOC) * CK::CB + 1) / 2) * sizeof(double);
+      const size_t res_smem = nsub * sub_res;
+      if (C.mode < 0 && res_smem <= 200 * 1024 && !getenv("NNMG_COARSE_NO_RESIDENT")) {
         auto kr = k_coarse_cg<D, P, NC, PH, 1>;
         NNMG_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
         NNMG_CUDA_TRY(cudaFuncSetAttribute(kr, cudaFuncAttributePreferredSharedMemoryCarveout,
                                            cudaSharedmemCarveoutMaxShared));
         int per_sm = 0;
-        NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kr, C.block, res_smem));
-        if (per_sm > 0 && L.nblk <= int64_t(per_sm) * nsm) {
+        NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kr, nsub * CK::NTHREADS, res_smem));
+        if (per_sm > 0 && nrank_one_round <= int64_t(per_sm) * nsm) {
           C.resident = true;
           C.mode = 1;
           C.smem = res_smem;
-          C.nrank = static_cast<int>(L.nblk);
+          C.nsub = nsub;
+          C.block = nsub * CK::NTHREADS;
+          C.nrank = static_cast<int>(nrank_one_round);
         }
       }
       if (C.mode < 0) {
         C.mode = 0;
         auto kern = k_coarse_cg<D, P, NC, PH, 0>;
-        C.smem = CK::SMEM;
+        C.nsub = nsub;
+        C.block = nsub * CK::NTHREADS;
+        C.smem = nsub * CK::SMEM;
         NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+        NNMG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           cudaSharedmemCarveoutMaxShared));
         int per_sm = 0;
         NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C.block, C.smem));
         NNMG_REQUIRE(per_sm > 0, kCudaError, "coarse CG kernel does not fit on an SM");
-        // one CTA per cell block (single apply round), capped by co-residency
-        const int64_t want = std::max<int64_t>(1, L.nblk);
-        C.nrank = static_cast<int>(std::min<int64_t>(want, int64_t(per_sm) * nsm));
+        C.nrank = static_cast<int>(std::min<int64_t>(nrank_one_round, int64_t(per_sm) * nsm));
       }
       C.part.alloc(4 * (2 * size_t(C.nrank) + 2));  // 2 banks of 32-byte slots + 2 result slots
       if (const char* e = getenv("NNMG_COARSE_BARRIER")) C.barrier = atoi(e);
@@ -522,6 +581,7 @@ struct CgLaunch {
     a.solve_epoch = reinterpret_cast<unsigned long long*>(C.epoch.ptr);
     a.reduction = C.reduction;
     a.max_iter = C.max_iter;
+    a.nsub = C.nsub;
     a.status = C.status.ptr;
     void* params[] = {&a};
     NNMG_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(C.nrank), dim3(C.block), params, C.smem, s));
@@ -588,10 +648,13 @@ void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
     std::vector<unsigned long long> t(C.trace.n);
     NNMG_CUDA_TRY(cudaMemcpy(t.data(), C.trace.ptr, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     const int n = std::min(st[0], 63);
-    double ph[4] = {0, 0, 0, 0}, tot = 0;
+    double ph[4] = {0, 0, 0, 0}, sub[3] = {0, 0, 0}, tot = 0;
     int cnt = 0;
     for (int it = 2; it < n; ++it) {
       const unsigned long long* r = &t[it * 8];
+      sub[0] += double(r[5] - r[0]);
+      sub[1] += double(r[6] - r[5]);
+      sub[2] += double(r[7] - r[6]);
       ph[0] += double(r[1] - r[0]);
       ph[1] += double(r[2] - r[1]);
       ph[2] += double(r[3] - r[2]);
@@ -602,8 +665,10 @@ void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
     if (cnt)
       fprintf(stderr,
               "[nnmg coarse trace] barrier=%d ctas=%d resident=%d per-iteration ns: applyA %.0f barrierA %.0f "
-              "phaseB %.0f barrierB %.0f total %.0f\n",
-              C.barrier, C.nrank, int(C.resident), ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt, tot / cnt);
+              "phaseB %.0f barrierB %.0f total %.0f | applyA = cells %.0f + owners %.0f + constrained %.0f + "
+              "reduce\n",
+              C.barrier, C.nrank, int(C.resident), ph[0] / cnt, ph[1] / cnt, ph[2] / cnt, ph[3] / cnt, tot / cnt,
+              sub[0] / cnt, sub[1] / cnt, sub[2] / cnt);
   }
 }
 

@@ -52,7 +52,6 @@ def test_distributed_gpu_backend_world1(cname, scale):
         zh = H.v_cycle(b, executor=False)
         assert np.linalg.norm(zd - zh) <= 1e-10 * np.linalg.norm(zh)
         x, its, conv, _ = distributed.dist_cg_solve(fine, fine.from_global(b), DH.precondition, 1e-8)
-        res = H.solve = None
         from paper_2412_10910_b200.solvers import cg_solve
 
         ref = cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
