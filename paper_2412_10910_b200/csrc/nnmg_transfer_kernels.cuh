@@ -10,6 +10,61 @@ namespace nnmg {
 
 static constexpr int kTransferWarps = 4;  // coarse cells (one per warp) per thread block
 
+// Software-pipelined stream over a lane's points p = first, first+stride, ...
+// (< end): point indices and coordinates are loaded two points ahead and the
+// gathered fine value one point ahead, so the dependent pt_dof -> r_f[dof]
+// chain overlaps the arithmetic of the current point.
+template <int DIM, int NCOMP, int VSTRIDE = NCOMP>
+struct PointStream {
+  const int* __restrict__ pt_dof;
+  const double* __restrict__ xhat;
+  const double* __restrict__ rf;
+  int end, stride;
+  int p0, p1, p2;
+  int64_t d0, d1, d2;
+  double x0[DIM], x1[DIM], x2[DIM];
+  double v0[NCOMP], v1[NCOMP];
+
+  __device__ __forceinline__ void load_idx(int p, int64_t& d, double (&x)[DIM]) {
+    const bool ok = p < end;
+    d = ok ? __ldcs(pt_dof + p) : 0;
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) x[j] = ok ? __ldcs(xhat + (int64_t)p * DIM + j) : 0.5;
+  }
+  __device__ __forceinline__ void load_val(int p, int64_t d, double (&v)[NCOMP]) {
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) v[c] = p < end ? rf[d * VSTRIDE + c] : 0.0;
+  }
+  __device__ __forceinline__ void start(int first) {
+    p0 = first;
+    p1 = first + stride;
+    p2 = first + 2 * stride;
+    load_idx(p0, d0, x0);
+    load_idx(p1, d1, x1);
+    load_val(p0, d0, v0);
+  }
+  __device__ __forceinline__ bool valid() const { return p0 < end; }
+  // issue the next loads; call before computing on (x0, v0)
+  __device__ __forceinline__ void prefetch() {
+    load_val(p1, d1, v1);
+    load_idx(p2, d2, x2);
+  }
+  __device__ __forceinline__ void advance() {
+    p0 = p1;
+    p1 = p2;
+    p2 += stride;
+    d0 = d1;
+    d1 = d2;
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) {
+      x0[j] = x1[j];
+      x1[j] = x2[j];
+    }
+#pragma unroll
+    for (int c = 0; c < NCOMP; ++c) v0[c] = v1[c];
+  }
+};
+
 // ---------------------------------------------------------------------------
 // K6: u_f[pt] (+)= sum_l u_c[gather[pt,l]] prod_j phi_{l_j}(xhat_j)
 // (transfer.py:31-44, 87-102).  The cell's coarse values are staged once in
@@ -65,7 +120,9 @@ __global__ void __launch_bounds__(kTransferWarps * 32, 6)
     for (int c = 0; c < NCOMP; ++c) su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] : 0.0;
   }
   __syncwarp();
-  constexpr int PPL = ((DIM == 2 || N1 <= 2) && NCOMP == 1) ? 2 : 1;  // points per lane per round
+  // measured: two independent points per lane per round beat a pipelined
+  // single-point stream here (C3: 0.195 vs 0.251 ms)
+  constexpr int PPL = ((DIM == 2 || N1 <= 2) && NCOMP == 1) ? 2 : 1;
   const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
   for (int base = p0; base < p1; base += 32 * PPL) {
     int pp[PPL], dd[PPL];
@@ -123,12 +180,14 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
       double acc[NLOC];
 #pragma unroll
       for (int l = 0; l < NLOC; ++l) acc[l] = 0.0;
-      for (int p = p0 + lane; p < p1; p += 32) {
-        const int64_t dof = __ldcs(pt_dof + p);
-        const double v = rf[dof * NCOMP + c];
+      // component c of the interleaved vector: values rf[dof*NCOMP + c]
+      PointStream<DIM, 1, NCOMP> ps{pt_dof, xhat, rf + c, p1, 32};
+      for (ps.start(p0 + lane); ps.valid(); ps.advance()) {
+        ps.prefetch();
+        const double v = ps.v0[0];
         double X[DIM][N1];
 #pragma unroll
-        for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, __ldcs(xhat + (int64_t)p * DIM + j), X[j]);
+        for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, ps.x0[j], X[j]);
 #pragma unroll
         for (int l = 0; l < NLOC; ++l) {
           const int i0 = l % N1, i1 = (l / N1) % N1, i2 = l / (N1 * N1);
@@ -149,44 +208,80 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
       if (lane < NLOC) cellbuf[cell * NOUT + lane * NCOMP + c] = mine;
     }
   } else {
-    constexpr int NPL = (NOUT + 31) / 32;
-    __shared__ double sv[kTransferWarps][32][NCOMP];
-    __shared__ double sx[kTransferWarps][32][DIM][N1];
-    double acc[NPL];
+    // G lanes share a point; lane slice g owns the outermost-axis planes
+    // [g*PPG, (g+1)*PPG) of the local vector, all components, in registers.
+    // Every register index is compile-time: the per-point inner-plane table
+    // IN[i] (x, or x*y in 3D) is static, only the plane's 1D value is
+    // evaluated at a runtime node index.  32/G points per round; fixed-order
+    // butterfly over the point slots at the end.
+    constexpr int INNER = DIM == 3 ? N1 * N1 : N1;  // points per plane
+    // power of two so the xor butterfly keeps each slice's lanes together
+    constexpr int G = (N1 * INNER * NCOMP <= 64) ? 1
+                      : ((N1 + 1) / 2 * INNER * NCOMP <= 80 ? 2 : (N1 <= 4 ? 4 : 8));
+    constexpr int PPG = (N1 + G - 1) / G;             // planes per lane
+    constexpr int SLOTS = 32 / G;
+    const int slice = lane % G, slot = lane / G;
+    double acc[PPG][INNER][NCOMP];
 #pragma unroll
-    for (int k = 0; k < NPL; ++k) acc[k] = 0.0;
-    for (int start = p0; start < p1; start += 32) {
-      const int p = start + lane;
-      if (p < p1) {
-        const int64_t dof = __ldcs(pt_dof + p);
+    for (int a = 0; a < PPG; ++a)
 #pragma unroll
-        for (int c = 0; c < NCOMP; ++c) sv[warp][lane][c] = rf[dof * NCOMP + c];
+      for (int i = 0; i < INNER; ++i)
 #pragma unroll
-        for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, __ldcs(xhat + (int64_t)p * DIM + j), sx[warp][lane][j]);
-      }
-      __syncwarp();
-      const int cnt = min(32, p1 - start);
+        for (int c = 0; c < NCOMP; ++c) acc[a][i][c] = 0.0;
+    PointStream<DIM, NCOMP> ps{pt_dof, xhat, rf, p1, SLOTS};
+    for (ps.start(slot < SLOTS ? p0 + slot : p1); ps.valid(); ps.advance()) {
+      ps.prefetch();
+      {
+        const double* v = ps.v0;
+        double X[DIM - 1][N1];
 #pragma unroll
-      for (int k = 0; k < NPL; ++k) {
-        const int o = lane + 32 * k;
-        if (o < NOUT) {
-          const int l = o / NCOMP, c = o % NCOMP;
-          const int i0 = l % N1, i1 = (l / N1) % N1, i2 = l / (N1 * N1);
-          double a = acc[k];
-          for (int j = 0; j < cnt; ++j) {
-            double w = sx[warp][j][1][i1] * sx[warp][j][0][i0];
-            if constexpr (DIM == 3) w = sx[warp][j][2][i2] * w;
-            a = fma(sv[warp][j][c], w, a);
+        for (int j = 0; j < DIM - 1; ++j) lagrange_values<N1>(tab, ps.x0[j], X[j]);
+        // inner table, reference product order X1[i1] * X0[i0] (transfer.py:104-109)
+        double IN[INNER];
+#pragma unroll
+        for (int i = 0; i < INNER; ++i) IN[i] = DIM == 3 ? X[1][i / N1] * X[0][i % N1] : X[0][i];
+        const double tz = ps.x0[DIM - 1];
+#pragma unroll
+        for (int a = 0; a < PPG; ++a) {
+          const int plane = slice * PPG + a;
+          if (plane < N1) {
+            // phi_plane(tz) with a runtime node index (no register-array indexing)
+            double z = 1.0;
+#pragma unroll
+            for (int j = 0; j < N1; ++j) z *= (j == plane) ? tab.rdenom[plane < N1 ? plane : 0] : (tz - tab.nodes[j]);
+            double vz[NCOMP];
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) vz[c] = v[c] * z;
+#pragma unroll
+            for (int i = 0; i < INNER; ++i)
+#pragma unroll
+              for (int c = 0; c < NCOMP; ++c) acc[a][i][c] = fma(vz[c], IN[i], acc[a][i][c]);
           }
-          acc[k] = a;
         }
       }
-      __syncwarp();
     }
 #pragma unroll
-    for (int k = 0; k < NPL; ++k) {
-      const int o = lane + 32 * k;
-      if (o < NOUT) cellbuf[cell * NOUT + o] = acc[k];
+    for (int a = 0; a < PPG; ++a)
+#pragma unroll
+      for (int i = 0; i < INNER; ++i)
+#pragma unroll
+        for (int c = 0; c < NCOMP; ++c) {
+          double s = acc[a][i][c];
+#pragma unroll
+          for (int off = G; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+          acc[a][i][c] = s;
+        }
+    if (slot == 0) {
+#pragma unroll
+      for (int a = 0; a < PPG; ++a) {
+        const int plane = slice * PPG + a;
+        if (plane < N1) {
+#pragma unroll
+          for (int i = 0; i < INNER; ++i)
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) cellbuf[cell * NOUT + (plane * INNER + i) * NCOMP + c] = acc[a][i][c];
+        }
+      }
     }
   }
 }
