@@ -366,8 +366,8 @@ struct ApplyLaunch {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
-        auto kr = neg ? (L.reg_minb >= 4 ? k_apply_reg<D, P, 4, true> : k_apply_reg<D, P, 1, true>)
-                      : (L.reg_minb >= 4 ? k_apply_reg<D, P, 4, false> : k_apply_reg<D, P, 1, false>);
+        auto kr = neg ? (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, true> : k_apply_reg<D, P, 1, true>)
+                      : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false> : k_apply_reg<D, P, 1, false>);
         kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
         NNMG_CHECK_LAUNCH();
         count_launch();
