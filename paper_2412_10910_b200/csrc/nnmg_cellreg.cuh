@@ -55,12 +55,75 @@ struct CellReg {
     }
   }
 
+  // number of cell edge-vector components: 2^(d-1) edges per direction
+  static constexpr int NE = DIM * (1 << (DIM - 1)) * DIM;
+
+  // G = J^-1 J^-T |det J| w at a quadrature point, recomputed from the cell's
+  // edge vectors E[b][k][a] (edge k along reference direction b):
+  // J[a][b] = sum_k w_bk(xi) E[b][k][a] (the multilinear map, mesh.py:138-143),
+  // C = cofactors of J, G = C^T C * w / det.
+  __device__ __forceinline__ static void recompute_g(const Tables& tab, const double (&E)[NE], int qx, int qy, int qz,
+                                                     double (&g)[NG]) {
+    const double xi[3] = {tab.xq[qx], tab.xq[qy], DIM == 3 ? tab.xq[qz] : 0.0};
+    const double wq = tab.w[qx] * tab.w[qy] * (DIM == 3 ? tab.w[qz] : 1.0);
+    double J[DIM][DIM];
+#pragma unroll
+    for (int b = 0; b < DIM; ++b) {
+      // the other axes in increasing order
+      const int o0 = b == 0 ? 1 : 0;
+      const int o1 = b == 2 ? 1 : 2;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < (1 << (DIM - 1)); ++k) {
+          double wk = (k & 1) ? xi[o0] : 1.0 - xi[o0];
+          if constexpr (DIM == 3) wk *= (k & 2) ? xi[o1] : 1.0 - xi[o1];
+          s = fma(wk, E[(b * (1 << (DIM - 1)) + k) * DIM + a], s);
+        }
+        J[a][b] = s;
+      }
+    }
+    if constexpr (DIM == 3) {
+      double C[3][3];
+      C[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      C[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      C[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      C[1][0] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+      C[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+      C[1][2] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+      C[2][0] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+      C[2][1] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+      C[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+      const double s = wq * __drcp_rn(det);
+      int k = 0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b) g[k++] = s * (C[0][a] * C[0][b] + C[1][a] * C[1][b] + C[2][a] * C[2][b]);
+    } else {
+      const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      const double s = wq * __drcp_rn(det);
+      // cofactors: C00 = J11, C01 = -J10, C10 = -J01, C11 = J00
+      g[0] = s * (J[1][1] * J[1][1] + J[0][1] * J[0][1]);
+      g[1] = -s * (J[1][1] * J[1][0] + J[0][1] * J[0][0]);
+      g[2] = s * (J[1][0] * J[1][0] + J[0][0] * J[0][0]);
+    }
+  }
+
   // Laplace only.  Returns the thread's cell energy sum_l u_l (A_K u)_l.
-  template <bool kStream, bool kEnergy, bool kNeg = false, class Src>
+  // GEO 0: stored G;  GEO 1: G recomputed from the cell's edge vectors
+  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class Src>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
-                                               int64_t blk, int lane) {
-    if constexpr (kStream) {
+                                               int64_t blk, int lane, const double* __restrict__ edges = nullptr) {
+    double E[GEO == 1 ? NE : 1];
+    if constexpr (GEO == 1) {
+      const double* eb = edges + blk * (int64_t)NE * CB + lane;
+#pragma unroll
+      for (int e = 0; e < NE; ++e) E[e] = ld_geo<kStream>(eb + e * CB);
+    } else if constexpr (kStream) {
       // the warp's geometry chunk (32 cells, 85% of the bytes) streams into L2
       // while the gathers and interpolation sweeps run
       constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
@@ -96,20 +159,22 @@ struct CellReg {
         gy = fma(tab.Dc[qy][r], v[at(qx, r, qz)], gy);
         if constexpr (DIM == 3) gz = fma(tab.Dc[qz][r], v[at(qx, qy, r)], gz);
       }
-      const double* G = g0 + q * NG * CB;
+      double gg[NG];
+      if constexpr (GEO == 1) {
+        recompute_g(tab, E, qx, qy, qz, gg);
+      } else {
+        const double* G = g0 + q * NG * CB;
+#pragma unroll
+        for (int k = 0; k < NG; ++k) gg[k] = ld_geo<kStream>(G + k * CB);
+      }
       double fx, fy, fz = 0.0;
       if constexpr (DIM == 3) {
-        const double g00 = ld_geo<kStream>(G + 0 * CB), g01 = ld_geo<kStream>(G + 1 * CB);
-        const double g02 = ld_geo<kStream>(G + 2 * CB), g11 = ld_geo<kStream>(G + 3 * CB);
-        const double g12 = ld_geo<kStream>(G + 4 * CB), g22 = ld_geo<kStream>(G + 5 * CB);
-        fx = g00 * gx + g01 * gy + g02 * gz;
-        fy = g01 * gx + g11 * gy + g12 * gz;
-        fz = g02 * gx + g12 * gy + g22 * gz;
+        fx = gg[0] * gx + gg[1] * gy + gg[2] * gz;
+        fy = gg[1] * gx + gg[3] * gy + gg[4] * gz;
+        fz = gg[2] * gx + gg[4] * gy + gg[5] * gz;
       } else {
-        const double g00 = ld_geo<kStream>(G + 0 * CB), g01 = ld_geo<kStream>(G + 1 * CB);
-        const double g11 = ld_geo<kStream>(G + 2 * CB);
-        fx = g00 * gx + g01 * gy;
-        fy = g01 * gx + g11 * gy;
+        fx = gg[0] * gx + gg[1] * gy;
+        fy = gg[1] * gx + gg[2] * gy;
       }
       // transposed collocation derivatives, accumulated at once
 #pragma unroll

@@ -85,6 +85,10 @@ __global__ void k_geometry(const double* __restrict__ verts, const int* __restri
   }
 }
 
+template <int DIM>
+__global__ void k_edges(const double* __restrict__ verts, const int* __restrict__ cells, int64_t n_cells, int cb,
+                        double* __restrict__ edges);
+
 template <int DIM, int P, int NCOMP, int PHYS, bool NEG>
 __global__ void __launch_bounds__(CellKernel<DIM, P, NCOMP, PHYS>::NTHREADS)
     k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
@@ -267,6 +271,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       L->reg_kernel = !(e && std::string(e) == "pencil");
       const char* m = getenv("NNMG_REG_MINB");
       L->reg_minb = m ? atoi(m) : 1;
+      const char* rm = getenv("NNMG_RECOMPUTE_MOD");
+      L->recompute_mod = rm ? atoi(rm) : 0;
     }
     // constraints: the kernels support whole-node constraints (every component
     // of a scalar DoF), which is what dirichlet_constraints produces
@@ -332,6 +338,18 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     int hbad = 0;
     NNMG_CUDA_TRY(cudaMemcpy(&hbad, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost));
     NNMG_REQUIRE(hbad == 0, kGeometryError, "mesh has non-positive Jacobians");
+    // edge vectors for the hybrid-geometry register kernel (Laplace, low order)
+    if (physics == kLaplace && ncomp == 1 && L->reg_kernel && L->recompute_mod > 0 && L->nloc <= 27) {
+      const int ne = dim * (1 << (dim - 1)) * dim;
+      L->edges.alloc(size_t(L->nblk) * ne * cb);
+      L->edges.zero();
+      if (dim == 2)
+        k_edges<2><<<grid_for(n_cells, 256), 256>>>(dverts, dcells, n_cells, cb, L->edges.ptr);
+      else
+        k_edges<3><<<grid_for(n_cells, 256), 256>>>(dverts, dcells, n_cells, cb, L->edges.ptr);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+    }
     L->diag.alloc(L->n_dofs);
     L->inv_diag.alloc(L->n_dofs);
   } catch (...) {
@@ -342,13 +360,46 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
 }
 
 // one warp per cell block, one thread per cell (register-resident kernel)
-template <int D, int P, int MINB, bool NEG>
+// Hybrid geometry: cell blocks with blk % rmod == 0 recompute G from their
+// edge vectors (288 B/cell instead of 1296 B/cell of stored G), the others
+// stream the stored G; warp-uniform branch, both kinds share every SM so the
+// FP64 pipe and HBM work concurrently.  rmod == 0: stored G only.
+// Measured on B200 (C3): stored-G only 0.620 ms; recompute-only 0.700 ms;
+// in-kernel hybrids 0.67-0.72 ms (both paths in one kernel spill).  HYB is an
+// opt-in instantiation (NNMG_RECOMPUTE_MOD) so the default kernel stays lean.
+template <int D, int P, int MINB, bool NEG, bool HYB>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const double* __restrict__ src, double* __restrict__ dst,
                                                    const int* __restrict__ idx, const double* __restrict__ geo,
-                                                   int64_t b0, int64_t b1) {
+                                                   int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod) {
   const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= b1) return;
-  CellReg<D, P>::template run<true, false, NEG>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
+  if constexpr (HYB) {
+    if (blk % rmod == 0) {
+      CellReg<D, P>::template run<true, false, NEG, 1>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31, edges);
+      return;
+    }
+  }
+  CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
+}
+
+// per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
+template <int DIM>
+__global__ void k_edges(const double* __restrict__ verts, const int* __restrict__ cells, int64_t n_cells, int cb,
+                        double* __restrict__ edges) {
+  constexpr int NV = 1 << DIM, NK = 1 << (DIM - 1), NE = DIM * NK * DIM;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_cells) return;
+  const int64_t blk = c / cb, lane = c % cb;
+  for (int b = 0; b < DIM; ++b) {
+    int k = 0;
+    for (int v = 0; v < NV; ++v) {
+      if ((v >> b) & 1) continue;  // base vertex of an edge along b, others' bits ascending
+      const int64_t v0 = cells[c * NV + v], v1 = cells[c * NV + (v | (1 << b))];
+      for (int a = 0; a < DIM; ++a)
+        edges[(blk * NE + (b * NK + k) * DIM + a) * cb + lane] = verts[v1 * DIM + a] - verts[v0 * DIM + a];
+      ++k;
+    }
+  }
 }
 
 struct ApplyLaunch {
@@ -366,9 +417,13 @@ struct ApplyLaunch {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
-        auto kr = neg ? (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, true> : k_apply_reg<D, P, 1, true>)
-                      : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false> : k_apply_reg<D, P, 1, false>);
-        kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
+        const bool hyb = L.edges.ptr && L.recompute_mod > 0;
+        auto kr = hyb ? (neg ? k_apply_reg<D, P, 1, true, true> : k_apply_reg<D, P, 1, false, true>)
+                      : (neg ? (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, true, false> : k_apply_reg<D, P, 1, true, false>)
+                             : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false, false>
+                                                : k_apply_reg<D, P, 1, false, false>));
+        kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
+                                            hyb ? L.recompute_mod : 0);
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;

@@ -24,6 +24,8 @@ struct Level {
   bool diag_ready = false;
   bool reg_kernel = true;  // register-resident thread-per-cell apply where supported
   int reg_minb = 1;        // min CTAs/SM launch bound of that kernel (4 caps registers at 128: spills)
+  int recompute_mod = 0;   // hybrid geometry: blocks with blk % mod == 0 recompute G (0 = off)
+  DevBuf<double> edges;    // [nblk][d*2^(d-1)*d][cb] cell edge vectors (hybrid geometry)
   std::vector<int> cell_dofs_host;  // plain (nc, nloc) copy for transfer setup
   std::vector<uint8_t> scalar_constrained;  // per scalar DoF
 };
