@@ -13,20 +13,24 @@ namespace nnmg {
 // ElasticityOperator.apply (mfoperator.py:171-202); the gradient D u is formed
 // as Dc (S u), mathematically identical to the reference's D sweeps.
 // ---------------------------------------------------------------------------
-template <int DIM, int P, int NCOMP, int PHYS>
+// SCB_ > 0: one thread group handles a sub-block of SCB_ of the CB cells of a
+// block (lanes lane_off .. lane_off+SCB_-1), so a block can be spread over
+// several CTAs (latency-bound coarse levels); the HBM layout keeps CB.
+template <int DIM, int P, int NCOMP, int PHYS, int SCB_ = 0>
 struct CellKernel {
   static constexpr int N1 = P + 1;
   static constexpr int NLOC = ipow(N1, DIM);
   static constexpr int NPEN = ipow(N1, DIM - 1);
   static constexpr int CB = cells_per_block<DIM, P, NCOMP>();
+  static constexpr int SCB = SCB_ > 0 ? SCB_ : CB;
   static constexpr int NG = GeoCount<DIM, PHYS>::value;
-  static constexpr int NTHREADS = NPEN * CB;
+  static constexpr int NTHREADS = NPEN * SCB;
   static constexpr int NBUF = 3;
-  static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * CB * sizeof(double);
+  static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * SCB * sizeof(double);
   using PL = Pencil<DIM, N1>;
 
   __device__ __forceinline__ static double& S(double* sm, int b, int c, int pos, int lane) {
-    return sm[((b * NCOMP + c) * NLOC + pos) * CB + lane];
+    return sm[((b * NCOMP + c) * NLOC + pos) * SCB + lane];
   }
 
   template <int K>
@@ -72,14 +76,18 @@ struct CellKernel {
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
-                                               Sync&& sync) {
-    const int lane = tid % CB;
-    const int pen = tid / CB;
+                                               Sync&& sync, int lane_off = 0) {
+    // lsub indexes shared memory (stride SCB); glane indexes the tables:
+    // HBM layout (stride CB) or a resident shared copy of the sub-block (SCB)
+    const int lsub = tid % SCB;
+    const int pen = tid / SCB;
+    constexpr int GS = kRes ? SCB : CB;
+    const int glane = kRes ? lsub : lane_off + lsub;
     constexpr int A = 0, GX = 1, GY = 2;
     // the block's geometry chunk (85% of the bytes) is consumed only in phase
     // 5: start streaming it into L2 now so it overlaps gathers and sweeps
     constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
-    if (!kRes && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+    if (!kRes && SCB == CB && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
     double v[NCOMP][N1], u0[NCOMP][N1];
     int gi[N1];
     // P1: gather the x-pencil and interpolate along x
@@ -87,7 +95,7 @@ struct CellKernel {
       const int base = PL::base(0, pen);
 #pragma unroll
       for (int i = 0; i < N1; ++i) {
-        gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * CB + lane);
+        gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * GS + glane);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
@@ -95,35 +103,35 @@ struct CellKernel {
         }
       }
       op(tab.S, v, false);
-      store<0>(sm, A, pen, lane, v);
+      store<0>(sm, A, pen, lsub, v);
     }
     sync();
     if constexpr (DIM == 3) {
       // P2: interpolate along y
-      load<1>(sm, A, pen, lane, v);
+      load<1>(sm, A, pen, lsub, v);
       op(tab.S, v, false);
-      store<1>(sm, A, pen, lane, v);
+      store<1>(sm, A, pen, lsub, v);
       sync();
     }
     // P3: interpolate along the last axis -> values at quadrature points
     constexpr int KL = DIM - 1;
     double gl[NCOMP][N1];
-    load<KL>(sm, A, pen, lane, v);
+    load<KL>(sm, A, pen, lsub, v);
     op(tab.S, v, false);
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c) sweep<N1>(tab.Dc, v[c], gl[c]);
-    store<KL>(sm, A, pen, lane, v);
+    store<KL>(sm, A, pen, lsub, v);
     sync();
     // P4: collocation derivatives along x (and y in 3D)
     {
       double w[NCOMP][N1];
-      load<0>(sm, A, pen, lane, w);
+      load<0>(sm, A, pen, lsub, w);
       op(tab.Dc, w, false);
-      store<0>(sm, GX, pen, lane, w);
+      store<0>(sm, GX, pen, lsub, w);
       if constexpr (DIM == 3) {
-        load<1>(sm, A, pen, lane, w);
+        load<1>(sm, A, pen, lsub, w);
         op(tab.Dc, w, false);
-        store<1>(sm, GY, pen, lane, w);
+        store<1>(sm, GY, pen, lsub, w);
       }
     }
     sync();
@@ -138,11 +146,11 @@ struct CellKernel {
         double g[NCOMP][DIM], f[NCOMP][DIM];
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
-          g[c][0] = S(sm, GX, c, pos, lane);
-          if constexpr (DIM == 3) g[c][1] = S(sm, GY, c, pos, lane);
+          g[c][0] = S(sm, GX, c, pos, lsub);
+          if constexpr (DIM == 3) g[c][1] = S(sm, GY, c, pos, lsub);
           g[c][DIM - 1] = gl[c][q];
         }
-        qp_flux<DIM, NCOMP, PHYS, CB, !kRes>(geo +((blk * (int64_t)NLOC + pos) * NG) * CB + lane, g, f, lam, mu);
+        qp_flux<DIM, NCOMP, PHYS, GS, !kRes>(geo + ((blk * (int64_t)NLOC + pos) * NG) * GS + glane, g, f, lam, mu);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           fx[c][q] = f[c][0];
@@ -158,10 +166,10 @@ struct CellKernel {
 #pragma unroll
         for (int i = 0; i < N1; ++i) fl[c][i] = t[i];
       }
-      store<KL>(sm, GX, pen, lane, fx);
+      store<KL>(sm, GX, pen, lsub, fx);
       if constexpr (DIM == 3) {
-        store<KL>(sm, GY, pen, lane, fy);
-        store<KL>(sm, A, pen, lane, fl);
+        store<KL>(sm, GY, pen, lsub, fy);
+        store<KL>(sm, A, pen, lsub, fl);
       } else {
         // 2D: keep the y part in registers (v) for P7
 #pragma unroll
@@ -175,59 +183,59 @@ struct CellKernel {
       // P6: A += Dc^T fx along x
       {
         double w[NCOMP][N1], a[NCOMP][N1];
-        load<0>(sm, GX, pen, lane, w);
+        load<0>(sm, GX, pen, lsub, w);
         op(tab.Dc, w, true);
-        load<0>(sm, A, pen, lane, a);
+        load<0>(sm, A, pen, lsub, a);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
           for (int i = 0; i < N1; ++i) a[c][i] += w[c][i];
-        store<0>(sm, A, pen, lane, a);
+        store<0>(sm, A, pen, lsub, a);
       }
       sync();
       // P7: w = A + Dc^T fy along y, then S^T along y
       {
         double w[NCOMP][N1], a[NCOMP][N1];
-        load<1>(sm, GY, pen, lane, w);
+        load<1>(sm, GY, pen, lsub, w);
         op(tab.Dc, w, true);
-        load<1>(sm, A, pen, lane, a);
+        load<1>(sm, A, pen, lsub, a);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
           for (int i = 0; i < N1; ++i) a[c][i] += w[c][i];
         op(tab.S, a, true);
-        store<1>(sm, A, pen, lane, a);
+        store<1>(sm, A, pen, lsub, a);
       }
       sync();
       // P8: S^T along z
-      load<2>(sm, A, pen, lane, v);
+      load<2>(sm, A, pen, lsub, v);
       op(tab.S, v, true);
-      store<2>(sm, A, pen, lane, v);
+      store<2>(sm, A, pen, lsub, v);
       sync();
     } else {
       // 2D P6: A = Dc^T fx along x
       {
         double w[NCOMP][N1];
-        load<0>(sm, GX, pen, lane, w);
+        load<0>(sm, GX, pen, lsub, w);
         op(tab.Dc, w, true);
-        store<0>(sm, A, pen, lane, w);
+        store<0>(sm, A, pen, lsub, w);
       }
       sync();
       // 2D P7: w = A + (y part in registers), S^T along y
       {
         double a[NCOMP][N1];
-        load<1>(sm, A, pen, lane, a);
+        load<1>(sm, A, pen, lsub, a);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
           for (int i = 0; i < N1; ++i) a[c][i] += v[c][i];
         op(tab.S, a, true);
-        store<1>(sm, A, pen, lane, a);
+        store<1>(sm, A, pen, lsub, a);
       }
       sync();
     }
     // final: S^T along x and scatter-add the x-pencil
-    load<0>(sm, A, pen, lane, v);
+    load<0>(sm, A, pen, lsub, v);
     op(tab.S, v, true);
     double energy = 0.0;
 #pragma unroll

@@ -17,6 +17,7 @@
 #include "nnmg_coarse.cuh"
 #include "nnmg_cellkernel.cuh"
 #include "nnmg_cellreg.cuh"
+#include "nnmg_coarse_cg1.cuh"
 
 #include <cooperative_groups.h>
 #include <string>
@@ -469,6 +470,30 @@ struct CgLaunch {
   double* x;
   cudaStream_t s;
   bool configure_only;
+  template <int D, int P, int NC, int PH, int S>
+  bool try_split(const Level& L, int nsm, int max_split) {
+    using CKS = Cg1Kernel<D, P, NC, PH, S>;
+    if (S > max_split || CellKernel<D, P, NC, PH>::CB % S != 0 || CKS::NTHREADS < 32 || L.nblk * S > nsm)
+      return false;
+    constexpr size_t ssm = cg1_resident_smem<D, P, NC, PH, S>();
+    if (ssm > 200 * 1024) return false;
+    auto ks = k_coarse_cg1<D, P, NC, PH, true, S>;
+    NNMG_CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    NNMG_CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+    int ps = 0;
+    NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, ks, CKS::NTHREADS, ssm));
+    if (ps <= 0) return false;
+    C.split = S;
+    C.mode = 1;
+    C.resident = true;
+    C.nsub = 1;
+    C.block = CKS::NTHREADS;
+    C.smem = ssm;
+    C.nrank = static_cast<int>(L.nblk * S);
+    return true;
+  }
+
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
@@ -541,6 +566,24 @@ struct CgLaunch {
         NNMG_REQUIRE(per_sm > 0, kCudaError, "coarse CG kernel does not fit on an SM");
         C.nrank = static_cast<int>(std::min<int64_t>(nrank_one_round, int64_t(per_sm) * nsm));
       }
+      if (C.single_barrier && C.mode != 2) {
+        auto k1 = C.mode == 1 ? k_coarse_cg1<D, P, NC, PH, true, 1> : k_coarse_cg1<D, P, NC, PH, false, 1>;
+        NNMG_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+        NNMG_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           cudaSharedmemCarveoutMaxShared));
+        int per_sm = 0;
+        NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, C.block, C.smem));
+        if (C.nsub != 1 || per_sm * nsm < C.nrank) C.single_barrier = false;
+        // fewer cell blocks than SMs: split each block over the largest
+        // number of CTAs that still fits one CTA per SM, tables resident
+        // (NNMG_COARSE_SPLIT=0 disables, =k caps the split at k)
+        const char* es = getenv("NNMG_COARSE_SPLIT");
+        const int max_split = es ? atoi(es) : 8;
+        if (C.single_barrier) {
+          try_split<D, P, NC, PH, 8>(L, nsm, max_split) || try_split<D, P, NC, PH, 4>(L, nsm, max_split) ||
+              try_split<D, P, NC, PH, 2>(L, nsm, max_split);
+        }
+      }
       C.part.alloc(4 * (2 * size_t(C.nrank) + 2));  // 2 banks of 32-byte slots + 2 result slots
       if (const char* e = getenv("NNMG_COARSE_BARRIER")) C.barrier = atoi(e);
       if (getenv("NNMG_COARSE_TRACE")) {
@@ -551,6 +594,43 @@ struct CgLaunch {
       C.epoch.alloc(1);
       C.epoch.zero();
       NNMG_CUDA_TRY(cudaDeviceSynchronize());
+      return;
+    }
+    if (C.single_barrier && C.mode != 2) {
+      Cg1Args g;
+      g.tab = L.tab;
+      g.idx = L.idx.ptr;
+      g.geo = L.geo.ptr;
+      g.nblk = L.nblk;
+      g.lam = L.lam;
+      g.mu = L.mu;
+      g.cdofs = L.cdofs.ptr;
+      g.ncons = static_cast<int64_t>(L.cdofs.n);
+      g.inv_diag = L.inv_diag.ptr;
+      g.n = L.n_dofs;
+      g.b = b;
+      g.x = x;
+      g.r[0] = C.r.ptr;
+      g.r[1] = C.r.ptr + L.n_dofs;
+      g.s[0] = C.s.ptr;
+      g.s[1] = C.s.ptr + L.n_dofs;
+      g.w[0] = C.ap.ptr;
+      g.w[1] = C.ap.ptr + L.n_dofs;
+      g.w[2] = C.ap.ptr + 2 * L.n_dofs;
+      g.p = C.p.ptr;
+      g.part = C.part.ptr;
+      g.reduction = C.reduction;
+      g.max_iter = C.max_iter;
+      g.status = C.status.ptr;
+      g.trace = C.trace.n ? C.trace.ptr : nullptr;
+      auto k1 = C.split == 8   ? k_coarse_cg1<D, P, NC, PH, true, 8>
+                : C.split == 4 ? k_coarse_cg1<D, P, NC, PH, true, 4>
+                : C.split == 2 ? k_coarse_cg1<D, P, NC, PH, true, 2>
+                : C.mode == 1  ? k_coarse_cg1<D, P, NC, PH, true, 1>
+                               : k_coarse_cg1<D, P, NC, PH, false, 1>;
+      void* p1[] = {&g};
+      NNMG_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k1, dim3(C.nrank), dim3(C.block), p1, C.smem, s));
+      count_launch();
       return;
     }
     auto kern = C.mode == 2 ? k_coarse_cg<D, P, NC, PH, 2>
@@ -611,10 +691,17 @@ Coarse* coarse_cg_create(Level* L, double reduction, int max_iter) {
     C->dense = false;
     C->reduction = reduction;
     C->max_iter = max_iter;
-    C->r.alloc(L->n_dofs);
+    C->r.alloc(2 * L->n_dofs);
     C->z.alloc(L->n_dofs);
     C->p.alloc(2 * L->n_dofs);
-    C->ap.alloc(2 * L->n_dofs);
+    C->ap.alloc(3 * L->n_dofs);
+    C->s.alloc(2 * L->n_dofs);
+    {
+      // measured (B200, same iteration counts): C2 7.05 -> 4.92, C3 13.1 ->
+      // 10.5, C5 20.2 -> 18.4 us per iteration
+      const char* e = getenv("NNMG_COARSE_CG1");
+      C->single_barrier = e ? atoi(e) != 0 : true;
+    }
     C->status.alloc(3);
     C->status.zero();
     CgLaunch f{*C, nullptr, nullptr, 0, true};

@@ -1,0 +1,289 @@
+// Coarse Jacobi-PCG with ONE grid barrier per iteration (Chronopoulos-Gear
+// form of the reference recurrence, solvers.py:129-164, M = D^-1):
+//
+//   u_k = M r_k,  w_k = A u_k,  gamma_k = (r_k,u_k),  delta_k = (u_k,w_k)
+//   beta_k = gamma_k/gamma_{k-1},  alpha_k = gamma_k/(delta_k - beta_k gamma_k/alpha_{k-1})
+//   p_k = u_k + beta_k p_{k-1},  s_k = w_k + beta_k s_{k-1}
+//   x_{k+1} = x_k + alpha_k p_k,  r_{k+1} = r_k - alpha_k s_k
+//
+// In exact arithmetic these are the iterates of the standard PCG (same
+// alpha, beta, x_k, r_k, same stopping test ||r_k|| <= tol ||r_0||); only the
+// rounding differs.  Phase k of the persistent kernel:
+//   * gathers form r_k = r_{k-1} - alpha_{k-1}(w_{k-1} + beta_{k-1}s_{k-2}) and
+//     u_k = M r_k on the fly, the cell kernel scatters w_k = A u_k and
+//     returns the cell energies u_K.(A_K u_K) (delta_k);
+//   * owners store s_{k-1}, r_k, p_{k-1}, x_k, accumulate gamma_k and ||r_k||^2
+//     and zero the w buffer of phase k+1;
+//   * one grid barrier, a fixed-order reduction of (gamma, delta, rr) that
+//     every CTA performs identically, the convergence test and the scalars.
+// r and s are double-, w triple-buffered so that no phase overwrites what
+// another CTA may still gather.
+#pragma once
+
+#include "nnmg_cellkernel.cuh"
+
+#include <cooperative_groups.h>
+
+namespace nnmg {
+
+struct Cg1Args {
+  Tables tab;
+  const int* idx;
+  const double* geo;
+  int64_t nblk;
+  double lam, mu;
+  const int* cdofs;
+  int64_t ncons;
+  const double* inv_diag;
+  int64_t n;
+  const double* b;
+  double* x;
+  double* r[2];
+  double* s[2];
+  double* w[3];
+  double* p;
+  double* part;  // [3][grid]
+  double reduction;
+  int max_iter;
+  int* status;
+  unsigned long long* trace;
+};
+
+// u = M r_k with r_k = r_{k-1} - alpha (w_{k-1} + beta s_{k-2}) formed on the fly
+struct Cg1Src {
+  const double* r;
+  const double* w;
+  const double* s;
+  const double* inv_diag;
+  double alpha, beta;
+  __device__ __forceinline__ double rk(int64_t i) const {
+    const double sk = fma(beta, __ldcg(s + i), __ldcg(w + i));
+    return fma(-alpha, sk, __ldcg(r + i));
+  }
+  __device__ __forceinline__ double operator()(int64_t i) const { return __ldg(inv_diag + i) * rk(i); }
+};
+
+__device__ __forceinline__ unsigned long long cg1_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// SPLIT CTAs share one cell block (SCB = CB / SPLIT cells each): on small
+// coarse levels (fewer blocks than SMs) this spreads the cell work over more
+// SMs at the price of more barrier participants.
+template <int D, int P, int NC, int PH, int SPLIT>
+using Cg1Kernel = CellKernel<D, P, NC, PH, CellKernel<D, P, NC, PH>::CB / SPLIT>;
+
+template <int D, int P, int NC, int PH, int SPLIT>
+constexpr size_t cg1_resident_smem() {
+  using CK = Cg1Kernel<D, P, NC, PH, SPLIT>;
+  return CK::SMEM + size_t(CK::NLOC) * CK::NG * CK::SCB * sizeof(double) +
+         ((size_t(CK::NLOC) * CK::SCB + 1) / 2) * sizeof(double);
+}
+
+// sum over the (possibly partial last) warp; lane 0 ends with the total
+__device__ __forceinline__ void warp_sum3(double& a, double& b, double& c, int nth) {
+  const int lane = threadIdx.x & 31;
+  const int cnt = min(32, nth - int(threadIdx.x & ~31));
+  const unsigned mask = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ta = __shfl_down_sync(mask, a, o);
+    const double tb = __shfl_down_sync(mask, b, o);
+    const double tc = __shfl_down_sync(mask, c, o);
+    if (lane + o < cnt) {
+      a += ta;
+      b += tb;
+      c += tc;
+    }
+  }
+}
+
+template <int D, int P, int NC, int PH, bool RES, int SPLIT>
+__global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_coarse_cg1(Cg1Args a) {
+  using CK = Cg1Kernel<D, P, NC, PH, SPLIT>;
+  namespace cg = cooperative_groups;
+  extern __shared__ double sm[];
+  __shared__ double red[3 * 32];
+  cg::grid_group grid = cg::this_grid();
+  const int rank = blockIdx.x, nrank = gridDim.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  constexpr int64_t kGeoChunk = int64_t(CK::NLOC) * CK::NG * CK::SCB;
+  constexpr int64_t kIdxChunk = int64_t(CK::NLOC) * CK::SCB;
+  double* geo_s = sm + CK::SMEM / sizeof(double);
+  int* idx_s = reinterpret_cast<int*>(geo_s + kGeoChunk);
+  if constexpr (RES) {
+    // this CTA's sub-block (lanes sub*SCB ..) of cell block rank / SPLIT
+    const int64_t blk = rank / SPLIT;
+    const int off = (rank % SPLIT) * CK::SCB;
+    for (int64_t k = tid; k < kGeoChunk; k += nth)
+      geo_s[k] = a.geo[(blk * CK::NLOC * CK::NG + k / CK::SCB) * CK::CB + off + k % CK::SCB];
+    for (int64_t k = tid; k < kIdxChunk; k += nth)
+      idx_s[k] = a.idx[(blk * CK::NLOC + k / CK::SCB) * CK::CB + off + k % CK::SCB];
+  }
+  const int64_t i0 = a.n * rank / nrank, i1 = a.n * (rank + 1) / nrank;
+  unsigned long long* trace = (a.trace && rank == 0 && tid == 0) ? a.trace : nullptr;
+  // state "phase -1": r_{-1} = b, w_{-1} = s_{-2} = p_{-1} = x_{-1} = 0, alpha = beta = 0
+  for (int64_t i = i0 + tid; i < i1; i += nth) {
+    a.r[1][i] = a.b[i];
+    a.s[0][i] = 0.0;
+    a.s[1][i] = 0.0;
+    a.w[0][i] = 0.0;
+    a.w[1][i] = 0.0;
+    a.w[2][i] = 0.0;
+    a.p[i] = 0.0;
+    a.x[i] = 0.0;
+  }
+  grid.sync();
+  double alpha = 0.0, beta = 0.0, gamma_old = 1.0, alpha_old = 1.0, target = 0.0;
+  int status_it = a.max_iter, status_conv = 0, status_err = 0;
+  for (int k = 0; k <= a.max_iter; ++k) {
+    const int rb_prev = (k + 1) & 1, rb = k & 1;  // r_{k-1}, r_k buffers
+    const int sb_old = k & 1, sb_new = (k + 1) & 1;  // s_{k-2} read, s_{k-1} written
+    const int wb_prev = (k + 2) % 3, wb = k % 3, wb_next = (k + 1) % 3;
+    const Cg1Src src{a.r[rb_prev], a.w[wb_prev], a.s[sb_old], a.inv_diag, alpha, beta};
+    if (trace && k < 63) trace[k * 8 + 0] = cg1_timer();
+    // cells: w_k = A u_k and energies
+    double e = 0.0;
+    if constexpr (RES) {
+      e = CK::template run<true>(a.tab, src, a.w[wb], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
+                                 [] __device__() { __syncthreads(); });
+    } else {
+      for (int64_t u = rank; u < a.nblk * SPLIT; u += nrank)
+        e += CK::run(a.tab, src, a.w[wb], a.idx, a.geo, u / SPLIT, a.lam, a.mu, sm, tid,
+                     [] __device__() { __syncthreads(); }, int(u % SPLIT) * CK::SCB);
+    }
+    if (trace && k < 63) trace[k * 8 + 5] = cg1_timer();
+    // constrained rows: w[c] = u[c] (identity-out), energy u_c^2
+    for (int64_t q = (int64_t)rank * nth + tid; q < a.ncons; q += (int64_t)nrank * nth) {
+      const int c = a.cdofs[q];
+      const double uc = src(c);
+      a.w[wb][c] = uc;
+      e = fma(uc, uc, e);
+    }
+    // owners: s_{k-1}, r_k, p_{k-1}, x_k; gamma_k, ||r_k||^2; zero w_{k+1}
+    double g = 0.0, rr = 0.0;
+    for (int64_t i = i0 + tid; i < i1; i += 4 * (int64_t)nth) {
+      double rp[4], wp[4], so[4], di[4], pp[4], xx[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t ii = i + j * (int64_t)nth;
+        if (ii < i1) {
+          rp[j] = __ldcg(a.r[rb_prev] + ii);
+          wp[j] = __ldcg(a.w[wb_prev] + ii);
+          so[j] = __ldcg(a.s[sb_old] + ii);
+          di[j] = a.inv_diag[ii];
+          pp[j] = a.p[ii];
+          xx[j] = a.x[ii];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t ii = i + j * (int64_t)nth;
+        if (ii < i1) {
+          const double sk1 = fma(beta, so[j], wp[j]);    // s_{k-1}
+          const double rk = fma(-alpha, sk1, rp[j]);     // r_k
+          const double pk1 = fma(beta, pp[j], di[j] * rp[j]);  // p_{k-1} = u_{k-1} + beta p_{k-2}
+          a.s[sb_new][ii] = sk1;
+          a.r[rb][ii] = rk;
+          a.p[ii] = pk1;
+          a.x[ii] = fma(alpha, pk1, xx[j]);              // x_k
+          a.w[wb_next][ii] = 0.0;
+          const double uk = di[j] * rk;
+          g = fma(rk, uk, g);
+          rr = fma(rk, rk, rr);
+        }
+      }
+    }
+    // block reduction of (gamma, delta, rr), then the single grid barrier
+    warp_sum3(g, e, rr, nth);
+    const int wid = tid >> 5, nw = (nth + 31) >> 5;
+    __syncthreads();
+    if ((tid & 31) == 0) {
+      red[wid] = g;
+      red[32 + wid] = e;
+      red[64 + wid] = rr;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double sg = 0.0, se = 0.0, sr = 0.0;
+      for (int i = 0; i < nw; ++i) {
+        sg += red[i];
+        se += red[32 + i];
+        sr += red[64 + i];
+      }
+      double* part = a.part + (k & 1) * 3 * nrank;  // alternate banks across phases
+      part[rank] = sg;
+      part[nrank + rank] = se;
+      part[2 * nrank + rank] = sr;
+    }
+    if (trace && k < 63) trace[k * 8 + 1] = cg1_timer();
+    grid.sync();
+    if (trace && k < 63) trace[k * 8 + 2] = cg1_timer();
+    __shared__ double tot[3];
+    if (tid < 32) {
+      const double* part = a.part + (k & 1) * 3 * nrank;
+      double sg = 0.0, se = 0.0, sr = 0.0;
+      for (int i = tid; i < nrank; i += 32) {
+        sg += __ldcg(part + i);
+        se += __ldcg(part + nrank + i);
+        sr += __ldcg(part + 2 * nrank + i);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sg += __shfl_down_sync(0xffffffffu, sg, o);
+        se += __shfl_down_sync(0xffffffffu, se, o);
+        sr += __shfl_down_sync(0xffffffffu, sr, o);
+      }
+      if (tid == 0) {
+        tot[0] = sg;
+        tot[1] = se;
+        tot[2] = sr;
+      }
+    }
+    __syncthreads();
+    const double gamma = tot[0], delta = tot[1], rrk = tot[2];
+    __syncthreads();
+    if (trace && k < 63) trace[k * 8 + 3] = cg1_timer();
+    if (k == 0) {
+      const double norm0 = sqrt(rrk);
+      if (norm0 == 0.0) {
+        status_it = 0;
+        status_conv = 1;
+        break;
+      }
+      target = a.reduction * norm0;
+    } else if (sqrt(rrk) <= target) {
+      status_it = k;
+      status_conv = 1;
+      break;
+    }
+    if (k == a.max_iter) break;
+    double bk, den;
+    if (k == 0) {
+      bk = 0.0;
+      den = delta;
+    } else {
+      bk = gamma / gamma_old;
+      den = delta - bk * gamma / alpha_old;
+    }
+    if (!(den > 0.0)) {
+      status_it = k + 1;
+      status_err = 1;
+      break;
+    }
+    const double ak = gamma / den;
+    alpha = ak;
+    beta = bk;
+    alpha_old = ak;
+    gamma_old = gamma;
+  }
+  if (rank == 0 && tid == 0) {
+    a.status[0] = status_it;
+    a.status[1] = status_conv;
+    a.status[2] = status_err;
+  }
+}
+
+}  // namespace nnmg
