@@ -14,7 +14,8 @@ from ctypes import POINTER, c_double, c_int, c_int64, c_uint8, c_uint64, c_void_
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnnmg_cuda.so")
+# NNMG_LIB_PATH: load another build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("NNMG_LIB_PATH") or os.path.join(_HERE, "libnnmg_cuda.so")
 
 STATUS_INVALID = 1
 STATUS_CUDA = 2

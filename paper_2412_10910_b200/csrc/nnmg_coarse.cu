@@ -19,6 +19,8 @@
 #include "nnmg_cellreg.cuh"
 #include "nnmg_coarse_cg1.cuh"
 
+#include <algorithm>
+
 #include <cooperative_groups.h>
 #include <string>
 
@@ -464,6 +466,11 @@ __global__ void __launch_bounds__(MODE == 2 ? kCgRegThreads : CellKernel<D, P, N
   }
 }
 
+__global__ void k_mark_rows(const int* __restrict__ rows, int64_t n, unsigned char* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) flag[rows[i]] = 1;
+}
+
 struct CgLaunch {
   Coarse& C;
   const double* b;
@@ -473,7 +480,11 @@ struct CgLaunch {
   template <int D, int P, int NC, int PH, int S>
   bool try_split(const Level& L, int nsm, int max_split) {
     using CKS = Cg1Kernel<D, P, NC, PH, S>;
-    if (S > max_split || CellKernel<D, P, NC, PH>::CB % S != 0 || CKS::NTHREADS < 32 || L.nblk * S > nsm)
+    // CTAs per SM allowed for the split grid (NNMG_COARSE_CPS, default 1)
+    const char* ec = getenv("NNMG_COARSE_CPS");
+    const int cps = ec ? std::max(1, atoi(ec)) : 1;
+    if (S > max_split || CellKernel<D, P, NC, PH>::CB % S != 0 || CKS::NTHREADS < 32 ||
+        L.nblk * S > int64_t(cps) * nsm)
       return false;
     constexpr size_t ssm = cg1_resident_smem<D, P, NC, PH, S>();
     if (ssm > 200 * 1024) return false;
@@ -483,7 +494,7 @@ struct CgLaunch {
                                        cudaSharedmemCarveoutMaxShared));
     int ps = 0;
     NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, ks, CKS::NTHREADS, ssm));
-    if (ps <= 0) return false;
+    if (ps <= 0 || L.nblk * S > int64_t(ps) * nsm) return false;
     C.split = S;
     C.mode = 1;
     C.resident = true;
@@ -584,10 +595,18 @@ struct CgLaunch {
               try_split<D, P, NC, PH, 2>(L, nsm, max_split);
         }
       }
+      if (C.single_barrier && C.mode != 2) {
+        C.con.alloc(size_t(L.n_dofs));
+        C.con.zero();
+        if (L.cdofs.n) {
+          k_mark_rows<<<unsigned((L.cdofs.n + 255) / 256), 256>>>(L.cdofs.ptr, int64_t(L.cdofs.n), C.con.ptr);
+          NNMG_CHECK_LAUNCH();
+        }
+      }
       C.part.alloc(4 * (2 * size_t(C.nrank) + 2));  // 2 banks of 32-byte slots + 2 result slots
       if (const char* e = getenv("NNMG_COARSE_BARRIER")) C.barrier = atoi(e);
       if (getenv("NNMG_COARSE_TRACE")) {
-        C.trace.alloc(8 * 64);
+        C.trace.alloc(8 * 64 + 8 * size_t(C.nrank));
         C.trace.zero();
       }
       C.part.zero();
@@ -604,8 +623,13 @@ struct CgLaunch {
       g.nblk = L.nblk;
       g.lam = L.lam;
       g.mu = L.mu;
+      g.con = C.con.ptr;
       g.cdofs = L.cdofs.ptr;
       g.ncons = static_cast<int64_t>(L.cdofs.n);
+      {
+        const char* e = getenv("NNMG_COARSE_PREFETCH");
+        g.prefetch_owned = e ? atoi(e) : 1;
+      }
       g.inv_diag = L.inv_diag.ptr;
       g.n = L.n_dofs;
       g.b = b;
@@ -748,6 +772,25 @@ void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
       ph[3] += double(r[4] - r[3]);
       tot += double(t[(it + 1) * 8] - r[0]);
       ++cnt;
+    }
+    if (st[0] >= 16) {
+      // arrival spread at the barrier, iterations 8..15: per-CTA lateness
+      // relative to the earliest CTA, averaged
+      std::vector<double> late(C.nrank, 0.0);
+      for (int it = 0; it < 8; ++it) {
+        const unsigned long long* r = &t[8 * 64 + size_t(it) * C.nrank];
+        unsigned long long mn = r[0];
+        for (int q = 0; q < C.nrank; ++q) mn = std::min(mn, r[q]);
+        for (int q = 0; q < C.nrank; ++q) late[q] += double(r[q] - mn) / 8.0;
+      }
+      std::vector<int> order(C.nrank);
+      for (int q = 0; q < C.nrank; ++q) order[q] = q;
+      std::sort(order.begin(), order.end(), [&](int x, int y) { return late[x] > late[y]; });
+      fprintf(stderr, "[nnmg coarse trace] barrier arrival lateness ns (slowest CTAs):");
+      for (int q = 0; q < std::min(C.nrank, 8); ++q) fprintf(stderr, " %d:%.0f", order[q], late[order[q]]);
+      double mean = 0;
+      for (double v : late) mean += v / C.nrank;
+      fprintf(stderr, " | mean %.0f, CTA0 %.0f\n", mean, late[0]);
     }
     if (cnt)
       fprintf(stderr,

@@ -12,6 +12,7 @@ struct Coarse {
   int max_iter = 10000;
   DevBuf<double> r, z, p, ap, part, s;
   bool single_barrier = false;  // Chronopoulos-Gear form, one grid barrier per iteration
+  DevBuf<unsigned char> con;  // constrained-row flags (single-barrier kernel)
   DevBuf<unsigned long long> epoch;  // last barrier epoch used (persists across solves)
   DevBuf<int> status;  // iterations, converged, error
   int nrank = 1, nsub = 1, block = 0;

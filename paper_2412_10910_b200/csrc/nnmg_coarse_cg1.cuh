@@ -12,8 +12,8 @@
 //   * gathers form r_k = r_{k-1} - alpha_{k-1}(w_{k-1} + beta_{k-1}s_{k-2}) and
 //     u_k = M r_k on the fly, the cell kernel scatters w_k = A u_k and
 //     returns the cell energies u_K.(A_K u_K) (delta_k);
-//   * owners store s_{k-1}, r_k, p_{k-1}, x_k, accumulate gamma_k and ||r_k||^2
-//     and zero the w buffer of phase k+1;
+//   * owners store s_{k-1}, r_k, p_{k-1}, x_k, accumulate gamma_k and ||r_k||^2,
+//     set the constrained rows of w_k and zero the w buffer of phase k+1;
 //   * one grid barrier, a fixed-order reduction of (gamma, delta, rr) that
 //     every CTA performs identically, the convergence test and the scalars.
 // r and s are double-, w triple-buffered so that no phase overwrites what
@@ -32,8 +32,7 @@ struct Cg1Args {
   const double* geo;
   int64_t nblk;
   double lam, mu;
-  const int* cdofs;
-  int64_t ncons;
+  const unsigned char* con;  // 1 on constrained rows
   const double* inv_diag;
   int64_t n;
   const double* b;
@@ -45,6 +44,9 @@ struct Cg1Args {
   double* part;  // [3][grid]
   double reduction;
   int max_iter;
+  int prefetch_owned;  // load the owners' operands before the cell phase
+  const int* cdofs;    // constrained rows (elasticity's separate pass)
+  int64_t ncons;
   int* status;
   unsigned long long* trace;
 };
@@ -144,6 +146,32 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     const int wb_prev = (k + 2) % 3, wb = k % 3, wb_next = (k + 1) % 3;
     const Cg1Src src{a.r[rb_prev], a.w[wb_prev], a.s[sb_old], a.inv_diag, alpha, beta};
     if (trace && k < 63) trace[k * 8 + 0] = cg1_timer();
+    // owners' operands (final since the last barrier) are loaded before the
+    // cell phase so that their L2 latency overlaps it, when the owned range
+    // fits KO registers per thread (always on the split/small levels)
+    constexpr int KO = 4;
+    // (Laplace only: measured, the live registers slow elasticity's cell phase)
+    constexpr bool kPrefetch = NC == 1;
+    constexpr bool kFold = NC == 1;
+    const bool fits = kPrefetch && a.prefetch_owned && (i1 - i0) <= KO * (int64_t)nth;
+    double rp[KO], wp[KO], so[KO], di[KO], pp[KO], xx[KO];
+    bool cf[KO];
+    auto load_owned = [&](int64_t i) {
+#pragma unroll
+      for (int j = 0; j < KO; ++j) {
+        const int64_t ii = i + j * (int64_t)nth;
+        if (ii < i1) {
+          rp[j] = __ldcg(a.r[rb_prev] + ii);
+          wp[j] = __ldcg(a.w[wb_prev] + ii);
+          so[j] = __ldcg(a.s[sb_old] + ii);
+          di[j] = a.inv_diag[ii];
+          pp[j] = a.p[ii];
+          xx[j] = a.x[ii];
+          if constexpr (kFold) cf[j] = a.con[ii] != 0;
+        }
+      }
+    };
+    if (fits) load_owned(i0 + tid);
     // cells: w_k = A u_k and energies
     double e = 0.0;
     if constexpr (RES) {
@@ -155,31 +183,23 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
                      [] __device__() { __syncthreads(); }, int(u % SPLIT) * CK::SCB);
     }
     if (trace && k < 63) trace[k * 8 + 5] = cg1_timer();
-    // constrained rows: w[c] = u[c] (identity-out), energy u_c^2
-    for (int64_t q = (int64_t)rank * nth + tid; q < a.ncons; q += (int64_t)nrank * nth) {
-      const int c = a.cdofs[q];
-      const double uc = src(c);
-      a.w[wb][c] = uc;
-      e = fma(uc, uc, e);
+    // constrained rows w_k[c] = u_k[c] (identity-out, energy u_c^2; no cell
+    // scatters into them): Laplace folds them into the owners' pass below,
+    // elasticity keeps a separate spread-out pass (measured faster there)
+    if constexpr (!kFold) {
+      for (int64_t q = (int64_t)rank * nth + tid; q < a.ncons; q += (int64_t)nrank * nth) {
+        const int c = a.cdofs[q];
+        const double uc = src(c);
+        a.w[wb][c] = uc;
+        e = fma(uc, uc, e);
+      }
     }
     // owners: s_{k-1}, r_k, p_{k-1}, x_k; gamma_k, ||r_k||^2; zero w_{k+1}
     double g = 0.0, rr = 0.0;
-    for (int64_t i = i0 + tid; i < i1; i += 4 * (int64_t)nth) {
-      double rp[4], wp[4], so[4], di[4], pp[4], xx[4];
+    for (int64_t i = i0 + tid; i < i1; i += KO * (int64_t)nth) {
+      if (!fits) load_owned(i);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t ii = i + j * (int64_t)nth;
-        if (ii < i1) {
-          rp[j] = __ldcg(a.r[rb_prev] + ii);
-          wp[j] = __ldcg(a.w[wb_prev] + ii);
-          so[j] = __ldcg(a.s[sb_old] + ii);
-          di[j] = a.inv_diag[ii];
-          pp[j] = a.p[ii];
-          xx[j] = a.x[ii];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < KO; ++j) {
         const int64_t ii = i + j * (int64_t)nth;
         if (ii < i1) {
           const double sk1 = fma(beta, so[j], wp[j]);    // s_{k-1}
@@ -191,12 +211,17 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
           a.x[ii] = fma(alpha, pk1, xx[j]);              // x_k
           a.w[wb_next][ii] = 0.0;
           const double uk = di[j] * rk;
+          if (kFold && cf[j]) {
+            a.w[wb][ii] = uk;
+            e = fma(uk, uk, e);
+          }
           g = fma(rk, uk, g);
           rr = fma(rk, rk, rr);
         }
       }
     }
     // block reduction of (gamma, delta, rr), then the single grid barrier
+    if (trace && k < 63) trace[k * 8 + 7] = cg1_timer();
     warp_sum3(g, e, rr, nth);
     const int wid = tid >> 5, nw = (nth + 31) >> 5;
     __syncthreads();
@@ -219,8 +244,11 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
       part[2 * nrank + rank] = sr;
     }
     if (trace && k < 63) trace[k * 8 + 1] = cg1_timer();
+    // per-CTA arrival times of iterations 8..15 (NNMG_COARSE_TRACE)
+    if (a.trace && tid == 0 && k >= 8 && k < 16) a.trace[8 * 64 + (k - 8) * nrank + rank] = cg1_timer();
     grid.sync();
     if (trace && k < 63) trace[k * 8 + 2] = cg1_timer();
+    // every CTA reduces the per-CTA partials in the same fixed order
     __shared__ double tot[3];
     if (tid < 32) {
       const double* part = a.part + (k & 1) * 3 * nrank;
@@ -278,6 +306,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     beta = bk;
     alpha_old = ak;
     gamma_old = gamma;
+    if (trace && k < 63) trace[k * 8 + 4] = cg1_timer();
   }
   if (rank == 0 && tid == 0) {
     a.status[0] = status_it;
