@@ -505,6 +505,34 @@ struct CgLaunch {
     return true;
   }
 
+  // a few more cell blocks than SMs: one CTA per SM, each owning an equal
+  // cell range (NNMG_COARSE_BALANCE=0 disables)
+  template <int D, int P, int NC, int PH>
+  bool try_balanced(const Level& L, int nsm) {
+    using CKB = Cg1Kernel<D, P, NC, PH, 0>;
+    const char* eb = getenv("NNMG_COARSE_BALANCE");
+    if ((eb && atoi(eb) == 0) || L.nblk <= nsm || L.nblk * CKB::CB > int64_t(nsm) * CKB::SCB ||
+        CKB::NTHREADS > 512)  // larger CTAs spill (register budget 64K / NTHREADS)
+      return false;
+    constexpr size_t bsm = cg1_resident_smem<D, P, NC, PH, 0>();
+    if (bsm > 200 * 1024) return false;
+    auto kb = k_coarse_cg1<D, P, NC, PH, true, 0>;
+    NNMG_CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+    NNMG_CUDA_TRY(cudaFuncSetAttribute(kb, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+    int ps = 0;
+    NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kb, CKB::NTHREADS, bsm));
+    if (ps <= 0) return false;
+    C.split = 0;
+    C.mode = 1;
+    C.resident = true;
+    C.nsub = 1;
+    C.block = CKB::NTHREADS;
+    C.smem = bsm;
+    C.nrank = nsm;
+    return true;
+  }
+
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
@@ -592,7 +620,7 @@ struct CgLaunch {
         const int max_split = es ? atoi(es) : 8;
         if (C.single_barrier) {
           try_split<D, P, NC, PH, 8>(L, nsm, max_split) || try_split<D, P, NC, PH, 4>(L, nsm, max_split) ||
-              try_split<D, P, NC, PH, 2>(L, nsm, max_split);
+              try_split<D, P, NC, PH, 2>(L, nsm, max_split) || try_balanced<D, P, NC, PH>(L, nsm);
         }
       }
       if (C.single_barrier && C.mode != 2) {
@@ -647,7 +675,8 @@ struct CgLaunch {
       g.max_iter = C.max_iter;
       g.status = C.status.ptr;
       g.trace = C.trace.n ? C.trace.ptr : nullptr;
-      auto k1 = C.split == 8   ? k_coarse_cg1<D, P, NC, PH, true, 8>
+      auto k1 = C.split == 0   ? k_coarse_cg1<D, P, NC, PH, true, 0>
+                : C.split == 8 ? k_coarse_cg1<D, P, NC, PH, true, 8>
                 : C.split == 4 ? k_coarse_cg1<D, P, NC, PH, true, 4>
                 : C.split == 2 ? k_coarse_cg1<D, P, NC, PH, true, 2>
                 : C.mode == 1  ? k_coarse_cg1<D, P, NC, PH, true, 1>

@@ -16,7 +16,7 @@ struct Coarse {
   DevBuf<unsigned long long> epoch;  // last barrier epoch used (persists across solves)
   DevBuf<int> status;  // iterations, converged, error
   int nrank = 1, nsub = 1, block = 0;
-  int split = 1;  // CTAs per cell block (single-barrier kernel, small levels)
+  int split = 1;  // CTAs per cell block (single-barrier kernel); 0: balanced cell ranges
   bool resident = false;  // cell-block tables kept in shared memory
   int mode = 0;           // 0 pencil, 1 pencil resident, 2 register kernel
   int barrier = 0;        // 0 grid.sync, 1 all-to-all slots, 2 root broadcast (NNMG_COARSE_BARRIER)

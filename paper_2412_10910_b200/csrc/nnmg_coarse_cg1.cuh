@@ -74,8 +74,13 @@ __device__ __forceinline__ unsigned long long cg1_timer() {
 // SPLIT CTAs share one cell block (SCB = CB / SPLIT cells each): on small
 // coarse levels (fewer blocks than SMs) this spreads the cell work over more
 // SMs at the price of more barrier participants.
+// SPLIT == 0 ("balanced"): CTA r owns the cell range [r nc/R, (r+1) nc/R) of
+// all nc = nblk CB block cells, up to 5/4 CB of them (a level with a few more
+// cell blocks than SMs would otherwise give some CTAs two whole blocks).
 template <int D, int P, int NC, int PH, int SPLIT>
-using Cg1Kernel = CellKernel<D, P, NC, PH, CellKernel<D, P, NC, PH>::CB / SPLIT>;
+using Cg1Kernel = CellKernel<D, P, NC, PH,
+                             (SPLIT > 0 ? CellKernel<D, P, NC, PH>::CB / (SPLIT > 0 ? SPLIT : 1)
+                                        : CellKernel<D, P, NC, PH>::CB + CellKernel<D, P, NC, PH>::CB / 4)>;
 
 template <int D, int P, int NC, int PH, int SPLIT>
 constexpr size_t cg1_resident_smem() {
@@ -115,7 +120,19 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
   constexpr int64_t kIdxChunk = int64_t(CK::NLOC) * CK::SCB;
   double* geo_s = sm + CK::SMEM / sizeof(double);
   int* idx_s = reinterpret_cast<int*>(geo_s + kGeoChunk);
-  if constexpr (RES) {
+  if constexpr (RES && SPLIT == 0) {
+    // this CTA's cell range, padded to SCB with empty cells
+    const int64_t ncell = a.nblk * CK::CB;
+    const int64_t c0 = ncell * rank / nrank, nmine = ncell * (rank + 1) / nrank - c0;
+    for (int64_t k = tid; k < kGeoChunk; k += nth) {
+      const int64_t pos = k / CK::SCB, l = k % CK::SCB, c = c0 + l;
+      geo_s[k] = l < nmine ? a.geo[((c / CK::CB) * CK::NLOC * CK::NG + pos) * CK::CB + c % CK::CB] : 0.0;
+    }
+    for (int64_t k = tid; k < kIdxChunk; k += nth) {
+      const int64_t pos = k / CK::SCB, l = k % CK::SCB, c = c0 + l;
+      idx_s[k] = l < nmine ? a.idx[((c / CK::CB) * CK::NLOC + pos) * CK::CB + c % CK::CB] : -1;
+    }
+  } else if constexpr (RES) {
     // this CTA's sub-block (lanes sub*SCB ..) of cell block rank / SPLIT
     const int64_t blk = rank / SPLIT;
     const int off = (rank % SPLIT) * CK::SCB;
