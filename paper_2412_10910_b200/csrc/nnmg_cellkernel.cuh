@@ -5,6 +5,41 @@
 
 namespace nnmg {
 
+// NNMG_CELL_TRACE builds (diagnostic only): thread 0 of CTA 0 accumulates the
+// SM cycles spent between the cell kernel's barriers, per phase
+#ifdef NNMG_CELL_TRACE
+__device__ unsigned long long nnmg_cell_trace[16];
+#define NNMG_CT(i)                                          \
+  do {                                                      \
+    if (_ct_on) {                                           \
+      const unsigned long long _now = clock64();            \
+      _ct[(i)] = _now - _ct_last;                           \
+      _ct_last = _now;                                      \
+    }                                                       \
+  } while (0)
+#define NNMG_CT_BEGIN                                                    \
+  const bool _ct_on = threadIdx.x == 0 && blockIdx.x == 0;               \
+  unsigned long long _ct[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};      \
+  unsigned long long _ct_last = clock64()
+#define NNMG_CT_END                                                           \
+  do {                                                                        \
+    if (_ct_on) {                                                             \
+      for (int _i = 1; _i < 12; ++_i) nnmg_cell_trace[_i] += _ct[_i];         \
+      nnmg_cell_trace[14] += 1;                                               \
+    }                                                                         \
+  } while (0)
+#else
+#define NNMG_CT(i) \
+  do {             \
+  } while (0)
+#define NNMG_CT_BEGIN \
+  do {                \
+  } while (0)
+#define NNMG_CT_END \
+  do {              \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // K1/K2: the sum-factorised cell kernel.  One thread block per block of CB
 // cells; gather -> interpolate to quadrature points (S sweeps) -> collocation
@@ -72,46 +107,70 @@ struct CellKernel {
   // that p.Ap can be formed without waiting for the scatter to complete.
   // kRes: idx/geo point at a shared-memory copy of this block's tables
   // kNeg: scatter -A_K u (dst -= A u, used to update residuals in place)
+  // global DoF indices of this thread's x-pencil nodes (-1: constrained / padding)
+  template <bool kRes = false>
+  __device__ __forceinline__ static void pencil_dofs(const int* __restrict__ idx, int64_t blk, int tid, int lane_off,
+                                                     int (&gi)[N1]) {
+    constexpr int GS = kRes ? SCB : CB;
+    const int glane = kRes ? tid % SCB : lane_off + tid % SCB;
+    const int base = PL::base(0, tid / SCB);
+#pragma unroll
+    for (int i = 0; i < N1; ++i) gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * GS + glane);
+  }
+
   template <bool kRes = false, bool kNeg = false, class Src, class Sync>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
                                                Sync&& sync, int lane_off = 0) {
+    // the block's geometry chunk (85% of the bytes) is consumed only in phase
+    // 5: start streaming it into L2 now so it overlaps gathers and sweeps
+    constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
+    if (!kRes && SCB == CB && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+    int gi[N1];
+    pencil_dofs<kRes>(idx, blk, tid, lane_off, gi);
+    double v[NCOMP][N1];
+#pragma unroll
+    for (int i = 0; i < N1; ++i)
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
+    return run_values<kRes, kNeg>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off);
+  }
+
+  // the cell kernel from gathered pencil values v (zero on gi < 0) onwards;
+  // callers that can issue the gather early (the coarse CG) enter here
+  template <bool kRes = false, bool kNeg = false, class Sync>
+  __device__ __forceinline__ static double run_values(const Tables& tab, const int (&gi)[N1],
+                                                      double (&v)[NCOMP][N1], double* __restrict__ dst,
+                                                      const double* __restrict__ geo, int64_t blk, double lam,
+                                                      double mu, double* sm, int tid, Sync&& sync, int lane_off = 0) {
     // lsub indexes shared memory (stride SCB); glane indexes the tables:
     // HBM layout (stride CB) or a resident shared copy of the sub-block (SCB)
+    NNMG_CT_BEGIN;
     const int lsub = tid % SCB;
     const int pen = tid / SCB;
     constexpr int GS = kRes ? SCB : CB;
     const int glane = kRes ? lsub : lane_off + lsub;
     constexpr int A = 0, GX = 1, GY = 2;
-    // the block's geometry chunk (85% of the bytes) is consumed only in phase
-    // 5: start streaming it into L2 now so it overlaps gathers and sweeps
-    constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
-    if (!kRes && SCB == CB && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
-    double v[NCOMP][N1], u0[NCOMP][N1];
-    int gi[N1];
-    // P1: gather the x-pencil and interpolate along x
+    double u0[NCOMP][N1];
+    // P1: interpolate the x-pencil along x
     {
-      const int base = PL::base(0, pen);
 #pragma unroll
-      for (int i = 0; i < N1; ++i) {
-        gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * GS + glane);
+      for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
-        for (int c = 0; c < NCOMP; ++c) {
-          v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
-          u0[c][i] = v[c][i];
-        }
-      }
+        for (int i = 0; i < N1; ++i) u0[c][i] = v[c][i];
       op(tab.S, v, false);
       store<0>(sm, A, pen, lsub, v);
     }
     sync();
+    NNMG_CT(1);
     if constexpr (DIM == 3) {
       // P2: interpolate along y
       load<1>(sm, A, pen, lsub, v);
       op(tab.S, v, false);
       store<1>(sm, A, pen, lsub, v);
       sync();
+      NNMG_CT(2);
     }
     // P3: interpolate along the last axis -> values at quadrature points
     constexpr int KL = DIM - 1;
@@ -122,6 +181,7 @@ struct CellKernel {
     for (int c = 0; c < NCOMP; ++c) sweep<N1>(tab.Dc, v[c], gl[c]);
     store<KL>(sm, A, pen, lsub, v);
     sync();
+    NNMG_CT(3);
     // P4: collocation derivatives along x (and y in 3D)
     {
       double w[NCOMP][N1];
@@ -135,6 +195,7 @@ struct CellKernel {
       }
     }
     sync();
+    NNMG_CT(4);
     // P5: quadrature-point physics on the last-axis pencil
     {
       const int base = PL::base(KL, pen);
@@ -179,6 +240,7 @@ struct CellKernel {
       }
     }
     sync();
+    NNMG_CT(5);
     if constexpr (DIM == 3) {
       // P6: A += Dc^T fx along x
       {
@@ -193,6 +255,7 @@ struct CellKernel {
         store<0>(sm, A, pen, lsub, a);
       }
       sync();
+      NNMG_CT(6);
       // P7: w = A + Dc^T fy along y, then S^T along y
       {
         double w[NCOMP][N1], a[NCOMP][N1];
@@ -207,11 +270,13 @@ struct CellKernel {
         store<1>(sm, A, pen, lsub, a);
       }
       sync();
+      NNMG_CT(7);
       // P8: S^T along z
       load<2>(sm, A, pen, lsub, v);
       op(tab.S, v, true);
       store<2>(sm, A, pen, lsub, v);
       sync();
+      NNMG_CT(8);
     } else {
       // 2D P6: A = Dc^T fx along x
       {
@@ -221,6 +286,7 @@ struct CellKernel {
         store<0>(sm, A, pen, lsub, w);
       }
       sync();
+      NNMG_CT(9);
       // 2D P7: w = A + (y part in registers), S^T along y
       {
         double a[NCOMP][N1];
@@ -233,6 +299,7 @@ struct CellKernel {
         store<1>(sm, A, pen, lsub, a);
       }
       sync();
+      NNMG_CT(10);
     }
     // final: S^T along x and scatter-add the x-pencil
     load<0>(sm, A, pen, lsub, v);
@@ -248,6 +315,8 @@ struct CellKernel {
         }
       }
     }
+    NNMG_CT(11);
+    NNMG_CT_END;
     return energy;
   }
 };

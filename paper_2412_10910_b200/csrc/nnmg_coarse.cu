@@ -779,6 +779,15 @@ void coarse_solve(Coarse& C, const double* b, double* x, cudaStream_t s) {
 }
 
 void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
+#ifdef NNMG_CELL_TRACE
+  {
+    unsigned long long ct[16];
+    NNMG_CUDA_TRY(cudaMemcpyFromSymbol(ct, nnmg_cell_trace, sizeof(ct)));
+    fprintf(stderr, "[nnmg cell trace] calls %llu, cycles per call by phase:", ct[14]);
+    for (int i = 1; i <= 11; ++i) fprintf(stderr, " P%d %.0f", i, ct[14] ? double(ct[i]) / double(ct[14]) : 0.0);
+    fprintf(stderr, "\n");
+  }
+#endif
   int st[3];
   NNMG_CUDA_TRY(cudaMemcpy(st, C.status.ptr, sizeof(st), cudaMemcpyDeviceToHost));
   *iterations = st[0];
@@ -821,7 +830,27 @@ void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
       for (double v : late) mean += v / C.nrank;
       fprintf(stderr, " | mean %.0f, CTA0 %.0f\n", mean, late[0]);
     }
-    if (cnt)
+    if (cnt && C.single_barrier && C.mode != 2) {
+      double q[6] = {0, 0, 0, 0, 0, 0};
+      for (int it = 2; it < n; ++it) {
+        const unsigned long long* r = &t[it * 8];
+        q[0] += double(r[5] - r[0]);
+        q[1] += double(r[7] - r[5]);
+        q[2] += double(r[1] - r[7]);
+        q[3] += double(r[2] - r[1]);
+        q[4] += double(r[3] - r[2]);
+        q[5] += double(r[4] - r[3]);
+      }
+      int dev = 0, khz = 0;
+      NNMG_CUDA_TRY(cudaGetDevice(&dev));
+      NNMG_CUDA_TRY(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev));
+      const double f = 1e6 / double(khz) / cnt;
+      fprintf(stderr,
+              "[nnmg coarse trace] cg1 ctas=%d threads=%d split=%d per-iteration ns (CTA 0): cells %.0f owners %.0f "
+              "local-reduce %.0f barrier %.0f global-reduce %.0f scalars %.0f total %.0f\n",
+              C.nrank, C.block, C.split, q[0] * f, q[1] * f, q[2] * f, q[3] * f, q[4] * f, q[5] * f,
+              tot * 1e6 / double(khz) / cnt);
+    } else if (cnt)
       fprintf(stderr,
               "[nnmg coarse trace] barrier=%d ctas=%d resident=%d per-iteration ns: applyA %.0f barrierA %.0f "
               "phaseB %.0f barrierB %.0f total %.0f | applyA = cells %.0f + owners %.0f + constrained %.0f + "

@@ -65,7 +65,10 @@ struct Cg1Src {
   __device__ __forceinline__ double operator()(int64_t i) const { return __ldg(inv_diag + i) * rk(i); }
 };
 
-__device__ __forceinline__ unsigned long long cg1_timer() {
+// phase stamps of CTA 0: SM cycles (the host converts at the SM clock);
+// cross-CTA arrival stamps: %globaltimer (ns, common to all SMs)
+__device__ __forceinline__ unsigned long long cg1_timer() { return (unsigned long long)clock64(); }
+__device__ __forceinline__ unsigned long long cg1_gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
@@ -155,6 +158,59 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     a.x[i] = 0.0;
   }
   grid.sync();
+  // owners' operands (final since the last barrier) are loaded right after
+  // each barrier, ahead of the global reduction and the cell phase, when the
+  // owned range fits KO registers per thread (always on the small levels).
+  // Laplace only: measured, the live registers slow elasticity's cell phase.
+  constexpr int KO = 4;
+  constexpr bool kPrefetch = NC == 1;
+  constexpr bool kFold = NC == 1;
+  const bool fits = kPrefetch && a.prefetch_owned && (i1 - i0) <= KO * (int64_t)nth;
+  double rp[KO], wp[KO], so[KO], di[KO], pp[KO], xx[KO];
+  bool cf[KO];
+  auto load_owned = [&](int k, int64_t i) {
+    const double* r = a.r[(k + 1) & 1];
+    const double* w = a.w[(k + 2) % 3];
+    const double* s = a.s[k & 1];
+#pragma unroll
+    for (int j = 0; j < KO; ++j) {
+      const int64_t ii = i + j * (int64_t)nth;
+      if (ii < i1) {
+        rp[j] = __ldcg(r + ii);
+        wp[j] = __ldcg(w + ii);
+        so[j] = __ldcg(s + ii);
+        di[j] = a.inv_diag[ii];
+        pp[j] = a.p[ii];
+        xx[j] = a.x[ii];
+        if constexpr (kFold) cf[j] = a.con[ii] != 0;
+      }
+    }
+  };
+  // RES: the pencil's DoFs never change, and the raw operands of the next
+  // phase's gather (r_{k-1}, w_{k-1}, s_{k-2}, D^-1) are issued right after
+  // the barrier too; u_k is formed from them once alpha, beta are known
+  constexpr int N1 = CK::N1;
+  int gi[N1];
+  double gr[NC][N1], gw[NC][N1], gs[NC][N1], gd[NC][N1];
+  if constexpr (RES) CK::template pencil_dofs<true>(idx_s, 0, tid, 0, gi);
+  auto gather = [&](int k) {
+    const double* r = a.r[(k + 1) & 1];
+    const double* w = a.w[(k + 2) % 3];
+    const double* s = a.s[k & 1];
+#pragma unroll
+    for (int i = 0; i < N1; ++i)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (gi[i] >= 0) {
+          const int64_t j = (int64_t)gi[i] * NC + c;
+          gr[c][i] = __ldcg(r + j);
+          gw[c][i] = __ldcg(w + j);
+          gs[c][i] = __ldcg(s + j);
+          gd[c][i] = __ldg(a.inv_diag + j);
+        }
+  };
+  if constexpr (RES) gather(0);
+  if (fits) load_owned(0, i0 + tid);
   double alpha = 0.0, beta = 0.0, gamma_old = 1.0, alpha_old = 1.0, target = 0.0;
   int status_it = a.max_iter, status_conv = 0, status_err = 0;
   for (int k = 0; k <= a.max_iter; ++k) {
@@ -163,37 +219,17 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     const int wb_prev = (k + 2) % 3, wb = k % 3, wb_next = (k + 1) % 3;
     const Cg1Src src{a.r[rb_prev], a.w[wb_prev], a.s[sb_old], a.inv_diag, alpha, beta};
     if (trace && k < 63) trace[k * 8 + 0] = cg1_timer();
-    // owners' operands (final since the last barrier) are loaded before the
-    // cell phase so that their L2 latency overlaps it, when the owned range
-    // fits KO registers per thread (always on the split/small levels)
-    constexpr int KO = 4;
-    // (Laplace only: measured, the live registers slow elasticity's cell phase)
-    constexpr bool kPrefetch = NC == 1;
-    constexpr bool kFold = NC == 1;
-    const bool fits = kPrefetch && a.prefetch_owned && (i1 - i0) <= KO * (int64_t)nth;
-    double rp[KO], wp[KO], so[KO], di[KO], pp[KO], xx[KO];
-    bool cf[KO];
-    auto load_owned = [&](int64_t i) {
-#pragma unroll
-      for (int j = 0; j < KO; ++j) {
-        const int64_t ii = i + j * (int64_t)nth;
-        if (ii < i1) {
-          rp[j] = __ldcg(a.r[rb_prev] + ii);
-          wp[j] = __ldcg(a.w[wb_prev] + ii);
-          so[j] = __ldcg(a.s[sb_old] + ii);
-          di[j] = a.inv_diag[ii];
-          pp[j] = a.p[ii];
-          xx[j] = a.x[ii];
-          if constexpr (kFold) cf[j] = a.con[ii] != 0;
-        }
-      }
-    };
-    if (fits) load_owned(i0 + tid);
     // cells: w_k = A u_k and energies
     double e = 0.0;
     if constexpr (RES) {
-      e = CK::template run<true>(a.tab, src, a.w[wb], idx_s, geo_s, 0, a.lam, a.mu, sm, tid,
-                                 [] __device__() { __syncthreads(); });
+      double v[NC][N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)  // = src(gi * NC + c), bit for bit
+          v[c][i] = gi[i] >= 0 ? gd[c][i] * fma(-alpha, fma(beta, gs[c][i], gw[c][i]), gr[c][i]) : 0.0;
+      e = CK::template run_values<true>(a.tab, gi, v, a.w[wb], geo_s, 0, a.lam, a.mu, sm, tid,
+                                        [] __device__() { __syncthreads(); });
     } else {
       for (int64_t u = rank; u < a.nblk * SPLIT; u += nrank)
         e += CK::run(a.tab, src, a.w[wb], a.idx, a.geo, u / SPLIT, a.lam, a.mu, sm, tid,
@@ -214,7 +250,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     // owners: s_{k-1}, r_k, p_{k-1}, x_k; gamma_k, ||r_k||^2; zero w_{k+1}
     double g = 0.0, rr = 0.0;
     for (int64_t i = i0 + tid; i < i1; i += KO * (int64_t)nth) {
-      if (!fits) load_owned(i);
+      if (!fits) load_owned(k, i);
 #pragma unroll
       for (int j = 0; j < KO; ++j) {
         const int64_t ii = i + j * (int64_t)nth;
@@ -262,9 +298,11 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     }
     if (trace && k < 63) trace[k * 8 + 1] = cg1_timer();
     // per-CTA arrival times of iterations 8..15 (NNMG_COARSE_TRACE)
-    if (a.trace && tid == 0 && k >= 8 && k < 16) a.trace[8 * 64 + (k - 8) * nrank + rank] = cg1_timer();
+    if (a.trace && tid == 0 && k >= 8 && k < 16) a.trace[8 * 64 + (k - 8) * nrank + rank] = cg1_gtimer();
     grid.sync();
     if (trace && k < 63) trace[k * 8 + 2] = cg1_timer();
+    if constexpr (RES) gather(k + 1);
+    if (fits) load_owned(k + 1, i0 + tid);
     // every CTA reduces the per-CTA partials in the same fixed order
     __shared__ double tot[3];
     if (tid < 32) {
