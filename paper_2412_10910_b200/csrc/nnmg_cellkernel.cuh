@@ -126,7 +126,7 @@ struct CellKernel {
     // the block's geometry chunk (85% of the bytes) is consumed only in phase
     // 5: start streaming it into L2 now so it overlaps gathers and sweeps
     constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
-    if (!kRes && SCB == CB && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+    if (!kRes && lane_off == 0 && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
     int gi[N1];
     pencil_dofs<kRes>(idx, blk, tid, lane_off, gi);
     double v[NCOMP][N1];

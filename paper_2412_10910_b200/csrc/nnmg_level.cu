@@ -89,14 +89,24 @@ template <int DIM>
 __global__ void k_edges(const double* __restrict__ verts, const int* __restrict__ cells, int64_t n_cells, int cb,
                         double* __restrict__ edges);
 
-template <int DIM, int P, int NCOMP, int PHYS, bool NEG>
-__global__ void __launch_bounds__(CellKernel<DIM, P, NCOMP, PHYS>::NTHREADS)
+// SPLIT CTAs per cell block (SCB = CB / SPLIT cells each): smaller CTAs get
+// a larger register budget per thread (the Q4 kernel spills at CB = 32)
+template <int DIM, int P, int NCOMP, int PHYS, int SPLIT>
+using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PHYS>::CB / SPLIT>;
+
+// min resident CTAs per SM for the split variants (measured on B200: 5 gives
+// C5 0.310 -> 0.279 ms, C4 0.643 -> 0.639 ms)
+#ifndef NNMG_APPLY_MINB
+#define NNMG_APPLY_MINB 5
+#endif
+template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT>
+__global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHREADS, SPLIT == 1 ? 1 : NNMG_APPLY_MINB)
     k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
             const double* __restrict__ geo, int64_t b0, double lam, double mu) {
   extern __shared__ double sm[];
-  CellKernel<DIM, P, NCOMP, PHYS>::template run<false, NEG>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x, lam,
-                                                            mu, sm, threadIdx.x,
-                                                            [] __device__() { __syncthreads(); });
+  using CK = ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>;
+  CK::template run<false, NEG>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm, threadIdx.x,
+                               [] __device__() { __syncthreads(); }, int(blockIdx.x % SPLIT) * CK::SCB);
 }
 
 // ---------------------------------------------------------------------------
@@ -270,6 +280,13 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       const char* e = getenv("NNMG_APPLY_KERNEL");
       L->reg_kernel = !(e && std::string(e) == "pencil");
       const char* m = getenv("NNMG_REG_MINB");
+      {
+        const char* sp = getenv("NNMG_APPLY_SPLIT");
+        // measured on B200: Q4 Laplace (C4) 0.684 -> 0.613 ms with 4, Q2
+        // elasticity (C5) 0.288 -> 0.279 ms with 2
+        L->apply_split = sp ? atoi(sp) : (dim == 3 && degree >= 4 ? 4 : (ncomp > 1 ? 2 : 1));
+        if (L->apply_split != 2 && L->apply_split != 4) L->apply_split = 1;
+      }
       L->reg_minb = m ? atoi(m) : 1;
       const char* rm = getenv("NNMG_RECOMPUTE_MOD");
       L->recompute_mod = rm ? atoi(rm) : 0;
@@ -429,19 +446,27 @@ struct ApplyLaunch {
         return;
       }
     }
-    auto kern = neg ? k_apply<D, P, NC, PH, true> : k_apply<D, P, NC, PH, false>;
+    if (L.apply_split == 4) return launch<D, P, NC, PH, 4>();
+    if (L.apply_split == 2) return launch<D, P, NC, PH, 2>();
+    launch<D, P, NC, PH, 1>();
+  }
+  template <int D, int P, int NC, int PH, int SPLIT>
+  void launch() {
+    using CK = ApplyKernel<D, P, NC, PH, SPLIT>;
+    auto kern = neg ? k_apply<D, P, NC, PH, true, SPLIT> : k_apply<D, P, NC, PH, false, SPLIT>;
     static bool attr = false;
     if (!attr) {
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)CK::SMEM));
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)CK::SMEM));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true, SPLIT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK::SMEM));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false, SPLIT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK::SMEM));
       attr = true;
     }
-    const int64_t nb = b1 - b0;
-    for (int64_t off = 0; off < nb; off += 0x7fffffff) {
-      const unsigned g = static_cast<unsigned>(std::min<int64_t>(nb - off, 0x7fffffff));
-      kern<<<g, CK::NTHREADS, CK::SMEM, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0 + off, L.lam, L.mu);
+    const int64_t nb = (b1 - b0) * SPLIT;
+    constexpr int64_t kMaxGrid = (0x7fffffff / SPLIT) * SPLIT;
+    for (int64_t off = 0; off < nb; off += kMaxGrid) {
+      const unsigned g = static_cast<unsigned>(std::min<int64_t>(nb - off, kMaxGrid));
+      kern<<<g, CK::NTHREADS, CK::SMEM, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0 + off / SPLIT, L.lam, L.mu);
       NNMG_CHECK_LAUNCH();
       count_launch();
     }
