@@ -146,15 +146,22 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle (NumPy port of the reference path) on a sample
 # ---------------------------------------------------------------------------
-def cpu_vcycle_rate(cfg, scale, seconds, steps=None):
+def cpu_vcycle_rate(cfg, scale, seconds, steps=None, warmup=1):
     from oracle import nnmg_oracle as O
 
     meshes = [O.jittered_mesh(cfg.level_grid(l, scale), cfg.extent, cfg.amplitude, 1000 * cfg.index + l + 1,
                               cfg.warp) for l in range(len(cfg.levels))]
-    H, spaces = O.build_hierarchy(meshes, cfg.degree, cfg.problem, cfg.dirichlet_ids, cfg.lame or (1.0, 1.0),
-                                  cfg.chebyshev_degree)
+    args = (meshes, cfg.degree, cfg.problem, cfg.dirichlet_ids, cfg.lame or (1.0, 1.0), cfg.chebyshev_degree)
+    try:
+        H, spaces = O.build_hierarchy(*args)
+    except O.LocateError:
+        # coarse sample meshes of the curved config miss boundary points: widen
+        # the box padding to 0.1 h_coarse as SURVEY.md §8(c) prescribes
+        h = min((hi - lo) / n for (lo, hi), n in zip(cfg.extent, cfg.level_grid(0, scale)))
+        H, spaces = O.build_hierarchy(*args, search={"eps_box": 0.1 * h})
     b = O.assemble_rhs_const(spaces[-1], cfg.body_force if cfg.body_force else 1.0)
-    H.precondition(b)  # warm-up
+    for _ in range(max(1, warmup)):
+        H.precondition(b)  # warm-up
     n = spaces[-1].n_dofs
     t0 = time.perf_counter()
     k = 0
@@ -171,12 +178,13 @@ def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    rate, n, k, el = cpu_vcycle_rate(cfg, args.cpu_scale, args.cpu_seconds, steps=max(1, args.steps))
+    rate, n, k, el = cpu_vcycle_rate(cfg, args.cpu_scale, args.cpu_seconds, steps=max(1, args.steps),
+                                     warmup=args.warmup)
     sample = (f"{cfg.name} at 1/{args.cpu_scale} cells per axis ({n} fine DoFs), {k} V-cycles, "
               f"NumPy oracle port of nnmg")
     line = {
         "impl": "reference", "metric": "fp64 V-cycle GDoF/s", "value": rate, "unit": "GDoF/s", "n_gpus": 0,
-        "steps": k, "warmup": 1, "ms_per_step": el / k * 1e3, "higher_is_better": True, "scaling": "weak",
+        "steps": k, "warmup": max(1, args.warmup), "ms_per_step": el / k * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8(d) meshes)",
         "config": {"workload": CONFIG_TEXT[cfg.name] + f" (CPU sample 1/{args.cpu_scale})", "config": cfg.name},
         "cpu_baseline": {"value": rate, "unit": "GDoF/s", "cores": 1, "kind": "port", "sample": sample},
