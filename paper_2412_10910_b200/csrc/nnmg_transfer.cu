@@ -5,6 +5,7 @@
 #include "nnmg_transfer_kernels.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 namespace nnmg {
@@ -31,8 +32,23 @@ struct TransferDispatch {
       NNMG_CHECK_LAUNCH();
       count_launch();
     } else {
-      k_restrict_cells<D, P, NC><<<g, kWarps * 32, 0, s>>>(C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
-                                                           T.ncc, T.cellbuf.ptr);
+      const int ch = T.chunk;
+      const int64_t nwarps = (T.ncc + ch - 1) / ch;
+      if constexpr (ipow(P + 1, D) * NC <= 32) {
+        if (T.restrict_kernel == 0 || T.restrict_kernel == 1) {
+          auto k = T.restrict_kernel == 0 ? k_restrict_lane<D, P, NC, 1> : k_restrict_lane<D, P, NC, 2>;
+          k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
+                                                            T.ncc, ch, T.cellbuf.ptr);
+        } else {
+          constexpr int W = StagedRestrict<D, P, NC>::WARPS;
+          k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
+              C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr, T.ncc, ch, T.cellbuf.ptr);
+        }
+      } else {
+        constexpr int W = StagedRestrict<D, P, NC>::WARPS;
+        k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
+            C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr, T.ncc, ch, T.cellbuf.ptr);
+      }
       NNMG_CHECK_LAUNCH();
       k_restrict_gather<<<grid_for(C.n_scalar, 256), 256, 0, s>>>(T.t_off.ptr, T.t_ent.ptr, T.cellbuf.ptr,
                                                                    C.n_scalar, NC, out);
@@ -95,6 +111,25 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
     T->t_off.upload(off);
     T->t_ent.upload(ent);
     T->cellbuf.alloc(size_t(ncc) * nloc * T->ncomp);
+    // restriction: consecutive coarse cells per warp, so the point stream is
+    // pipelined across cell boundaries; aim for >= ~4 warps per SM slot
+    {
+      const char* e = getenv("NNMG_RESTRICT_CHUNK");
+      const int64_t target_warps = int64_t(148) * 16 * 4;
+      int ch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, ncc / target_warps)));
+      if (e) ch = std::max(1, std::min(31, atoi(e)));
+      T->chunk = ch;
+      // NLOC*NCOMP <= 32: 0 = lane-owned (1 point/round), 1 = lane-owned (2), 2 = staged groups
+      const char* k = getenv("NNMG_RESTRICT_KERNEL");
+      T->restrict_kernel = k ? atoi(k) : 1;
+    }
+    // fine scalar DoFs without a transfer point: zeroed by the plain prolongation
+    std::vector<uint8_t> has(fine->n_scalar, 0);
+    for (int64_t i = 0; i < npts; ++i) has[point_dofs[i]] = 1;
+    std::vector<int> nopt;
+    for (int64_t d = 0; d < fine->n_scalar; ++d)
+      if (!has[d]) nopt.push_back(static_cast<int>(d));
+    T->no_point.upload(nopt);
   } catch (...) {
     delete T;
     throw;
@@ -103,7 +138,15 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
 }
 
 void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s) {
-  if (!accumulate) NNMG_CUDA_TRY(cudaMemsetAsync(uf, 0, sizeof(double) * T.fine->n_dofs, s));
+  if (!accumulate) {
+    // every point DoF is written below; only the point-less ones need zeros
+    const int64_t n = int64_t(T.no_point.n) * T.ncomp;
+    if (n) {
+      k_zero_list<<<grid_for(n, 256), 256, 0, s>>>(T.no_point.ptr, int64_t(T.no_point.n), T.ncomp, uf);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+    }
+  }
   TransferDispatch f{T, uc, uf, accumulate ? 1 : 0, s};
   dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
 }

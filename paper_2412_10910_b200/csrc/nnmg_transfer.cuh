@@ -12,11 +12,14 @@ struct Transfer {
   Level* fine = nullptr;
   int dim = 0, pc = 0, ncomp = 1;
   int64_t npts = 0, ncc = 0;
+  int chunk = 1;            // coarse cells per warp in the restriction
+  int restrict_kernel = 1;  // variant for NLOC*NCOMP <= 32 (see transfer_create)
   DevBuf<int> cell_start;   // [ncc+1] CSR of points by owning coarse cell
   DevBuf<int> pt_dof;       // [npts] fine scalar DoF (sorted by cell, then point order)
   DevBuf<double> xhat;      // [npts][dim]
   DevBuf<double> cellbuf;   // [ncc][nloc][ncomp] restriction partial local vectors
   DevBuf<int> t_off, t_ent; // coarse DoF -> (cell*nloc + l) entries, fixed order
+  DevBuf<int> no_point;     // fine scalar DoFs without a point (zero in P u_c)
 };
 
 Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_t* point_dofs, const int64_t* cells,

@@ -2,6 +2,15 @@
 //
 // Records are grouped by owning coarse cell (CSR cell_start / pt_dof / xhat),
 // one warp per coarse cell.  See DESIGN.md "Transfers".
+//
+// FP64 instruction count decides these kernels on B200 (ncu: FP64 pipe 42-55%
+// busy while DRAM is far from peak), so the per-point arithmetic is kept at the
+// minimum of the tensor-product form:
+//   * 1D Lagrange values by prefix/suffix products (5 N1 - 6 ops per axis);
+//   * restriction weights factorised (v X2[i2]) X1[i1] X0[i0]: N1^d FMAs plus
+//     N1 + N1^2 products instead of 2 N1^d products;
+//   * cell-end reductions as a transposing shuffle reduction (31 shuffles for
+//     32 outputs) instead of a butterfly per output (5 per output).
 #pragma once
 
 #include "nnmg_kernels.cuh"
@@ -10,67 +19,69 @@ namespace nnmg {
 
 static constexpr int kTransferWarps = 4;  // coarse cells (one per warp) per thread block
 
-// Software-pipelined stream over a lane's points p = first, first+stride, ...
-// (< end): point indices and coordinates are loaded two points ahead and the
-// gathered fine value one point ahead, so the dependent pt_dof -> r_f[dof]
-// chain overlaps the arithmetic of the current point.
-template <int DIM, int NCOMP, int VSTRIDE = NCOMP>
-struct PointStream {
-  const int* __restrict__ pt_dof;
-  const double* __restrict__ xhat;
-  const double* __restrict__ rf;
-  int end, stride;
-  int p0, p1, p2;
-  int64_t d0, d1, d2;
-  double x0[DIM], x1[DIM], x2[DIM];
-  double v0[NCOMP], v1[NCOMP];
-
-  __device__ __forceinline__ void load_idx(int p, int64_t& d, double (&x)[DIM]) {
-    const bool ok = p < end;
-    d = ok ? __ldcs(pt_dof + p) : 0;
+// phi_i(t) for the N1 Lobatto-node Lagrange polynomials (fespace.py:42-51):
+// rdenom_i * prod_{j<i} d_j * prod_{j>i} d_j, d_j = t - node_j
+template <int N1>
+__device__ __forceinline__ void lagrange_pp(const Tables& tab, double t, double (&out)[N1]) {
+  if constexpr (N1 == 1) {
+    out[0] = 1.0;
+  } else {
+    double d[N1];
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) x[j] = ok ? __ldcs(xhat + (int64_t)p * DIM + j) : 0.5;
-  }
-  __device__ __forceinline__ void load_val(int p, int64_t d, double (&v)[NCOMP]) {
+    for (int j = 0; j < N1; ++j) d[j] = t - tab.nodes[j];
+    double suf[N1];
+    suf[N1 - 1] = d[N1 - 1];
 #pragma unroll
-    for (int c = 0; c < NCOMP; ++c) v[c] = p < end ? rf[d * VSTRIDE + c] : 0.0;
-  }
-  __device__ __forceinline__ void start(int first) {
-    p0 = first;
-    p1 = first + stride;
-    p2 = first + 2 * stride;
-    load_idx(p0, d0, x0);
-    load_idx(p1, d1, x1);
-    load_val(p0, d0, v0);
-  }
-  __device__ __forceinline__ bool valid() const { return p0 < end; }
-  // issue the next loads; call before computing on (x0, v0)
-  __device__ __forceinline__ void prefetch() {
-    load_val(p1, d1, v1);
-    load_idx(p2, d2, x2);
-  }
-  __device__ __forceinline__ void advance() {
-    p0 = p1;
-    p1 = p2;
-    p2 += stride;
-    d0 = d1;
-    d1 = d2;
+    for (int j = N1 - 2; j >= 1; --j) suf[j] = d[j] * suf[j + 1];
+    out[0] = tab.rdenom[0] * suf[1];
+    double pre = d[0];
 #pragma unroll
-    for (int j = 0; j < DIM; ++j) {
-      x0[j] = x1[j];
-      x1[j] = x2[j];
+    for (int i = 1; i < N1 - 1; ++i) {
+      out[i] = (tab.rdenom[i] * pre) * suf[i + 1];
+      pre *= d[i];
     }
-#pragma unroll
-    for (int c = 0; c < NCOMP; ++c) v0[c] = v1[c];
+    out[N1 - 1] = tab.rdenom[N1 - 1] * pre;
   }
-};
+}
+
+// phi_g(t) for one runtime node index g (the cooperative evaluation below)
+template <int N1>
+__device__ __forceinline__ double lagrange_one(const Tables& tab, double t, int g) {
+  double v = tab.rdenom[g];
+#pragma unroll
+  for (int j = 0; j < N1; ++j) v *= (j == g) ? 1.0 : (t - tab.nodes[j]);
+  return v;
+}
+
+// Transposing warp reduction of 32 per-lane values (entries >= N are zero):
+// afterwards lane l holds sum over lanes of a[l].  Recursive halving, each step
+// keeps the half selected by the lane bit and adds the partner's copy of it:
+// 31 shuffles + 31 adds per lane, fixed order (deterministic).
+template <int N>
+__device__ __forceinline__ double transpose_reduce(double (&a)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      if (i >= N && i + o >= N && o == 16) {
+        a[i] = 0.0;  // both halves are padding
+        continue;
+      }
+      const double keep = hi ? a[i + o] : a[i];
+      const double send = hi ? a[i] : a[i + o];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return a[0];
+}
 
 // ---------------------------------------------------------------------------
 // K6: u_f[pt] (+)= sum_l u_c[gather[pt,l]] prod_j phi_{l_j}(xhat_j)
 // (transfer.py:31-44, 87-102).  The cell's coarse values are staged once in
-// shared memory and broadcast; each lane evaluates two points per round so two
-// independent load/store chains are in flight.  Contraction order x, y, z as
-// transfer.py:93-95.
+// shared memory and broadcast; each lane evaluates PPL points per round.  The
+// records of the next round are loaded before the current round's arithmetic.
+// Contraction order x, y, z as transfer.py:93-95.
 // ---------------------------------------------------------------------------
 template <int DIM, int N1>
 __device__ __forceinline__ double contract(const double* __restrict__ U, const double (&X)[DIM][N1]) {
@@ -114,37 +125,48 @@ __global__ void __launch_bounds__(kTransferWarps * 32, 6)
   const int64_t cell = blockIdx.x * (int64_t)kTransferWarps + warp;
   if (cell >= ncc) return;
   const int64_t blk = cell / CBC, cl = cell % CBC;
+  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
+  // measured: two independent points per lane per round beat one (C3)
+  constexpr int PPL = ((DIM == 2 || N1 <= 3) && NCOMP == 1) ? 2 : 1;
+  constexpr int STEP = 32 * PPL;
+  // first round's records are in flight while the coarse values are staged
+  int dd[PPL];
+  double xt[PPL][DIM];
+  auto load = [&](int base) {
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+      const int p = base + 32 * k + lane;
+      const bool ok = p < p1;
+      dd[k] = ok ? __ldcs(pt_dof + p) : -1;
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) xt[k][j] = ok ? __ldcs(xhat + (int64_t)p * DIM + j) : 0.5;
+    }
+  };
+  load(p0);
   for (int l = lane; l < NLOC; l += 32) {
     const int g = cidx[(blk * NLOC + l) * CBC + cl];
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c) su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] : 0.0;
   }
   __syncwarp();
-  // measured: two independent points per lane per round beat a pipelined
-  // single-point stream here (C3: 0.195 vs 0.251 ms)
-  constexpr int PPL = ((DIM == 2 || N1 <= 2) && NCOMP == 1) ? 2 : 1;
-  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
-  for (int base = p0; base < p1; base += 32 * PPL) {
-    int pp[PPL], dd[PPL];
-    bool vv[PPL];
+  for (int base = p0; base < p1; base += STEP) {
+    int cd[PPL];
     double X[PPL][DIM][N1];
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
-      pp[k] = base + 32 * k + lane;
-      vv[k] = pp[k] < p1;
-      dd[k] = vv[k] ? __ldcs(pt_dof + pp[k]) : 0;
+      cd[k] = dd[k];
 #pragma unroll
-      for (int j = 0; j < DIM; ++j)
-        lagrange_values<N1>(tab, vv[k] ? __ldcs(xhat + (int64_t)pp[k] * DIM + j) : 0.5, X[k][j]);
+      for (int j = 0; j < DIM; ++j) lagrange_pp<N1>(tab, xt[k][j], X[k][j]);
     }
+    if (base + STEP < p1) load(base + STEP);
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c) {
       const double* U = su[warp] + c * NLOC;
 #pragma unroll
       for (int k = 0; k < PPL; ++k) {
         const double a = contract<DIM, N1>(U, X[k]);
-        if (vv[k]) {
-          double* o = uf + (int64_t)dd[k] * NCOMP + c;
+        if (cd[k] >= 0) {
+          double* o = uf + (int64_t)cd[k] * NCOMP + c;
           *o = accumulate ? *o + a : a;
         }
       }
@@ -152,138 +174,310 @@ __global__ void __launch_bounds__(kTransferWarps * 32, 6)
   }
 }
 
+// zero the fine DoFs that carry no transfer point (constrained): the
+// non-accumulating prolongation writes every other entry
+__global__ void k_zero_list(const int* __restrict__ list, int64_t n, int ncomp, double* __restrict__ uf) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n * ncomp) uf[(int64_t)list[i / ncomp] * ncomp + i % ncomp] = 0.0;
+}
+
 // ---------------------------------------------------------------------------
 // K7 phase 1: per owning coarse cell the local vector
-//   R_l = sum_pt r_f[pt] W_l(pt),  W = phi_{l2}(z) (phi_{l1}(y) phi_{l0}(x))
-// (transfer.py:104-109, 115).  Deterministic, no atomics:
-//  * NLOC <= 32: every lane accumulates the full local vector over a fixed
-//    subset of the cell's points in registers, then a butterfly reduction
-//    (fixed order) sums the lanes; one pass per component;
-//  * larger NLOC: lanes own local outputs and sweep the cell's points staged
-//    in shared memory.
+//   R_l = sum_pt r_f[pt] W_l(pt),  W = phi_{l2}(z) phi_{l1}(y) phi_{l0}(x)
+// (transfer.py:104-109, 115).  Deterministic, no atomics.
+//
+// A warp owns a chunk of consecutive coarse cells and streams their points in
+// rounds that never straddle a cell.  The gather r_f[pt_dof[p]] is a
+// dependent load chain, so the stream is software-pipelined ACROSS cells: the
+// records (pt_dof, xhat) of round k+2 and the values of round k+1 are in
+// flight while round k is evaluated.  (With ~160 points per coarse cell, a
+// per-cell pipeline spends most of its time in the cell_start -> records ->
+// values latency chain at each cell start.)
 // ---------------------------------------------------------------------------
-template <int DIM, int PC, int NCOMP>
+
+// Round state machine over the cells [c0, c0+nch) of a chunk (nch <= 31).
+// Lane i holds cell_start[c0+i]; rounds of RS points; empty cells are skipped
+// (their outputs are zero-filled separately).  Warp-uniform.
+struct CellRounds {
+  int cs, nch;
+  __device__ __forceinline__ int start(int i) const { return __shfl_sync(0xffffffffu, cs, i); }
+  __device__ __forceinline__ void skip(int& ci, int base) const {
+    while (ci < nch && base >= start(ci + 1)) ++ci;
+  }
+  __device__ __forceinline__ void first(int& ci, int& base) const {
+    ci = 0;
+    base = start(0);
+    skip(ci, base);
+  }
+  __device__ __forceinline__ void next(int& ci, int& base, int rs) const {
+    if (ci >= nch) return;
+    base += rs;
+    const int e = start(ci + 1);
+    if (base >= e) {
+      base = e;
+      ++ci;
+      skip(ci, base);
+    }
+  }
+  __device__ __forceinline__ int end(int ci) const { return start(ci < nch ? ci + 1 : nch); }
+};
+
+__device__ __forceinline__ void zero_empty_cells(const CellRounds& R, int64_t c0, int nout, int lane,
+                                                 double* __restrict__ cellbuf) {
+  const int a = R.start(lane < R.nch ? lane : R.nch), b = R.start(lane < R.nch ? lane + 1 : R.nch);
+  if (lane < R.nch && a == b)
+    for (int o = 0; o < nout; ++o) cellbuf[(c0 + lane) * nout + o] = 0.0;
+}
+
+// per-lane point records of one round: point p = base + k*stride + off
+template <int DIM, int NCOMP, int PPR>
+struct PointRec {
+  int d[PPR];
+  double x[PPR][DIM];
+  __device__ __forceinline__ void load(const int* __restrict__ pt_dof, const double* __restrict__ xhat, int base,
+                                       int end, int stride, int off, bool live) {
+#pragma unroll
+    for (int k = 0; k < PPR; ++k) {
+      const int p = base + k * stride + off;
+      const bool ok = live && p < end;
+      d[k] = ok ? __ldcs(pt_dof + p) : -1;
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) x[k][j] = ok ? __ldcs(xhat + (int64_t)p * DIM + j) : 0.5;
+    }
+  }
+  __device__ __forceinline__ void values(const double* __restrict__ rf, double (&v)[PPR][NCOMP]) const {
+#pragma unroll
+    for (int k = 0; k < PPR; ++k)
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) v[k][c] = d[k] >= 0 ? rf[(int64_t)d[k] * NCOMP + c] : 0.0;
+  }
+};
+
+// The pipelined round loop shared by the restriction kernels.  body(rec_x, v)
+// evaluates the current round; flush(ci) is called after the last round of
+// chunk cell ci.
+template <int DIM, int NCOMP, int PPR, class Body, class Flush>
+__device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __restrict__ pt_dof,
+                                              const double* __restrict__ xhat, const double* __restrict__ rf,
+                                              int stride, int off, bool live, Body&& body, Flush&& flush) {
+  constexpr int RS_K = PPR;
+  const int rs = RS_K * stride;
+  int ciA, bA;
+  R.first(ciA, bA);
+  int ciB = ciA, bB = bA;
+  R.next(ciB, bB, rs);
+  int ciC = ciB, bC = bB;
+  R.next(ciC, bC, rs);
+  PointRec<DIM, NCOMP, PPR> rA, rB, rC;
+  rA.load(pt_dof, xhat, bA, R.end(ciA), stride, off, live && ciA < R.nch);
+  rB.load(pt_dof, xhat, bB, R.end(ciB), stride, off, live && ciB < R.nch);
+  double vA[PPR][NCOMP], vB[PPR][NCOMP];
+  rA.values(rf, vA);
+  while (ciA < R.nch) {
+    rB.values(rf, vB);
+    rC.load(pt_dof, xhat, bC, R.end(ciC), stride, off, live && ciC < R.nch);
+    body(rA.x, vA);
+    if (ciB != ciA) flush(ciA);
+    ciA = ciB;
+    ciB = ciC;
+    bB = bC;
+    R.next(ciC, bC, rs);
+    rA = rB;
+    rB = rC;
+#pragma unroll
+    for (int k = 0; k < PPR; ++k)
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) vA[k][c] = vB[k][c];
+  }
+}
+
+// NLOC*NCOMP <= 32 (Q1/Q2 scalar, 2D vector): a lane owns a point and the full
+// local vector in registers; a cell's lanes are combined by the transposing
+// shuffle reduction, lane l ending with output l.
+template <int DIM, int PC, int NCOMP, int PPR>
 __global__ void __launch_bounds__(kTransferWarps * 32)
-    k_restrict_cells(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
-                     const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc,
-                     double* __restrict__ cellbuf) {
+    k_restrict_lane(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
+                    const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc, int chunk,
+                    double* __restrict__ cellbuf) {
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
   constexpr int NOUT = NLOC * NCOMP;
+  static_assert(NOUT <= 32, "lane-owned local vector");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t cell = blockIdx.x * (int64_t)kTransferWarps + warp;
-  if (cell >= ncc) return;
-  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
-  if constexpr (NLOC <= 32) {
-#pragma unroll 1
-    for (int c = 0; c < NCOMP; ++c) {
-      double acc[NLOC];
+  const int64_t c0 = (blockIdx.x * (int64_t)kTransferWarps + warp) * chunk;
+  if (c0 >= ncc) return;
+  const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
+  const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
+  zero_empty_cells(R, c0, NOUT, lane, cellbuf);
+  double acc[32];
 #pragma unroll
-      for (int l = 0; l < NLOC; ++l) acc[l] = 0.0;
-      // component c of the interleaved vector: values rf[dof*NCOMP + c]
-      PointStream<DIM, 1, NCOMP> ps{pt_dof, xhat, rf + c, p1, 32};
-      for (ps.start(p0 + lane); ps.valid(); ps.advance()) {
-        ps.prefetch();
-        const double v = ps.v0[0];
-        double X[DIM][N1];
+  for (int o = 0; o < 32; ++o) acc[o] = 0.0;
+  stream_rounds<DIM, NCOMP, PPR>(
+      R, pt_dof, xhat, rf, 32, lane, true,
+      [&](const double (&xs)[PPR][DIM], const double (&vs)[PPR][NCOMP]) {
 #pragma unroll
-        for (int j = 0; j < DIM; ++j) lagrange_values<N1>(tab, ps.x0[j], X[j]);
+        for (int k = 0; k < PPR; ++k) {
+          double X[DIM][N1];
 #pragma unroll
-        for (int l = 0; l < NLOC; ++l) {
-          const int i0 = l % N1, i1 = (l / N1) % N1, i2 = l / (N1 * N1);
-          double w = X[1][i1] * X[0][i0];
-          if constexpr (DIM == 3) w = X[2][i2] * w;
-          acc[l] = fma(v, w, acc[l]);
-        }
-      }
+          for (int j = 0; j < DIM; ++j) lagrange_pp<N1>(tab, xs[k][j], X[j]);
 #pragma unroll
-      for (int l = 0; l < NLOC; ++l) {
+          for (int c = 0; c < NCOMP; ++c) {
+            if constexpr (DIM == 3) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
-      }
-      double mine = 0.0;
+              for (int i2 = 0; i2 < N1; ++i2) {
+                const double a = vs[k][c] * X[2][i2];
 #pragma unroll
-      for (int l = 0; l < NLOC; ++l)
-        if (lane == l) mine = acc[l];
-      if (lane < NLOC) cellbuf[cell * NOUT + lane * NCOMP + c] = mine;
-    }
-  } else {
-    // G lanes share a point; lane slice g owns the outermost-axis planes
-    // [g*PPG, (g+1)*PPG) of the local vector, all components, in registers.
-    // Every register index is compile-time: the per-point inner-plane table
-    // IN[i] (x, or x*y in 3D) is static, only the plane's 1D value is
-    // evaluated at a runtime node index.  32/G points per round; fixed-order
-    // butterfly over the point slots at the end.
-    constexpr int INNER = DIM == 3 ? N1 * N1 : N1;  // points per plane
-    // power of two so the xor butterfly keeps each slice's lanes together
-    constexpr int G = (N1 * INNER * NCOMP <= 64) ? 1
-                      : ((N1 + 1) / 2 * INNER * NCOMP <= 80 ? 2 : (N1 <= 4 ? 4 : 8));
-    constexpr int PPG = (N1 + G - 1) / G;             // planes per lane
-    constexpr int SLOTS = 32 / G;
-    const int slice = lane % G, slot = lane / G;
-    double acc[PPG][INNER][NCOMP];
+                for (int i1 = 0; i1 < N1; ++i1) {
+                  const double b = a * X[1][i1];
 #pragma unroll
-    for (int a = 0; a < PPG; ++a)
+                  for (int i0 = 0; i0 < N1; ++i0) {
+                    const int o = (i0 + N1 * (i1 + N1 * i2)) * NCOMP + c;
+                    acc[o] = fma(b, X[0][i0], acc[o]);
+                  }
+                }
+              }
+            } else {
 #pragma unroll
-      for (int i = 0; i < INNER; ++i)
+              for (int i1 = 0; i1 < N1; ++i1) {
+                const double b = vs[k][c] * X[1][i1];
 #pragma unroll
-        for (int c = 0; c < NCOMP; ++c) acc[a][i][c] = 0.0;
-    PointStream<DIM, NCOMP> ps{pt_dof, xhat, rf, p1, SLOTS};
-    for (ps.start(slot < SLOTS ? p0 + slot : p1); ps.valid(); ps.advance()) {
-      ps.prefetch();
-      {
-        const double* v = ps.v0;
-        double X[DIM - 1][N1];
-#pragma unroll
-        for (int j = 0; j < DIM - 1; ++j) lagrange_values<N1>(tab, ps.x0[j], X[j]);
-        // inner table, reference product order X1[i1] * X0[i0] (transfer.py:104-109)
-        double IN[INNER];
-#pragma unroll
-        for (int i = 0; i < INNER; ++i) IN[i] = DIM == 3 ? X[1][i / N1] * X[0][i % N1] : X[0][i];
-        const double tz = ps.x0[DIM - 1];
-#pragma unroll
-        for (int a = 0; a < PPG; ++a) {
-          const int plane = slice * PPG + a;
-          if (plane < N1) {
-            // phi_plane(tz) with a runtime node index (no register-array indexing)
-            double z = 1.0;
-#pragma unroll
-            for (int j = 0; j < N1; ++j) z *= (j == plane) ? tab.rdenom[plane < N1 ? plane : 0] : (tz - tab.nodes[j]);
-            double vz[NCOMP];
-#pragma unroll
-            for (int c = 0; c < NCOMP; ++c) vz[c] = v[c] * z;
-#pragma unroll
-            for (int i = 0; i < INNER; ++i)
-#pragma unroll
-              for (int c = 0; c < NCOMP; ++c) acc[a][i][c] = fma(vz[c], IN[i], acc[a][i][c]);
+                for (int i0 = 0; i0 < N1; ++i0) {
+                  const int o = (i0 + N1 * i1) * NCOMP + c;
+                  acc[o] = fma(b, X[0][i0], acc[o]);
+                }
+              }
+            }
           }
         }
-      }
-    }
+      },
+      [&](int ci) {
+        const double r = transpose_reduce<NOUT>(acc, lane);
+        if (lane < NOUT) cellbuf[(c0 + ci) * NOUT + lane] = r;
 #pragma unroll
-    for (int a = 0; a < PPG; ++a)
+        for (int o = 0; o < 32; ++o) acc[o] = 0.0;
+      });
+}
+
+// NLOC*NCOMP > 32 (3D Q2 elasticity, Q3/Q4 scalar).  Rounds of P = SLOTS*SUB
+// points (SLOTS = 32/N1): every lane loads one point and evaluates its full 1D
+// tables (prefix/suffix products, once per point) into a shared staging
+// buffer; then, in SUB sub-rounds, the N1 lanes of a slot share a staged point
+// and lane g accumulates the outermost-axis plane l_last = g of the local
+// vector (all components) in registers.  Slots are combined in shared memory
+// in a fixed order at each cell end.
+template <int DIM, int PC, int NCOMP>
+struct StagedRestrict {
+  static constexpr int N1 = PC + 1;
+  static constexpr int NLOC = ipow(N1, DIM);
+  static constexpr int NOUT = NLOC * NCOMP;
+  static constexpr int G = N1;
+  static constexpr int SLOTS = 32 / G;
+  static constexpr int SUB = 32 / SLOTS;
+  static constexpr int P = SLOTS * SUB;  // points per round
+  static constexpr int INNER = NLOC / N1;
+  static constexpr int PLANE = INNER * NCOMP;
+  static constexpr int REC0 = DIM * N1 + NCOMP;
+  static constexpr int REC = REC0 | 1;  // odd stride in doubles: distinct banks across slots
+  static constexpr int WARP_DOUBLES = 2 * P * REC + SLOTS * G * PLANE;
+  static constexpr int WARPS = (48 * 1024) / (WARP_DOUBLES * 8) >= kTransferWarps
+                                   ? kTransferWarps
+                                   : ((48 * 1024) / (WARP_DOUBLES * 8) >= 1 ? (48 * 1024) / (WARP_DOUBLES * 8) : 1);
+};
+
+template <int DIM, int PC, int NCOMP>
+__global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
+    k_restrict_staged(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
+                      const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc, int chunk,
+                      double* __restrict__ cellbuf) {
+  using K = StagedRestrict<DIM, PC, NCOMP>;
+  constexpr int N1 = K::N1, G = K::G, SLOTS = K::SLOTS, SUB = K::SUB, P = K::P, INNER = K::INNER,
+                PLANE = K::PLANE, REC = K::REC, NOUT = K::NOUT;
+  __shared__ double smem[K::WARPS][K::WARP_DOUBLES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = (blockIdx.x * (int64_t)K::WARPS + warp) * chunk;
+  if (c0 >= ncc) return;
+  const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
+  double* stage = smem[warp];                // [2][P][REC]
+  double* red = smem[warp] + 2 * P * REC;    // [SLOTS*G][PLANE]
+  const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
+  zero_empty_cells(R, c0, NOUT, lane, cellbuf);
+  const int slot = lane / G, g = lane % G;
+  const bool grp = slot < SLOTS;
+  double acc[INNER][NCOMP];
 #pragma unroll
-      for (int i = 0; i < INNER; ++i)
+  for (int i = 0; i < INNER; ++i)
 #pragma unroll
-        for (int c = 0; c < NCOMP; ++c) {
-          double s = acc[a][i][c];
+    for (int c = 0; c < NCOMP; ++c) acc[i][c] = 0.0;
+  int buf = 0;
+  stream_rounds<DIM, NCOMP, 1>(
+      R, pt_dof, xhat, rf, P, lane, lane < P,
+      [&](const double (&xs)[1][DIM], const double (&vs)[1][NCOMP]) {
+        // stage this lane's point: 1D tables and values
+        double* st = stage + buf * P * REC;
+        if (lane < P) {
+          double X[N1];
 #pragma unroll
-          for (int off = G; off < 32; off <<= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-          acc[a][i][c] = s;
+          for (int j = 0; j < DIM; ++j) {
+            lagrange_pp<N1>(tab, xs[0][j], X);
+#pragma unroll
+            for (int i = 0; i < N1; ++i) st[lane * REC + j * N1 + i] = X[i];
+          }
+#pragma unroll
+          for (int c = 0; c < NCOMP; ++c) st[lane * REC + DIM * N1 + c] = vs[0][c];
         }
-    if (slot == 0) {
+        __syncwarp();
+        if (grp) {
+#pragma unroll 1
+          for (int s = 0; s < SUB; ++s) {
+            const double* q = st + (s * SLOTS + slot) * REC;
+            double X0[N1], X1[DIM == 3 ? N1 : 1];
 #pragma unroll
-      for (int a = 0; a < PPG; ++a) {
-        const int plane = slice * PPG + a;
-        if (plane < N1) {
+            for (int i = 0; i < N1; ++i) X0[i] = q[i];
+            if constexpr (DIM == 3) {
+#pragma unroll
+              for (int i = 0; i < N1; ++i) X1[i] = q[N1 + i];
+            }
+            const double z = q[(DIM - 1) * N1 + g];
+#pragma unroll
+            for (int c = 0; c < NCOMP; ++c) {
+              const double a = q[DIM * N1 + c] * z;
+              if constexpr (DIM == 3) {
+#pragma unroll
+                for (int i1 = 0; i1 < N1; ++i1) {
+                  const double b = a * X1[i1];
+#pragma unroll
+                  for (int i0 = 0; i0 < N1; ++i0) acc[i0 + N1 * i1][c] = fma(b, X0[i0], acc[i0 + N1 * i1][c]);
+                }
+              } else {
+#pragma unroll
+                for (int i0 = 0; i0 < N1; ++i0) acc[i0][c] = fma(a, X0[i0], acc[i0][c]);
+              }
+            }
+          }
+        }
+        buf ^= 1;  // the next round writes the other buffer: one barrier per round
+      },
+      [&](int ci) {
+        if (grp) {
 #pragma unroll
           for (int i = 0; i < INNER; ++i)
 #pragma unroll
-            for (int c = 0; c < NCOMP; ++c) cellbuf[cell * NOUT + (plane * INNER + i) * NCOMP + c] = acc[a][i][c];
+            for (int c = 0; c < NCOMP; ++c) {
+              red[lane * PLANE + i * NCOMP + c] = acc[i][c];
+              acc[i][c] = 0.0;
+            }
         }
-      }
-    }
-  }
+        __syncwarp();
+        // output o = l * NCOMP + c with l = plane * INNER + i: slot sum in fixed order
+        for (int o = lane; o < NOUT; o += 32) {
+          const int plane = o / PLANE, k = o % PLANE;
+          double sum = 0.0;
+#pragma unroll
+          for (int sl = 0; sl < SLOTS; ++sl) sum += red[(sl * G + plane) * PLANE + k];
+          cellbuf[(c0 + ci) * NOUT + o] = sum;
+        }
+        __syncwarp();
+      });
 }
 
 // K7 phase 2: r_c[g] = sum over the (cell, l) slots holding g, fixed order
