@@ -76,6 +76,26 @@ def transfer_bytes(dim, p, ncomp, npts, n_dofs_coarse, n_cells_coarse):
     return npts * (4 + 4 + 8 * dim + 8 * ncomp) + 8 * n_dofs_coarse + 4 * n_cells_coarse * nloc
 
 
+def vmult_flops(dim, p, ncomp, n_cells, physics):
+    """F = nc [4 d^2 ncomp n1^(d+1) + nq f_qp]."""
+    n1 = p + 1
+    fqp = 2 * dim * dim + dim if physics == "poisson" else 150
+    return n_cells * (4 * dim * dim * ncomp * n1 ** (dim + 1) + n1 ** dim * fqp)
+
+
+def transfer_flops(dim, p, ncomp, npts):
+    """contraction + 1D basis evaluation from xhat."""
+    n1 = p + 1
+    return npts * ncomp * 2 * sum(n1 ** k for k in range(1, dim + 1)) + npts * dim * n1 * 2 * (n1 - 1)
+
+
+def roof_frac(t, nbytes, flops, hbm_gbs, fp64_tflops):
+    """t_roof / t with t_roof = max(B / HBM, F / FP64) and the binding resource."""
+    tb = nbytes / (hbm_gbs * 1e9)
+    tf = flops / (fp64_tflops * 1e12) if fp64_tflops else 0.0
+    return max(tb, tf) / t, ("hbm" if tb >= tf else "fp64")
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -349,6 +369,12 @@ def run_ours(args, cfg):
     t_res = e1.elapsed_time(e2) * 1e-3 / reps
     cm = T.coarse_space.mesh
     BT = transfer_bytes(sp.mesh.dim, T.coarse_space.degree, ncomp, len(T.cells), T.coarse_space.n_dofs, cm.n_cells)
+    FT = transfer_flops(sp.mesh.dim, T.coarse_space.degree, ncomp, len(T.cells))
+    FV = vmult_flops(sp.mesh.dim, sp.degree, ncomp, sp.mesh.n_cells, cfg.problem)
+    fp64 = _lib.fp64_peak(local)
+    v_rf, v_bound = roof_frac(t_apply, B, FV, peak, fp64)
+    p_rf, p_bound = roof_frac(t_pro, BT, FT, peak, fp64)
+    r_rf, r_bound = roof_frac(t_res, BT, FT, peak, fp64)
     applies_per_cycle = 2 * cfg.chebyshev_degree + 1
 
     # ---- optional full solve ----
@@ -392,6 +418,10 @@ def run_ours(args, cfg):
                 "prolongate_ms": t_pro * 1e3, "prolongate_frac": BT / t_pro / 1e9 / peak,
                 "restrict_ms": t_res * 1e3, "restrict_frac": BT / t_res / 1e9 / peak,
                 "transfer_bytes": BT, "geometry_bytes": info["geometry_bytes"],
+                "fp64_peak_tflops": fp64, "vmult_flops": FV, "transfer_flops": FT,
+                "vmult_roof_frac": v_rf, "vmult_bound": v_bound,
+                "prolongate_roof_frac": p_rf, "prolongate_bound": p_bound,
+                "restrict_roof_frac": r_rf, "restrict_bound": r_bound,
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},

@@ -48,6 +48,9 @@ int nnmg_abi_version(void);
 const char* nnmg_last_error(void);
 /* number of kernels this library has launched so far (process-wide) */
 uint64_t nnmg_launch_count(void);
+/* measured DFMA throughput of `device` in TFLOP/s (synchronises; the FP64
+ * roofline denominator bench.py reports - not on any hot path) */
+int nnmg_measure_fp64_peak(int device, double* tflops);
 
 /* ---- levels: replaces _OperatorBase.__init__ (mfoperator.py:28-48),
  *      LaplaceOperator.__init__ (mfoperator.py:101-106) and

@@ -40,6 +40,7 @@ _SIGNATURES = {
     "nnmg_abi_version": [],
     "nnmg_last_error": [],
     "nnmg_launch_count": [],
+    "nnmg_measure_fp64_peak": [c_int, POINTER(c_double)],
     "nnmg_level_create": [c_int, c_int, c_int, c_int, c_int, c_int64, c_int64, c_void_p, c_void_p, c_int64,
                           c_void_p, c_int64, c_void_p, c_double, c_double, POINTER(_handle)],
     "nnmg_level_destroy": [_handle],
@@ -136,3 +137,10 @@ def as_i64(a):
 
 def as_f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def fp64_peak(device=0):
+    """Measured DFMA throughput (TFLOP/s) of ``device``: the FP64 roofline denominator."""
+    out = ctypes.c_double(0.0)
+    call("nnmg_measure_fp64_peak", int(device), ctypes.byref(out))
+    return out.value

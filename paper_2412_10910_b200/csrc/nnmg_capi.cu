@@ -45,6 +45,13 @@ int nnmg_abi_version(void) { return 1; }
 const char* nnmg_last_error(void) { return last_error(); }
 uint64_t nnmg_launch_count(void) { return launch_count(); }
 
+int nnmg_measure_fp64_peak(int device, double* tflops) {
+  return guard([&] {
+    NNMG_REQUIRE(tflops, kInvalidArgument, "null argument");
+    *tflops = measure_fp64_peak(device);
+  });
+}
+
 int nnmg_level_create(int device, int dim, int degree, int n_components, int physics, int64_t n_cells,
                       int64_t n_vertices, const double* vertices_host, const int64_t* cells_host,
                       int64_t n_scalar_dofs, const int64_t* cell_dofs_host, int64_t n_constrained,

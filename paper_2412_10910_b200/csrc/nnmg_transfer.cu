@@ -35,8 +35,10 @@ struct TransferDispatch {
       const int ch = T.chunk;
       const int64_t nwarps = (T.ncc + ch - 1) / ch;
       if constexpr (ipow(P + 1, D) * NC <= 32) {
-        if (T.restrict_kernel == 0 || T.restrict_kernel == 1) {
-          auto k = T.restrict_kernel == 0 ? k_restrict_lane<D, P, NC, 1> : k_restrict_lane<D, P, NC, 2>;
+        if (T.restrict_kernel != 2) {
+          auto k = T.restrict_kernel == 0 ? k_restrict_lane<D, P, NC, 1>
+                   : T.restrict_kernel == 3 ? k_restrict_lane<D, P, NC, 3>
+                                            : k_restrict_lane<D, P, NC, 2>;
           k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
                                                             T.ncc, ch, T.cellbuf.ptr);
         } else {
@@ -119,7 +121,7 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
       int ch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, ncc / target_warps)));
       if (e) ch = std::max(1, std::min(31, atoi(e)));
       T->chunk = ch;
-      // NLOC*NCOMP <= 32: 0 = lane-owned (1 point/round), 1 = lane-owned (2), 2 = staged groups
+      // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups
       const char* k = getenv("NNMG_RESTRICT_KERNEL");
       T->restrict_kernel = k ? atoi(k) : 1;
     }

@@ -213,3 +213,51 @@ void cg_update(int64_t n, double alpha, const double* p, const double* ap, doubl
 }
 
 }  // namespace nnmg
+
+// ---------------------------------------------------------------------------
+// FP64 roofline denominator: dependent-chain-free DFMA throughput (8
+// independent chains per thread, 16 warps per SM), timed with CUDA events.
+// MEASURED_PEAKS.json carries no FP64 figure; bench.py reports this one.
+// ---------------------------------------------------------------------------
+namespace nnmg {
+
+__global__ void k_dfma_probe(double* out, int iters, double b, double c) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
+double measure_fp64_peak(int device) {
+  NNMG_CUDA_TRY(cudaSetDevice(device));
+  int sms = 0;
+  NNMG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  DevBuf<double> out;
+  out.alloc(1);
+  const int threads = 512, blocks = sms * 4, iters = 4096;
+  cudaEvent_t e0, e1;
+  NNMG_CUDA_TRY(cudaEventCreate(&e0));
+  NNMG_CUDA_TRY(cudaEventCreate(&e1));
+  k_dfma_probe<<<blocks, threads>>>(out.ptr, 64, 0.999, 1e-3);  // warm-up
+  NNMG_CUDA_TRY(cudaEventRecord(e0));
+  k_dfma_probe<<<blocks, threads>>>(out.ptr, iters, 0.999, 1e-3);
+  NNMG_CUDA_TRY(cudaEventRecord(e1));
+  NNMG_CUDA_TRY(cudaEventSynchronize(e1));
+  NNMG_CHECK_LAUNCH();
+  count_launch(2);
+  float ms = 0.f;
+  NNMG_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = 2.0 * 8.0 * iters * double(threads) * blocks;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
+}  // namespace nnmg

@@ -21,4 +21,7 @@ void sub(int64_t n, const double* a, const double* b, double* out, cudaStream_t 
 void mul(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
 void cg_update(int64_t n, double alpha, const double* p, const double* ap, double* x, double* r, cudaStream_t s);
 
+// DFMA throughput of the device in TFLOP/s (roofline denominator for FP64-bound kernels)
+double measure_fp64_peak(int device);
+
 }  // namespace nnmg
