@@ -1,0 +1,188 @@
+// Register-resident elasticity cell kernel (K2, 3D, NLOC <= 27): one thread
+// per (cell, component).
+//
+// The pencil kernel (nnmg_cellkernel.cuh) keeps every sweep intermediate of
+// the 3 x 27 cell values in shared memory; ncu shows it L1/shared-pipe bound
+// on C5 (l1tex 92% busy, mio_throttle the top stall, DRAM 33%).  Here a CTA of
+// 3 warps owns one block of 32 cells and warp w holds component w of them:
+// gather, the three interpolation sweeps, the collocation gradient, the
+// transposed sweeps and the scatter all run in registers exactly as the
+// Laplace register kernel (nnmg_cellreg.cuh).  Only the quadrature-point
+// physics couples the components (mfoperator.py:183-191); it runs per
+// z-slice of 9 points with two shared-memory exchanges:
+//   A  every thread writes d u_w / d xhat (3 values) at the 9 points;
+//   B  thread w evaluates the full stress at points s = w, w+3, w+6 of the
+//      slice (so each geometry entry J^-1, |det J| w_q is loaded exactly once)
+//      and writes the reference flux of all 3 components;
+//   C  every thread reads its component's flux and applies the transposed
+//      collocation derivatives.
+// Shared memory is [point][component][direction][cell] (cell fastest: no bank
+// conflicts), 2 x 20.7 KB per CTA.
+#pragma once
+
+#include "nnmg_kernels.cuh"
+
+namespace nnmg {
+
+template <int P>
+struct CellRegElast {
+  static constexpr int DIM = 3;
+  static constexpr int N1 = P + 1;
+  static constexpr int NLOC = N1 * N1 * N1;
+  static constexpr int CB = 32;
+  static constexpr int NG = DIM * DIM + 1;  // J^-1 row-major, then |det J| w_q
+  static constexpr int SLICE = N1 * N1;     // quadrature points per z-slice
+  static constexpr int PER = (SLICE + 2) / 3;  // points per thread in phase B
+  static constexpr bool kSupported = NLOC <= 27;
+  static constexpr int SMEM_DOUBLES = 2 * SLICE * 9 * CB;
+
+  __host__ __device__ static constexpr int at(int i0, int i1, int i2) { return i0 + N1 * (i1 + N1 * i2); }
+
+  template <int K, bool TRANS>
+  __device__ __forceinline__ static void sweep_axis(const double (&M)[kMaxN1][kMaxN1], double (&v)[NLOC]) {
+    constexpr int S0 = K == 0 ? 1 : (K == 1 ? N1 : N1 * N1);
+    constexpr int NL = NLOC / N1;
+#pragma unroll
+    for (int line = 0; line < NL; ++line) {
+      int base;
+      if constexpr (K == 0)
+        base = line * N1;
+      else if constexpr (K == 1)
+        base = (line % N1) + (line / N1) * N1 * N1;
+      else
+        base = line;
+      double in[N1], out[N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) in[i] = v[base + i * S0];
+#pragma unroll
+      for (int q = 0; q < N1; ++q) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < N1; ++i) s = fma(TRANS ? M[i][q] : M[q][i], in[i], s);
+        out[q] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < N1; ++i) v[base + i * S0] = out[i];
+    }
+  }
+
+  // one cell block; threads: w = threadIdx.x / 32 (component), lane = cell
+  template <bool kNeg>
+  __device__ __forceinline__ static void run(const Tables& tab, const double* __restrict__ src, double* __restrict__ dst,
+                                             const int* __restrict__ idx, const double* __restrict__ geo, int64_t blk,
+                                             double lam, double mu, double* sm) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w == 0 && lane == 0) {
+      constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
+      prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+    }
+    double* gbuf = sm;                     // [SLICE][3 comps][3 dirs][CB]
+    double* fbuf = sm + SLICE * 9 * CB;    // same layout, reference flux
+    double v[NLOC];
+    const int* ib = idx + blk * NLOC * CB + lane;
+#pragma unroll
+    for (int l = 0; l < NLOC; ++l) {
+      const int g = __ldcs(ib + l * CB);
+      v[l] = g >= 0 ? __ldg(src + (int64_t)g * 3 + w) : 0.0;
+    }
+    sweep_axis<0, false>(tab.S, v);
+    sweep_axis<1, false>(tab.S, v);
+    sweep_axis<2, false>(tab.S, v);
+    double acc[NLOC];
+#pragma unroll
+    for (int l = 0; l < NLOC; ++l) acc[l] = 0.0;
+    const double* gb = geo + blk * (int64_t)NLOC * NG * CB + lane;
+#pragma unroll
+    for (int qz = 0; qz < N1; ++qz) {
+      // A: d u_w / d xhat_j at the slice's points (collocation)
+#pragma unroll
+      for (int s = 0; s < SLICE; ++s) {
+        const int qx = s % N1, qy = s / N1;
+        double gx = 0.0, gy = 0.0, gz = 0.0;
+#pragma unroll
+        for (int r = 0; r < N1; ++r) {
+          gx = fma(tab.Dc[qx][r], v[at(r, qy, qz)], gx);
+          gy = fma(tab.Dc[qy][r], v[at(qx, r, qz)], gy);
+          gz = fma(tab.Dc[qz][r], v[at(qx, qy, r)], gz);
+        }
+        double* o = gbuf + ((s * 3 + w) * 3) * CB + lane;
+        o[0] = gx;
+        o[CB] = gy;
+        o[2 * CB] = gz;
+      }
+      __syncthreads();
+      // B: full stress at points s = w + 3k of the slice
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int s = w + 3 * k;
+        if (s < SLICE) {
+          const double* G = gb + (qz * SLICE + s) * NG * CB;
+          double K[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) K[a][b] = __ldcs(G + (a * 3 + b) * CB);
+          const double dv = __ldcs(G + 9 * CB);
+          double g[3][3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[c][j] = gbuf[((s * 3 + c) * 3 + j) * CB + lane];
+          // pg = ghat J^-1, eps = sym(pg), sigma = 2 mu eps + lam tr(eps) I, flux = sigma J^-T dv
+          double pg[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              double t = 0.0;
+#pragma unroll
+              for (int j = 0; j < 3; ++j) t = fma(g[a][j], K[j][b], t);
+              pg[a][b] = t;
+            }
+          const double tr = pg[0][0] + pg[1][1] + pg[2][2];
+          double sig[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) sig[a][b] = mu * (pg[a][b] + pg[b][a]) + (a == b ? lam * tr : 0.0);
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              double t = 0.0;
+#pragma unroll
+              for (int b = 0; b < 3; ++b) t = fma(sig[a][b], K[j][b], t);
+              fbuf[((s * 3 + a) * 3 + j) * CB + lane] = t * dv;
+            }
+        }
+      }
+      __syncthreads();
+      // C: transposed collocation derivatives of this component's flux
+#pragma unroll
+      for (int s = 0; s < SLICE; ++s) {
+        const int qx = s % N1, qy = s / N1;
+        const double* f = fbuf + ((s * 3 + w) * 3) * CB + lane;
+        const double fx = f[0], fy = f[CB], fz = f[2 * CB];
+#pragma unroll
+        for (int r = 0; r < N1; ++r) {
+          acc[at(r, qy, qz)] = fma(tab.Dc[qx][r], fx, acc[at(r, qy, qz)]);
+          acc[at(qx, r, qz)] = fma(tab.Dc[qy][r], fy, acc[at(qx, r, qz)]);
+          acc[at(qx, qy, r)] = fma(tab.Dc[qz][r], fz, acc[at(qx, qy, r)]);
+        }
+      }
+      // the next slice's phase A overwrites gbuf only after every thread
+      // passed the phase-B barrier above; fbuf is rewritten after the next
+      // phase-A barrier, which every phase-C reader has passed
+    }
+    sweep_axis<2, true>(tab.S, acc);
+    sweep_axis<1, true>(tab.S, acc);
+    sweep_axis<0, true>(tab.S, acc);
+#pragma unroll
+    for (int l = 0; l < NLOC; ++l) {
+      const int g = __ldg(ib + l * CB);
+      if (g >= 0) atomicAdd(dst + (int64_t)g * 3 + w, kNeg ? -acc[l] : acc[l]);
+    }
+  }
+};
+
+}  // namespace nnmg

@@ -3,6 +3,7 @@
 #include "nnmg_kernels.cuh"
 #include "nnmg_cellkernel.cuh"
 #include "nnmg_cellreg.cuh"
+#include "nnmg_cellreg_elast.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -399,6 +400,18 @@ __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const doubl
   CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
 }
 
+// 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
+template <int P, bool NEG>
+__global__ void __launch_bounds__(96) k_apply_reg_elast(Tables tab, const double* __restrict__ src,
+                                                        double* __restrict__ dst, const int* __restrict__ idx,
+                                                        const double* __restrict__ geo, int64_t b0, int64_t b1,
+                                                        double lam, double mu) {
+  __shared__ double sm[CellRegElast<P>::SMEM_DOUBLES];
+  const int64_t blk = b0 + blockIdx.x;
+  if (blk >= b1) return;
+  CellRegElast<P>::template run<NEG>(tab, src, dst, idx, geo, blk, lam, mu, sm);
+}
+
 // per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
 template <int DIM>
 __global__ void k_edges(const double* __restrict__ verts, const int* __restrict__ cells, int64_t n_cells, int cb,
@@ -441,6 +454,16 @@ struct ApplyLaunch {
                                                 : k_apply_reg<D, P, 1, false, false>));
         kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
                                             hyb ? L.recompute_mod : 0);
+        NNMG_CHECK_LAUNCH();
+        count_launch();
+        return;
+      }
+    }
+    if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported) {
+      if (L.reg_kernel) {
+        const int64_t nb = b1 - b0;
+        auto kr = neg ? k_apply_reg_elast<P, true> : k_apply_reg_elast<P, false>;
+        kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.lam, L.mu);
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;
