@@ -62,6 +62,8 @@ struct CellKernel {
   static constexpr int NTHREADS = NPEN * SCB;
   static constexpr int NBUF = 3;
   static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * SCB * sizeof(double);
+  // kGeoS: the sub-block's geometry staged in shared memory behind SMEM
+  static constexpr size_t GEO_SMEM = size_t(NLOC) * NG * SCB * sizeof(double);
   using PL = Pencil<DIM, N1>;
 
   __device__ __forceinline__ static double& S(double* sm, int b, int c, int pos, int lane) {
@@ -118,7 +120,7 @@ struct CellKernel {
     for (int i = 0; i < N1; ++i) gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * GS + glane);
   }
 
-  template <bool kRes = false, bool kNeg = false, class Src, class Sync>
+  template <bool kRes = false, bool kNeg = false, bool kGeoS = false, class Src, class Sync>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
@@ -126,7 +128,23 @@ struct CellKernel {
     // the block's geometry chunk (85% of the bytes) is consumed only in phase
     // 5: start streaming it into L2 now so it overlaps gathers and sweeps
     constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
-    if (!kRes && lane_off == 0 && tid == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+    if constexpr (kGeoS) {
+      // kGeoS: copy the sub-block's geometry rows (SCB doubles of each
+      // [q][k] row) into shared memory asynchronously (LDGSTS, L2 only); it
+      // lands while the gathers and sweeps run and is waited for before P5
+      static_assert(!kRes && (SCB * sizeof(double)) % 16 == 0, "16-byte chunks");
+      double* gs = sm + SMEM / sizeof(double);
+      constexpr int CH = SCB * sizeof(double) / 16;
+      constexpr int TOT = NLOC * NG * CH;
+      const double* gsrc = geo + blk * (int64_t)NLOC * NG * CB + lane_off;
+      for (int i = tid; i < TOT; i += NTHREADS) {
+        const int row = i / CH, ch = i % CH;
+        cp_async16(gs + row * SCB + ch * 2, gsrc + (int64_t)row * CB + ch * 2);
+      }
+      cp_async_commit();
+    } else if (!kRes && lane_off == 0 && tid == 0) {
+      prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+    }
     int gi[N1];
     pencil_dofs<kRes>(idx, blk, tid, lane_off, gi);
     double v[NCOMP][N1];
@@ -134,12 +152,12 @@ struct CellKernel {
     for (int i = 0; i < N1; ++i)
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
-    return run_values<kRes, kNeg>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off);
+    return run_values<kRes, kNeg, kGeoS>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off);
   }
 
   // the cell kernel from gathered pencil values v (zero on gi < 0) onwards;
   // callers that can issue the gather early (the coarse CG) enter here
-  template <bool kRes = false, bool kNeg = false, class Sync>
+  template <bool kRes = false, bool kNeg = false, bool kGeoS = false, class Sync>
   __device__ __forceinline__ static double run_values(const Tables& tab, const int (&gi)[N1],
                                                       double (&v)[NCOMP][N1], double* __restrict__ dst,
                                                       const double* __restrict__ geo, int64_t blk, double lam,
@@ -194,6 +212,7 @@ struct CellKernel {
         store<1>(sm, GY, pen, lsub, w);
       }
     }
+    if constexpr (kGeoS) cp_async_wait_all();
     sync();
     NNMG_CT(4);
     // P5: quadrature-point physics on the last-axis pencil
@@ -211,7 +230,10 @@ struct CellKernel {
           if constexpr (DIM == 3) g[c][1] = S(sm, GY, c, pos, lsub);
           g[c][DIM - 1] = gl[c][q];
         }
-        qp_flux<DIM, NCOMP, PHYS, GS, !kRes>(geo + ((blk * (int64_t)NLOC + pos) * NG) * GS + glane, g, f, lam, mu);
+        if constexpr (kGeoS)
+          qp_flux<DIM, NCOMP, PHYS, SCB, false>(sm + SMEM / sizeof(double) + pos * NG * SCB + lsub, g, f, lam, mu);
+        else
+          qp_flux<DIM, NCOMP, PHYS, GS, !kRes>(geo + ((blk * (int64_t)NLOC + pos) * NG) * GS + glane, g, f, lam, mu);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           fx[c][q] = f[c][0];

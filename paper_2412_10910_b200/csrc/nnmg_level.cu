@@ -100,14 +100,20 @@ using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PH
 #ifndef NNMG_APPLY_MINB
 #define NNMG_APPLY_MINB 5
 #endif
-template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT>
-__global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHREADS, SPLIT == 1 ? 1 : NNMG_APPLY_MINB)
+// with the geometry staged in shared memory (GEOS) fewer CTAs fit per SM
+#ifndef NNMG_APPLY_MINB_GEOS
+#define NNMG_APPLY_MINB_GEOS 3
+#endif
+template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, bool GEOS = false>
+__global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHREADS,
+                                  SPLIT == 1 ? 1 : (GEOS ? NNMG_APPLY_MINB_GEOS : NNMG_APPLY_MINB))
     k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
             const double* __restrict__ geo, int64_t b0, double lam, double mu) {
   extern __shared__ double sm[];
   using CK = ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>;
-  CK::template run<false, NEG>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm, threadIdx.x,
-                               [] __device__() { __syncthreads(); }, int(blockIdx.x % SPLIT) * CK::SCB);
+  CK::template run<false, NEG, GEOS>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm,
+                                     threadIdx.x, [] __device__() { __syncthreads(); },
+                                     int(blockIdx.x % SPLIT) * CK::SCB);
 }
 
 // ---------------------------------------------------------------------------
@@ -286,7 +292,11 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
         // measured on B200: Q4 Laplace (C4) 0.684 -> 0.613 ms with 4, Q2
         // elasticity (C5) 0.288 -> 0.279 ms with 2
         L->apply_split = sp ? atoi(sp) : (dim == 3 && degree >= 4 ? 4 : (ncomp > 1 ? 2 : 1));
-        if (L->apply_split != 2 && L->apply_split != 4) L->apply_split = 1;
+        if (L->apply_split != 2 && L->apply_split != 4 && L->apply_split != 8) L->apply_split = 1;
+        // Q3/Q4: geometry staged in shared memory by LDGSTS (k_apply GEOS)
+        const char* gs = getenv("NNMG_APPLY_GEOS");
+        // measured on B200 (C4): 0.643 ms with, 0.641 ms without: opt-in
+        L->apply_geos = gs ? atoi(gs) != 0 : false;
       }
       L->reg_minb = m ? atoi(m) : 1;
       const char* rm = getenv("NNMG_RECOMPUTE_MOD");
@@ -469,27 +479,34 @@ struct ApplyLaunch {
         return;
       }
     }
+    if constexpr (D == 3 && P >= 3 && CK::CB % 16 == 0) {
+      if (L.apply_geos) {
+        if (L.apply_split == 8) return launch<D, P, NC, PH, 8, true>();
+        if (L.apply_split == 4) return launch<D, P, NC, PH, 4, true>();
+      }
+    }
     if (L.apply_split == 4) return launch<D, P, NC, PH, 4>();
     if (L.apply_split == 2) return launch<D, P, NC, PH, 2>();
     launch<D, P, NC, PH, 1>();
   }
-  template <int D, int P, int NC, int PH, int SPLIT>
+  template <int D, int P, int NC, int PH, int SPLIT, bool GEOS = false>
   void launch() {
     using CK = ApplyKernel<D, P, NC, PH, SPLIT>;
-    auto kern = neg ? k_apply<D, P, NC, PH, true, SPLIT> : k_apply<D, P, NC, PH, false, SPLIT>;
+    constexpr size_t kSmem = CK::SMEM + (GEOS ? CK::GEO_SMEM : 0);
+    auto kern = neg ? k_apply<D, P, NC, PH, true, SPLIT, GEOS> : k_apply<D, P, NC, PH, false, SPLIT, GEOS>;
     static bool attr = false;
     if (!attr) {
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true, SPLIT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK::SMEM));
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false, SPLIT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CK::SMEM));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true, SPLIT, GEOS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false, SPLIT, GEOS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
       attr = true;
     }
     const int64_t nb = (b1 - b0) * SPLIT;
     constexpr int64_t kMaxGrid = (0x7fffffff / SPLIT) * SPLIT;
     for (int64_t off = 0; off < nb; off += kMaxGrid) {
       const unsigned g = static_cast<unsigned>(std::min<int64_t>(nb - off, kMaxGrid));
-      kern<<<g, CK::NTHREADS, CK::SMEM, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0 + off / SPLIT, L.lam, L.mu);
+      kern<<<g, CK::NTHREADS, kSmem, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0 + off / SPLIT, L.lam, L.mu);
       NNMG_CHECK_LAUNCH();
       count_launch();
     }
