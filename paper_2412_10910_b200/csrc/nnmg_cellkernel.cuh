@@ -62,8 +62,15 @@ struct CellKernel {
   static constexpr int NTHREADS = NPEN * SCB;
   static constexpr int NBUF = 3;
   static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * SCB * sizeof(double);
-  // kGeoS: the sub-block's geometry staged in shared memory behind SMEM
+  // geometry modes (template GEO of run / run_values):
+  //   0  stored G / J^-1 streamed from HBM (L2 bulk prefetch)
+  //   1  stored, the sub-block's rows staged in shared memory (LDGSTS) behind SMEM
+  //   2  3D Laplace: G recomputed from the cell's 12 edge vectors (36 doubles,
+  //      staged in shared memory behind SMEM) - 288 B per cell instead of
+  //      NLOC*6*8 (6 KB for Q4), traded for ~60 FP64 operations per point
+  static constexpr int NE = DIM * (1 << (DIM - 1)) * DIM;
   static constexpr size_t GEO_SMEM = size_t(NLOC) * NG * SCB * sizeof(double);
+  static constexpr size_t EDGE_SMEM = size_t(NE) * SCB * sizeof(double);
   using PL = Pencil<DIM, N1>;
 
   __device__ __forceinline__ static double& S(double* sm, int b, int c, int pos, int lane) {
@@ -99,6 +106,9 @@ struct CellKernel {
     }
   }
 
+  // GEO 2 receives the edge-vector table in place of the geometry pointer
+  __device__ __forceinline__ static const double* edges_of(const double* p) { return p; }
+
   // one cell block; the NTHREADS threads tid = 0..NTHREADS-1 of a (sub)group
   // participate, `sync` synchronises exactly that group.  kNC selects the
   // read-only (non-coherent) path for the source vector, which is only legal
@@ -120,7 +130,7 @@ struct CellKernel {
     for (int i = 0; i < N1; ++i) gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * GS + glane);
   }
 
-  template <bool kRes = false, bool kNeg = false, bool kGeoS = false, class Src, class Sync>
+  template <bool kRes = false, bool kNeg = false, int GEO = 0, class Src, class Sync>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
@@ -128,7 +138,20 @@ struct CellKernel {
     // the block's geometry chunk (85% of the bytes) is consumed only in phase
     // 5: start streaming it into L2 now so it overlaps gathers and sweeps
     constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
-    if constexpr (kGeoS) {
+    if constexpr (GEO == 2) {
+      static_assert(!kRes && DIM == 3 && PHYS == kLaplace, "edge recompute: 3D Laplace apply");
+      // asynchronous (LDGSTS) so the gathers below are issued right behind it
+      double* es = sm + SMEM / sizeof(double);
+      const double* esrc = edges_of(geo) + blk * (int64_t)NE * CB + lane_off;
+      if constexpr ((SCB * sizeof(double)) % 16 == 0) {
+        constexpr int CH = SCB * sizeof(double) / 16;
+        for (int i = tid; i < NE * CH; i += NTHREADS)
+          cp_async16(es + (i / CH) * SCB + (i % CH) * 2, esrc + (int64_t)(i / CH) * CB + (i % CH) * 2);
+        cp_async_commit();
+      } else {
+        for (int i = tid; i < NE * SCB; i += NTHREADS) es[i] = __ldcs(esrc + (int64_t)(i / SCB) * CB + i % SCB);
+      }
+    } else if constexpr (GEO == 1) {
       // kGeoS: copy the sub-block's geometry rows (SCB doubles of each
       // [q][k] row) into shared memory asynchronously (LDGSTS, L2 only); it
       // lands while the gathers and sweeps run and is waited for before P5
@@ -152,12 +175,12 @@ struct CellKernel {
     for (int i = 0; i < N1; ++i)
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
-    return run_values<kRes, kNeg, kGeoS>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off);
+    return run_values<kRes, kNeg, GEO>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off);
   }
 
   // the cell kernel from gathered pencil values v (zero on gi < 0) onwards;
   // callers that can issue the gather early (the coarse CG) enter here
-  template <bool kRes = false, bool kNeg = false, bool kGeoS = false, class Sync>
+  template <bool kRes = false, bool kNeg = false, int GEO = 0, class Sync>
   __device__ __forceinline__ static double run_values(const Tables& tab, const int (&gi)[N1],
                                                       double (&v)[NCOMP][N1], double* __restrict__ dst,
                                                       const double* __restrict__ geo, int64_t blk, double lam,
@@ -212,7 +235,7 @@ struct CellKernel {
         store<1>(sm, GY, pen, lsub, w);
       }
     }
-    if constexpr (kGeoS) cp_async_wait_all();
+    if constexpr (GEO == 1 || GEO == 2) cp_async_wait_all();
     sync();
     NNMG_CT(4);
     // P5: quadrature-point physics on the last-axis pencil
@@ -220,6 +243,25 @@ struct CellKernel {
       const int base = PL::base(KL, pen);
       double fl[NCOMP][N1];
       double fx[NCOMP][N1], fy[NCOMP][N1];
+      // GEO 2: the z-pencil (qx, qy) = (pen % N1, pen / N1) of the trilinear
+      // map: dx/dz is constant along it, dx/dx and dx/dy are affine in z
+      double A0[3], B0[3], A1[3], B1[3], J2[3], wxy = 0.0;
+      if constexpr (GEO == 2) {
+        const double* E = sm + SMEM / sizeof(double) + lsub;
+        auto e = [&](int b, int k, int a) { return E[((b * 4 + k) * 3 + a) * SCB]; };
+        const int qx = pen % N1, qy = pen / N1;
+        const double x = tab.xq[qx], y = tab.xq[qy];
+        wxy = tab.w[qx] * tab.w[qy];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          // edges along b, k = (lower other axis) + 2 (higher other axis)
+          J2[a] = (1.0 - y) * fma(x, e(2, 1, a) - e(2, 0, a), e(2, 0, a)) + y * fma(x, e(2, 3, a) - e(2, 2, a), e(2, 2, a));
+          A0[a] = fma(y, e(0, 1, a) - e(0, 0, a), e(0, 0, a));
+          B0[a] = fma(y, e(0, 3, a) - e(0, 2, a), e(0, 2, a)) - A0[a];
+          A1[a] = fma(x, e(1, 1, a) - e(1, 0, a), e(1, 0, a));
+          B1[a] = fma(x, e(1, 3, a) - e(1, 2, a), e(1, 2, a)) - A1[a];
+        }
+      }
 #pragma unroll
       for (int q = 0; q < N1; ++q) {
         const int pos = base + q * PL::stride(KL);
@@ -230,7 +272,34 @@ struct CellKernel {
           if constexpr (DIM == 3) g[c][1] = S(sm, GY, c, pos, lsub);
           g[c][DIM - 1] = gl[c][q];
         }
-        if constexpr (kGeoS)
+        if constexpr (GEO == 2) {
+          // J = [A0 + z B0 | A1 + z B1 | J2]; G g = (w / det) C^T (C g), C = cofactors
+          const double z = tab.xq[q];
+          double J[3][3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            J[a][0] = fma(z, B0[a], A0[a]);
+            J[a][1] = fma(z, B1[a], A1[a]);
+            J[a][2] = J2[a];
+          }
+          double C[3][3];
+          C[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+          C[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+          C[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+          C[1][0] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+          C[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+          C[1][2] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+          C[2][0] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+          C[2][1] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+          C[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+          const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+          const double sc = wxy * tab.w[q] * __drcp_rn(det);
+          double h[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) h[i] = sc * (C[i][0] * g[0][0] + C[i][1] * g[0][1] + C[i][2] * g[0][2]);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) f[0][a] = C[0][a] * h[0] + C[1][a] * h[1] + C[2][a] * h[2];
+        } else if constexpr (GEO == 1)
           qp_flux<DIM, NCOMP, PHYS, SCB, false>(sm + SMEM / sizeof(double) + pos * NG * SCB + lsub, g, f, lam, mu);
         else
           qp_flux<DIM, NCOMP, PHYS, GS, !kRes>(geo + ((blk * (int64_t)NLOC + pos) * NG) * GS + glane, g, f, lam, mu);

@@ -104,14 +104,15 @@ using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PH
 #ifndef NNMG_APPLY_MINB_GEOS
 #define NNMG_APPLY_MINB_GEOS 3
 #endif
-template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, bool GEOS = false>
+template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, int GEO = 0, int MINB = 0>
 __global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHREADS,
-                                  SPLIT == 1 ? 1 : (GEOS ? NNMG_APPLY_MINB_GEOS : NNMG_APPLY_MINB))
+                                  MINB > 0 ? MINB
+                                           : (SPLIT == 1 ? 1 : (GEO == 1 ? NNMG_APPLY_MINB_GEOS : NNMG_APPLY_MINB)))
     k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
             const double* __restrict__ geo, int64_t b0, double lam, double mu) {
   extern __shared__ double sm[];
   using CK = ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>;
-  CK::template run<false, NEG, GEOS>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm,
+  CK::template run<false, NEG, GEO>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm,
                                      threadIdx.x, [] __device__() { __syncthreads(); },
                                      int(blockIdx.x % SPLIT) * CK::SCB);
 }
@@ -288,10 +289,16 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       L->reg_kernel = !(e && std::string(e) == "pencil");
       const char* m = getenv("NNMG_REG_MINB");
       {
+        // Q3/Q4 Laplace: G recomputed from edge vectors in the pencil apply.
+        // Measured on B200 (C4, Q4): stored G 0.639 ms (split 4), recomputed
+        // 0.531 ms (split 8), 0.712 (split 4), 0.876 (split 2)
+        const char* rc = getenv("NNMG_APPLY_RECOMPUTE");
+        L->apply_recompute = rc ? atoi(rc) != 0 : (dim == 3 && degree >= 3 && physics == kLaplace);
         const char* sp = getenv("NNMG_APPLY_SPLIT");
-        // measured on B200: Q4 Laplace (C4) 0.684 -> 0.613 ms with 4, Q2
-        // elasticity (C5) 0.288 -> 0.279 ms with 2
-        L->apply_split = sp ? atoi(sp) : (dim == 3 && degree >= 4 ? 4 : (ncomp > 1 ? 2 : 1));
+        // measured on B200: stored-G Q4 Laplace (C4) 0.684 -> 0.613 ms with 4,
+        // Q2 elasticity pencil (C5) 0.288 -> 0.279 ms with 2
+        L->apply_split = sp ? atoi(sp)
+                            : (L->apply_recompute ? 8 : (dim == 3 && degree >= 4 ? 4 : (ncomp > 1 ? 2 : 1)));
         if (L->apply_split != 2 && L->apply_split != 4 && L->apply_split != 8) L->apply_split = 1;
         // Q3/Q4: geometry staged in shared memory by LDGSTS (k_apply GEOS)
         const char* gs = getenv("NNMG_APPLY_GEOS");
@@ -367,7 +374,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     NNMG_CUDA_TRY(cudaMemcpy(&hbad, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost));
     NNMG_REQUIRE(hbad == 0, kGeometryError, "mesh has non-positive Jacobians");
     // edge vectors for the hybrid-geometry register kernel (Laplace, low order)
-    if (physics == kLaplace && ncomp == 1 && L->reg_kernel && L->recompute_mod > 0 && L->nloc <= 27) {
+    if (physics == kLaplace && ncomp == 1 &&
+        ((L->reg_kernel && L->recompute_mod > 0 && L->nloc <= 27) || (dim == 3 && L->apply_recompute))) {
       const int ne = dim * (1 << (dim - 1)) * dim;
       L->edges.alloc(size_t(L->nblk) * ne * cb);
       L->edges.zero();
@@ -479,26 +487,35 @@ struct ApplyLaunch {
         return;
       }
     }
+    if constexpr (D == 3 && P >= 3 && PH == kLaplace) {
+      if (L.edges.ptr && L.apply_recompute) {
+        if (L.apply_split == 8) return launch<D, P, NC, PH, 8, 2>();
+        if (L.apply_split == 4) return launch<D, P, NC, PH, 4, 2>();
+        if (L.apply_split == 2) return launch<D, P, NC, PH, 2, 2>();
+        return launch<D, P, NC, PH, 1, 2>();
+      }
+    }
     if constexpr (D == 3 && P >= 3 && CK::CB % 16 == 0) {
       if (L.apply_geos) {
-        if (L.apply_split == 8) return launch<D, P, NC, PH, 8, true>();
-        if (L.apply_split == 4) return launch<D, P, NC, PH, 4, true>();
+        if (L.apply_split == 8) return launch<D, P, NC, PH, 8, 1>();
+        if (L.apply_split == 4) return launch<D, P, NC, PH, 4, 1>();
       }
     }
     if (L.apply_split == 4) return launch<D, P, NC, PH, 4>();
     if (L.apply_split == 2) return launch<D, P, NC, PH, 2>();
     launch<D, P, NC, PH, 1>();
   }
-  template <int D, int P, int NC, int PH, int SPLIT, bool GEOS = false>
+  template <int D, int P, int NC, int PH, int SPLIT, int GEO = 0, int MINB = 0>
   void launch() {
     using CK = ApplyKernel<D, P, NC, PH, SPLIT>;
-    constexpr size_t kSmem = CK::SMEM + (GEOS ? CK::GEO_SMEM : 0);
-    auto kern = neg ? k_apply<D, P, NC, PH, true, SPLIT, GEOS> : k_apply<D, P, NC, PH, false, SPLIT, GEOS>;
+    constexpr size_t kSmem = CK::SMEM + (GEO == 1 ? CK::GEO_SMEM : (GEO == 2 ? CK::EDGE_SMEM : 0));
+    auto kern = neg ? k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB> : k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB>;
+    const double* gsrc = GEO == 2 ? L.edges.ptr : L.geo.ptr;
     static bool attr = false;
     if (!attr) {
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true, SPLIT, GEOS>,
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false, SPLIT, GEOS>,
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
       attr = true;
     }
@@ -506,7 +523,7 @@ struct ApplyLaunch {
     constexpr int64_t kMaxGrid = (0x7fffffff / SPLIT) * SPLIT;
     for (int64_t off = 0; off < nb; off += kMaxGrid) {
       const unsigned g = static_cast<unsigned>(std::min<int64_t>(nb - off, kMaxGrid));
-      kern<<<g, CK::NTHREADS, kSmem, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0 + off / SPLIT, L.lam, L.mu);
+      kern<<<g, CK::NTHREADS, kSmem, s>>>(L.tab, src, dst, L.idx.ptr, gsrc, b0 + off / SPLIT, L.lam, L.mu);
       NNMG_CHECK_LAUNCH();
       count_launch();
     }

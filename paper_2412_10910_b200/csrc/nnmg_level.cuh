@@ -25,6 +25,7 @@ struct Level {
   bool reg_kernel = true;  // register-resident thread-per-cell apply where supported
   int apply_split = 1;     // CTAs per cell block of the pencil apply kernel (1, 2, 4, 8)
   bool apply_geos = false; // pencil apply: geometry staged in shared memory (Q3/Q4)
+  bool apply_recompute = false; // pencil apply: G recomputed from edge vectors (3D Laplace Q3/Q4)
   int reg_minb = 1;        // min CTAs/SM launch bound of that kernel (4 caps registers at 128: spills)
   int recompute_mod = 0;   // hybrid geometry: blocks with blk % mod == 0 recompute G (0 = off)
   DevBuf<double> edges;    // [nblk][d*2^(d-1)*d][cb] cell edge vectors (hybrid geometry)
