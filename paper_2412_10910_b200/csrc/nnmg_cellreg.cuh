@@ -113,7 +113,8 @@ struct CellReg {
   }
 
   // Laplace only.  Returns the thread's cell energy sum_l u_l (A_K u)_l.
-  // GEO 0: stored G;  GEO 1: G recomputed from the cell's edge vectors
+  // GEO 0: stored G;  GEO 1: G recomputed from the cell's edge vectors held in
+  // registers (naive per point);  GEO 2: recomputed, sum-factorised (3D)
   template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class Src>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
@@ -123,7 +124,7 @@ struct CellReg {
       const double* eb = edges + blk * (int64_t)NE * CB + lane;
 #pragma unroll
       for (int e = 0; e < NE; ++e) E[e] = ld_geo<kStream>(eb + e * CB);
-    } else if constexpr (kStream) {
+    } else if constexpr (kStream && GEO == 0) {
       // the warp's geometry chunk (32 cells, 85% of the bytes) streams into L2
       // while the gathers and interpolation sweeps run
       constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
@@ -148,10 +149,9 @@ struct CellReg {
     double w[NLOC];
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) w[l] = 0.0;
-    const double* g0 = geo + blk * (int64_t)NLOC * NG * CB + lane;
-#pragma unroll
-    for (int q = 0; q < NLOC; ++q) {
-      const int qx = q % N1, qy = (q / N1) % N1, qz = DIM == 3 ? q / (N1 * N1) : 0;
+    // one quadrature point: collocation gradient, flux (G g), transposed
+    // collocation derivatives accumulated at once
+    auto point = [&](int qx, int qy, int qz, auto&& flux) {
       double gx = 0.0, gy = 0.0, gz = 0.0;
 #pragma unroll
       for (int r = 0; r < N1; ++r) {
@@ -159,29 +159,99 @@ struct CellReg {
         gy = fma(tab.Dc[qy][r], v[at(qx, r, qz)], gy);
         if constexpr (DIM == 3) gz = fma(tab.Dc[qz][r], v[at(qx, qy, r)], gz);
       }
-      double gg[NG];
-      if constexpr (GEO == 1) {
-        recompute_g(tab, E, qx, qy, qz, gg);
-      } else {
-        const double* G = g0 + q * NG * CB;
-#pragma unroll
-        for (int k = 0; k < NG; ++k) gg[k] = ld_geo<kStream>(G + k * CB);
-      }
       double fx, fy, fz = 0.0;
-      if constexpr (DIM == 3) {
-        fx = gg[0] * gx + gg[1] * gy + gg[2] * gz;
-        fy = gg[1] * gx + gg[3] * gy + gg[4] * gz;
-        fz = gg[2] * gx + gg[4] * gy + gg[5] * gz;
-      } else {
-        fx = gg[0] * gx + gg[1] * gy;
-        fy = gg[1] * gx + gg[2] * gy;
-      }
-      // transposed collocation derivatives, accumulated at once
+      flux(gx, gy, gz, fx, fy, fz);
 #pragma unroll
       for (int r = 0; r < N1; ++r) {
         w[at(r, qy, qz)] = fma(tab.Dc[qx][r], fx, w[at(r, qy, qz)]);
         w[at(qx, r, qz)] = fma(tab.Dc[qy][r], fy, w[at(qx, r, qz)]);
         if constexpr (DIM == 3) w[at(qx, qy, r)] = fma(tab.Dc[qz][r], fz, w[at(qx, qy, r)]);
+      }
+    };
+    if constexpr (GEO == 2) {
+      // 3D: G from the cell's edge vectors, sum-factorised along z-pencils of
+      // the trilinear map (dx/dz constant along a pencil, dx/dx and dx/dy
+      // affine in z); edges read through L1 (coalesced across the warp)
+      static_assert(DIM == 3, "GEO 2 is 3D");
+      const double* eb = edges + blk * (int64_t)NE * CB + lane;
+      auto e = [&](int b, int k, int a) { return __ldg(eb + ((b * 4 + k) * 3 + a) * CB); };
+#pragma unroll
+      for (int qy = 0; qy < N1; ++qy) {
+        const double y = tab.xq[qy];
+        double A0[3], B0[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          A0[a] = fma(y, e(0, 1, a) - e(0, 0, a), e(0, 0, a));
+          B0[a] = fma(y, e(0, 3, a) - e(0, 2, a), e(0, 2, a)) - A0[a];
+        }
+#pragma unroll
+        for (int qx = 0; qx < N1; ++qx) {
+          const double x = tab.xq[qx];
+          const double wxy = tab.w[qx] * tab.w[qy];
+          double A1[3], B1[3], J2[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            A1[a] = fma(x, e(1, 1, a) - e(1, 0, a), e(1, 0, a));
+            B1[a] = fma(x, e(1, 3, a) - e(1, 2, a), e(1, 2, a)) - A1[a];
+            J2[a] = (1.0 - y) * fma(x, e(2, 1, a) - e(2, 0, a), e(2, 0, a)) +
+                    y * fma(x, e(2, 3, a) - e(2, 2, a), e(2, 2, a));
+          }
+#pragma unroll
+          for (int qz = 0; qz < N1; ++qz) {
+            point(qx, qy, qz, [&](double gx, double gy, double gz, double& fx, double& fy, double& fz) {
+              const double z = tab.xq[qz];
+              double J[3][3];
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                J[a][0] = fma(z, B0[a], A0[a]);
+                J[a][1] = fma(z, B1[a], A1[a]);
+                J[a][2] = J2[a];
+              }
+              double C[3][3];
+              C[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+              C[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+              C[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+              C[1][0] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+              C[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+              C[1][2] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+              C[2][0] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+              C[2][1] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+              C[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+              const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+              const double sc = wxy * tab.w[qz] * __drcp_rn(det);
+              const double h0 = sc * (C[0][0] * gx + C[0][1] * gy + C[0][2] * gz);
+              const double h1 = sc * (C[1][0] * gx + C[1][1] * gy + C[1][2] * gz);
+              const double h2 = sc * (C[2][0] * gx + C[2][1] * gy + C[2][2] * gz);
+              fx = C[0][0] * h0 + C[1][0] * h1 + C[2][0] * h2;
+              fy = C[0][1] * h0 + C[1][1] * h1 + C[2][1] * h2;
+              fz = C[0][2] * h0 + C[1][2] * h1 + C[2][2] * h2;
+            });
+          }
+        }
+      }
+    } else {
+      const double* g0 = geo + blk * (int64_t)NLOC * NG * CB + lane;
+#pragma unroll
+      for (int q = 0; q < NLOC; ++q) {
+        const int qx = q % N1, qy = (q / N1) % N1, qz = DIM == 3 ? q / (N1 * N1) : 0;
+        point(qx, qy, qz, [&](double gx, double gy, double gz, double& fx, double& fy, double& fz) {
+          double gg[NG];
+          if constexpr (GEO == 1) {
+            recompute_g(tab, E, qx, qy, qz, gg);
+          } else {
+            const double* G = g0 + q * NG * CB;
+#pragma unroll
+            for (int k = 0; k < NG; ++k) gg[k] = ld_geo<kStream>(G + k * CB);
+          }
+          if constexpr (DIM == 3) {
+            fx = gg[0] * gx + gg[1] * gy + gg[2] * gz;
+            fy = gg[1] * gx + gg[3] * gy + gg[4] * gz;
+            fz = gg[2] * gx + gg[4] * gy + gg[5] * gz;
+          } else {
+            fx = gg[0] * gx + gg[1] * gy;
+            fy = gg[1] * gx + gg[2] * gy;
+          }
+        });
       }
     }
     // back to the nodal basis: S^T sweeps

@@ -308,6 +308,10 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       L->reg_minb = m ? atoi(m) : 1;
       const char* rm = getenv("NNMG_RECOMPUTE_MOD");
       L->recompute_mod = rm ? atoi(rm) : 0;
+      const char* rn = getenv("NNMG_RECOMPUTE_NUM");
+      L->recompute_num = rn ? atoi(rn) : 1;
+      const char* rr = getenv("NNMG_REG_RECOMPUTE");
+      L->reg_recompute = rr ? atoi(rr) != 0 : false;
     }
     // constraints: the kernels support whole-node constraints (every component
     // of a scalar DoF), which is what dirichlet_constraints produces
@@ -375,7 +379,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     NNMG_REQUIRE(hbad == 0, kGeometryError, "mesh has non-positive Jacobians");
     // edge vectors for the hybrid-geometry register kernel (Laplace, low order)
     if (physics == kLaplace && ncomp == 1 &&
-        ((L->reg_kernel && L->recompute_mod > 0 && L->nloc <= 27) || (dim == 3 && L->apply_recompute))) {
+        ((L->reg_kernel && (L->recompute_mod > 0 || (L->reg_recompute && dim == 3)) && L->nloc <= 27) ||
+         (dim == 3 && L->apply_recompute))) {
       const int ne = dim * (1 << (dim - 1)) * dim;
       L->edges.alloc(size_t(L->nblk) * ne * cb);
       L->edges.zero();
@@ -400,22 +405,38 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
 // edge vectors (288 B/cell instead of 1296 B/cell of stored G), the others
 // stream the stored G; warp-uniform branch, both kinds share every SM so the
 // FP64 pipe and HBM work concurrently.  rmod == 0: stored G only.
-// Measured on B200 (C3): stored-G only 0.620 ms; recompute-only 0.700 ms;
-// in-kernel hybrids 0.67-0.72 ms (both paths in one kernel spill).  HYB is an
-// opt-in instantiation (NNMG_RECOMPUTE_MOD) so the default kernel stays lean.
+// Measured on B200 (C3): stored-G only 0.620 ms; naive recompute-only 0.700
+// ms, in-kernel hybrids 0.67-0.72 ms (both paths in one kernel spill);
+// sum-factorised recompute (GEO 2, 3D, k_apply_reg_rc) 0.633 ms; GEO-2
+// hybrids 0.67-0.74 ms (1/4 .. 3/4 of the blocks recomputing).  Blocks with
+// blk % rmod < rnum take the recompute path.  HYB is an opt-in instantiation
+// (NNMG_RECOMPUTE_MOD / NNMG_RECOMPUTE_NUM) so the default kernel stays lean.
 template <int D, int P, int MINB, bool NEG, bool HYB>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const double* __restrict__ src, double* __restrict__ dst,
                                                    const int* __restrict__ idx, const double* __restrict__ geo,
-                                                   int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod) {
+                                                   int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod,
+                                                   int rnum) {
   const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= b1) return;
   if constexpr (HYB) {
-    if (blk % rmod == 0) {
-      CellReg<D, P>::template run<true, false, NEG, 1>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31, edges);
+    if (blk % rmod < rnum) {
+      CellReg<D, P>::template run<true, false, NEG, D == 3 ? 2 : 1>(tab, PlainSrc{src}, dst, idx, geo, blk,
+                                                                    threadIdx.x & 31, edges);
       return;
     }
   }
   CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
+}
+
+// all blocks recompute G from edge vectors, sum-factorised along z-pencils (3D)
+template <int D, int P, bool NEG>
+__global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const double* __restrict__ src,
+                                                        double* __restrict__ dst, const int* __restrict__ idx,
+                                                        int64_t b0, int64_t b1, const double* __restrict__ edges) {
+  const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (blk >= b1) return;
+  CellReg<D, P>::template run<true, false, NEG, 2>(tab, PlainSrc{src}, dst, idx, nullptr, blk, threadIdx.x & 31,
+                                                   edges);
 }
 
 // 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
@@ -465,13 +486,22 @@ struct ApplyLaunch {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
+        if constexpr (D == 3) {
+          if (L.edges.ptr && L.reg_recompute) {
+            auto kr = neg ? k_apply_reg_rc<D, P, true> : k_apply_reg_rc<D, P, false>;
+            kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, b0, b1, L.edges.ptr);
+            NNMG_CHECK_LAUNCH();
+            count_launch();
+            return;
+          }
+        }
         const bool hyb = L.edges.ptr && L.recompute_mod > 0;
         auto kr = hyb ? (neg ? k_apply_reg<D, P, 1, true, true> : k_apply_reg<D, P, 1, false, true>)
                       : (neg ? (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, true, false> : k_apply_reg<D, P, 1, true, false>)
                              : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false, false>
                                                 : k_apply_reg<D, P, 1, false, false>));
         kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
-                                            hyb ? L.recompute_mod : 0);
+                                            hyb ? L.recompute_mod : 0, L.recompute_num);
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;

@@ -26,8 +26,10 @@ struct Level {
   int apply_split = 1;     // CTAs per cell block of the pencil apply kernel (1, 2, 4, 8)
   bool apply_geos = false; // pencil apply: geometry staged in shared memory (Q3/Q4)
   bool apply_recompute = false; // pencil apply: G recomputed from edge vectors (3D Laplace Q3/Q4)
+  bool reg_recompute = false;   // register apply: G recomputed from edge vectors (3D Laplace Q1/Q2)
   int reg_minb = 1;        // min CTAs/SM launch bound of that kernel (4 caps registers at 128: spills)
-  int recompute_mod = 0;   // hybrid geometry: blocks with blk % mod == 0 recompute G (0 = off)
+  int recompute_mod = 0;   // hybrid geometry: blocks with blk % mod < num recompute G (0 = off)
+  int recompute_num = 1;
   DevBuf<double> edges;    // [nblk][d*2^(d-1)*d][cb] cell edge vectors (hybrid geometry)
   std::vector<int> cell_dofs_host;  // plain (nc, nloc) copy for transfer setup
   std::vector<uint8_t> scalar_constrained;  // per scalar DoF
