@@ -27,8 +27,10 @@ struct TransferDispatch {
     const Level& C = *T.coarse;
     const unsigned g = grid_for(T.ncc, kWarps);
     if (mode < 2) {
-      k_prolongate<D, P, NC, CBC><<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.cell_start.ptr,
-                                                             T.pt_dof.ptr, T.xhat.ptr, T.ncc);
+      constexpr int PPL = prolongate_ppl<D, P, NC>();
+      auto kp = (T.prolong_ppl == 2 && PPL == 1) ? k_prolongate<D, P, NC, CBC, 2> : k_prolongate<D, P, NC, CBC, PPL>;
+      kp<<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
+                                   T.ncc);
       NNMG_CHECK_LAUNCH();
       count_launch();
     } else {
@@ -122,6 +124,8 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
       if (e) ch = std::max(1, std::min(31, atoi(e)));
       T->chunk = ch;
       // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups
+      const char* pp = getenv("NNMG_PROLONG_PPL");
+      T->prolong_ppl = pp ? atoi(pp) : 1;
       const char* k = getenv("NNMG_RESTRICT_KERNEL");
       T->restrict_kernel = k ? atoi(k) : 1;
     }

@@ -14,6 +14,7 @@ struct Transfer {
   int64_t npts = 0, ncc = 0;
   int chunk = 1;            // coarse cells per warp in the restriction
   int restrict_kernel = 1;  // variant for NLOC*NCOMP <= 32 (see transfer_create)
+  int prolong_ppl = 1;      // 2: two points per lane also where one is the default
   DevBuf<int> cell_start;   // [ncc+1] CSR of points by owning coarse cell
   DevBuf<int> pt_dof;       // [npts] fine scalar DoF (sorted by cell, then point order)
   DevBuf<double> xhat;      // [npts][dim]

@@ -113,8 +113,16 @@ __device__ __forceinline__ double contract(const double* __restrict__ U, const d
   }
 }
 
-template <int DIM, int PC, int NCOMP, int CBC>
-__global__ void __launch_bounds__(kTransferWarps * 32, 6)
+// points per lane per round: two (each staged coarse value read from shared
+// memory serves both) for scalar fields; measured on B200: C3 0.251 -> 0.195
+// ms, C4 (Q4) 0.365 -> 0.314 ms; the 3-component variant spills
+template <int DIM, int PC, int NCOMP>
+__host__ __device__ constexpr int prolongate_ppl() {
+  return NCOMP == 1 ? 2 : 1;
+}
+
+template <int DIM, int PC, int NCOMP, int CBC, int PPL>
+__global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && PC >= 3 ? 4 : 6)
     k_prolongate(Tables tab, const double* __restrict__ uc, double* __restrict__ uf, int accumulate,
                  const int* __restrict__ cidx, const int* __restrict__ cell_start, const int* __restrict__ pt_dof,
                  const double* __restrict__ xhat, int64_t ncc) {
@@ -126,8 +134,6 @@ __global__ void __launch_bounds__(kTransferWarps * 32, 6)
   if (cell >= ncc) return;
   const int64_t blk = cell / CBC, cl = cell % CBC;
   const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
-  // measured: two independent points per lane per round beat one (C3)
-  constexpr int PPL = ((DIM == 2 || N1 <= 3) && NCOMP == 1) ? 2 : 1;
   constexpr int STEP = 32 * PPL;
   // first round's records are in flight while the coarse values are staged
   int dd[PPL];
