@@ -382,9 +382,15 @@ struct StagedRestrict {
   static constexpr int P = SLOTS * SUB;  // points per round
   static constexpr int INNER = NLOC / N1;
   static constexpr int PLANE = INNER * NCOMP;
-  static constexpr int REC0 = DIM * N1 + NCOMP;
-  static constexpr int REC = REC0 | 1;  // odd stride in doubles: distinct banks across slots
-  static constexpr int WARP_DOUBLES = 2 * P * REC + SLOTS * G * PLANE;
+  // staged record of a point: X0 at 0, X1 at A (16-byte aligned pairs, read
+  // as double2), X_last at OZ, values at OV; stride REC = 2 mod 16 doubles so
+  // the slots' 16-byte reads fall in distinct bank quads
+  static constexpr int A = (N1 + 1) & ~1;
+  static constexpr int OZ = DIM == 3 ? A + N1 : A;
+  static constexpr int OV = OZ + N1;
+  static constexpr int REC0 = OV + NCOMP;
+  static constexpr int REC = ((REC0 - 2 + 15) / 16) * 16 + 2;
+  static constexpr int WARP_DOUBLES = (2 * P * REC + SLOTS * G * PLANE + 1) & ~1;  // keeps 16-byte alignment
   static constexpr int WARPS = (48 * 1024) / (WARP_DOUBLES * 8) >= kTransferWarps
                                    ? kTransferWarps
                                    : ((48 * 1024) / (WARP_DOUBLES * 8) >= 1 ? (48 * 1024) / (WARP_DOUBLES * 8) : 1);
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
   using K = StagedRestrict<DIM, PC, NCOMP>;
   constexpr int N1 = K::N1, G = K::G, SLOTS = K::SLOTS, SUB = K::SUB, P = K::P, INNER = K::INNER,
                 PLANE = K::PLANE, REC = K::REC, NOUT = K::NOUT;
-  __shared__ double smem[K::WARPS][K::WARP_DOUBLES];
+  __shared__ __align__(16) double smem[K::WARPS][K::WARP_DOUBLES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = (blockIdx.x * (int64_t)K::WARPS + warp) * chunk;
   if (c0 >= ncc) return;
@@ -426,27 +432,35 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
           for (int j = 0; j < DIM; ++j) {
             lagrange_pp<N1>(tab, xs[0][j], X);
 #pragma unroll
-            for (int i = 0; i < N1; ++i) st[lane * REC + j * N1 + i] = X[i];
+            for (int i = 0; i < N1; ++i) st[lane * REC + (j == 0 ? 0 : (j == DIM - 1 ? K::OZ : K::A)) + i] = X[i];
           }
 #pragma unroll
-          for (int c = 0; c < NCOMP; ++c) st[lane * REC + DIM * N1 + c] = vs[0][c];
+          for (int c = 0; c < NCOMP; ++c) st[lane * REC + K::OV + c] = vs[0][c];
         }
         __syncwarp();
         if (grp) {
 #pragma unroll 1
           for (int s = 0; s < SUB; ++s) {
             const double* q = st + (s * SLOTS + slot) * REC;
-            double X0[N1], X1[DIM == 3 ? N1 : 1];
+            double X0[K::A], X1[DIM == 3 ? K::A : 1];
 #pragma unroll
-            for (int i = 0; i < N1; ++i) X0[i] = q[i];
+            for (int i = 0; i < K::A; i += 2) {
+              const double2 t = *reinterpret_cast<const double2*>(q + i);
+              X0[i] = t.x;
+              X0[i + 1] = t.y;
+            }
             if constexpr (DIM == 3) {
 #pragma unroll
-              for (int i = 0; i < N1; ++i) X1[i] = q[N1 + i];
+              for (int i = 0; i < K::A; i += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(q + K::A + i);
+                X1[i] = t.x;
+                X1[i + 1] = t.y;
+              }
             }
-            const double z = q[(DIM - 1) * N1 + g];
+            const double z = q[K::OZ + g];
 #pragma unroll
             for (int c = 0; c < NCOMP; ++c) {
-              const double a = q[DIM * N1 + c] * z;
+              const double a = q[K::OV + c] * z;
               if constexpr (DIM == 3) {
 #pragma unroll
                 for (int i1 = 0; i1 < N1; ++i1) {
