@@ -623,6 +623,7 @@ struct CgLaunch {
               try_split<D, P, NC, PH, 2>(L, nsm, max_split) || try_balanced<D, P, NC, PH>(L, nsm);
         }
       }
+      if (C.nrank > 256) C.single_barrier = false;  // k_coarse_cg1 reduces <= 8 partials per lane
       if (C.single_barrier && C.mode != 2) {
         C.con.alloc(size_t(L.n_dofs));
         C.con.zero();
@@ -671,6 +672,10 @@ struct CgLaunch {
       g.w[2] = C.ap.ptr + 2 * L.n_dofs;
       g.p = C.p.ptr;
       g.part = C.part.ptr;
+      {
+        const char* e = getenv("NNMG_COARSE_ATOMIC_DOTS");
+        g.atomic_dots = e ? atoi(e) : 1;
+      }
       g.reduction = C.reduction;
       g.max_iter = C.max_iter;
       g.status = C.status.ptr;

@@ -42,6 +42,7 @@ struct Cg1Args {
   double* w[3];
   double* p;
   double* part;  // [3][grid]
+  int atomic_dots;  // 1: (gamma, delta, rr) accumulated by fp64 atomics into 3 rotating banks
   double reduction;
   int max_iter;
   int prefetch_owned;  // load the owners' operands before the cell phase
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     a.p[i] = 0.0;
     a.x[i] = 0.0;
   }
+  if (a.atomic_dots && rank == 0 && tid < 12) a.part[tid] = 0.0;
   grid.sync();
   // owners' operands (final since the last barrier) are loaded right after
   // each barrier, ahead of the global reduction and the cell phase, when the
@@ -206,10 +208,16 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
           gr[c][i] = __ldcg(r + j);
           gw[c][i] = __ldcg(w + j);
           gs[c][i] = __ldcg(s + j);
-          gd[c][i] = __ldg(a.inv_diag + j);
         }
   };
-  if constexpr (RES) gather(0);
+  if constexpr (RES) {
+    // D^-1 at the pencil's DoFs never changes: loaded once, not per phase
+#pragma unroll
+    for (int i = 0; i < N1; ++i)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) gd[c][i] = gi[i] >= 0 ? __ldg(a.inv_diag + (int64_t)gi[i] * NC + c) : 0.0;
+    gather(0);
+  }
   if (fits) load_owned(0, i0 + tid);
   double alpha = 0.0, beta = 0.0, gamma_old = 1.0, alpha_old = 1.0, target = 0.0;
   int status_it = a.max_iter, status_conv = 0, status_err = 0;
@@ -291,21 +299,39 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
         se += red[32 + i];
         sr += red[64 + i];
       }
-      double* part = a.part + (k & 1) * 3 * nrank;  // alternate banks across phases
-      part[rank] = sg;
-      part[nrank + rank] = se;
-      part[2 * nrank + rank] = sr;
+      if (a.atomic_dots) {
+        // every CTA reading all per-CTA partials after the barrier is a
+        // same-line hot spot in L2 (~1.2 us per iteration on 136 CTAs); one
+        // fp64 RED per quantity into a rotating bank makes the read a single
+        // sector.  Summation order (rounding only) varies run to run.
+        double* bank = a.part + (k % 3) * 4;
+        atomicAdd(bank + 0, sg);
+        atomicAdd(bank + 1, se);
+        atomicAdd(bank + 2, sr);
+      } else {
+        double* part = a.part + (k & 1) * 3 * nrank;  // alternate banks across phases
+        part[rank] = sg;
+        part[nrank + rank] = se;
+        part[2 * nrank + rank] = sr;
+      }
     }
     if (trace && k < 63) trace[k * 8 + 1] = cg1_timer();
     // per-CTA arrival times of iterations 8..15 (NNMG_COARSE_TRACE)
     if (a.trace && tid == 0 && k >= 8 && k < 16) a.trace[8 * 64 + (k - 8) * nrank + rank] = cg1_gtimer();
     grid.sync();
     if (trace && k < 63) trace[k * 8 + 2] = cg1_timer();
+    // the reduced scalars are the critical path: their load goes out ahead of
+    // the next phase's gather / owner prefetches (which queue many sectors)
+    const double totv = (a.atomic_dots && tid < 3) ? __ldcg(a.part + (k % 3) * 4 + tid) : 0.0;
     if constexpr (RES) gather(k + 1);
     if (fits) load_owned(k + 1, i0 + tid);
     // every CTA reduces the per-CTA partials in the same fixed order
     __shared__ double tot[3];
-    if (tid < 32) {
+    if (a.atomic_dots) {
+      if (tid < 3) tot[tid] = totv;
+      if (rank == 0 && tid == nth - 1)  // bank of phase k+2 (last read before barrier k)
+        for (int j = 0; j < 3; ++j) a.part[((k + 2) % 3) * 4 + j] = 0.0;
+    } else if (tid < 32) {
       const double* part = a.part + (k & 1) * 3 * nrank;
       double sg = 0.0, se = 0.0, sr = 0.0;
       for (int i = tid; i < nrank; i += 32) {
