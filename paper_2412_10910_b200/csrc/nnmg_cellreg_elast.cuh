@@ -66,15 +66,28 @@ struct CellRegElast {
     }
   }
 
-  // one cell block; threads: w = threadIdx.x / 32 (component), lane = cell
-  template <bool kNeg>
+  // one cell block; threads: w = threadIdx.x / 32 (component), lane = cell.
+  // GEO 0: J^-1 and |det J| w streamed from HBM.  GEO 2 (Q2): J recomputed
+  // from the cell's 12 edge vectors (`geo` is then the edge table
+  // [blk][36][CB]): 288 B per cell instead of 2,160 B.  In phase B thread w
+  // evaluates the points (qx, qy) = (w, k) of each z-slice, so on the
+  // trilinear map dx/dz is affine in qy, dx/dy constant per slice and dx/dx
+  // affine in qy per slice; with cofactors C: J^-1 = C^T / det,
+  // pg = g C^T / det and flux = w_q sigma C.
+  template <bool kNeg, int GEO = 0>
   __device__ __forceinline__ static void run(const Tables& tab, const double* __restrict__ src, double* __restrict__ dst,
                                              const int* __restrict__ idx, const double* __restrict__ geo, int64_t blk,
                                              double lam, double mu, double* sm) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    static_assert(GEO == 0 || N1 == 3, "edge recompute relies on qx == component in phase B");
+    constexpr int NE = 36;
     if (w == 0 && lane == 0) {
-      constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
-      prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+      if constexpr (GEO == 0) {
+        constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
+        prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+      } else {
+        prefetch_l2_bulk(geo + blk * (int64_t)NE * CB, unsigned(NE) * CB * sizeof(double));
+      }
     }
     double* gbuf = sm;                     // [SLICE][3 comps][3 dirs][CB]
     double* fbuf = sm + SLICE * 9 * CB;    // same layout, reference flux
@@ -92,8 +105,36 @@ struct CellRegElast {
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) acc[l] = 0.0;
     const double* gb = geo + blk * (int64_t)NLOC * NG * CB + lane;
+    const double* eb = geo + blk * (int64_t)NE * CB + lane;
+    auto e = [&](int b, int k, int a) { return __ldg(eb + ((b * 4 + k) * 3 + a) * CB); };
+    // GEO 2: dx/dz at (qx = w, y) = A2 + y B2 (edges along z, k = x + 2y)
+    double A2[3], B2[3];
+    if constexpr (GEO == 2) {
+      const double x = tab.xq[w];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        A2[a] = fma(x, e(2, 1, a) - e(2, 0, a), e(2, 0, a));
+        B2[a] = fma(x, e(2, 3, a) - e(2, 2, a), e(2, 2, a)) - A2[a];
+      }
+    }
 #pragma unroll
     for (int qz = 0; qz < N1; ++qz) {
+      // GEO 2: per slice dx/dy at (x = w, z) and dx/dx = A0 + y B0 at z
+      double J1[3], A0[3], B0[3];
+      if constexpr (GEO == 2) {
+        const double x = tab.xq[w], z = tab.xq[qz];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          // edges along y: k = x + 2z;  along x: k = y + 2z
+          const double lo1 = fma(x, e(1, 1, a) - e(1, 0, a), e(1, 0, a));
+          const double hi1 = fma(x, e(1, 3, a) - e(1, 2, a), e(1, 2, a));
+          J1[a] = fma(z, hi1 - lo1, lo1);
+          const double y0 = fma(z, e(0, 2, a) - e(0, 0, a), e(0, 0, a));  // y = 0
+          const double y1 = fma(z, e(0, 3, a) - e(0, 1, a), e(0, 1, a));  // y = 1
+          A0[a] = y0;
+          B0[a] = y1 - y0;
+        }
+      }
       // A: d u_w / d xhat_j at the slice's points (collocation)
 #pragma unroll
       for (int s = 0; s < SLICE; ++s) {
@@ -116,18 +157,47 @@ struct CellRegElast {
       for (int k = 0; k < PER; ++k) {
         const int s = w + 3 * k;
         if (s < SLICE) {
-          const double* G = gb + (qz * SLICE + s) * NG * CB;
-          double K[3][3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) K[a][b] = __ldcs(G + (a * 3 + b) * CB);
-          const double dv = __ldcs(G + 9 * CB);
           double g[3][3];
 #pragma unroll
           for (int c = 0; c < 3; ++c)
 #pragma unroll
             for (int j = 0; j < 3; ++j) g[c][j] = gbuf[((s * 3 + c) * 3 + j) * CB + lane];
+          double K[3][3], dv;
+          if constexpr (GEO == 2) {
+            // J at (qx, qy, qz) = (w, k, qz); K = J^-1 = C^T / det, dv = det w_q
+            const double y = tab.xq[k];
+            double J[3][3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              J[a][0] = fma(y, B0[a], A0[a]);
+              J[a][1] = J1[a];
+              J[a][2] = fma(y, B2[a], A2[a]);
+            }
+            double C[3][3];
+            C[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+            C[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+            C[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+            C[1][0] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+            C[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+            C[1][2] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+            C[2][0] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+            C[2][1] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+            C[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+            const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+            const double rdet = __drcp_rn(det);
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) K[a][b] = C[b][a] * rdet;
+            dv = det * (tab.w[w] * tab.w[k] * tab.w[qz]);
+          } else {
+            const double* G = gb + (qz * SLICE + s) * NG * CB;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) K[a][b] = __ldcs(G + (a * 3 + b) * CB);
+            dv = __ldcs(G + 9 * CB);
+          }
           // pg = ghat J^-1, eps = sym(pg), sigma = 2 mu eps + lam tr(eps) I, flux = sigma J^-T dv
           double pg[3][3];
 #pragma unroll

@@ -310,6 +310,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       L->recompute_mod = rm ? atoi(rm) : 0;
       const char* rn = getenv("NNMG_RECOMPUTE_NUM");
       L->recompute_num = rn ? atoi(rn) : 1;
+      const char* er = getenv("NNMG_ELAST_RECOMPUTE");
+      L->elast_recompute = er ? atoi(er) != 0 : false;
       const char* rr = getenv("NNMG_REG_RECOMPUTE");
       L->reg_recompute = rr ? atoi(rr) != 0 : false;
     }
@@ -378,9 +380,10 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
     NNMG_CUDA_TRY(cudaMemcpy(&hbad, bad.ptr, sizeof(int), cudaMemcpyDeviceToHost));
     NNMG_REQUIRE(hbad == 0, kGeometryError, "mesh has non-positive Jacobians");
     // edge vectors for the hybrid-geometry register kernel (Laplace, low order)
-    if (physics == kLaplace && ncomp == 1 &&
-        ((L->reg_kernel && (L->recompute_mod > 0 || (L->reg_recompute && dim == 3)) && L->nloc <= 27) ||
-         (dim == 3 && L->apply_recompute))) {
+    if ((physics == kLaplace && ncomp == 1 &&
+         ((L->reg_kernel && (L->recompute_mod > 0 || (L->reg_recompute && dim == 3)) && L->nloc <= 27) ||
+          (dim == 3 && L->apply_recompute))) ||
+        (physics == kElasticity && dim == 3 && degree == 2 && L->reg_kernel && L->elast_recompute)) {
       const int ne = dim * (1 << (dim - 1)) * dim;
       L->edges.alloc(size_t(L->nblk) * ne * cb);
       L->edges.zero();
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const doubl
 }
 
 // 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
-template <int P, bool NEG>
+template <int P, bool NEG, int GEO = 0>
 __global__ void __launch_bounds__(96) k_apply_reg_elast(Tables tab, const double* __restrict__ src,
                                                         double* __restrict__ dst, const int* __restrict__ idx,
                                                         const double* __restrict__ geo, int64_t b0, int64_t b1,
@@ -448,7 +451,7 @@ __global__ void __launch_bounds__(96) k_apply_reg_elast(Tables tab, const double
   __shared__ double sm[CellRegElast<P>::SMEM_DOUBLES];
   const int64_t blk = b0 + blockIdx.x;
   if (blk >= b1) return;
-  CellRegElast<P>::template run<NEG>(tab, src, dst, idx, geo, blk, lam, mu, sm);
+  CellRegElast<P>::template run<NEG, GEO>(tab, src, dst, idx, geo, blk, lam, mu, sm);
 }
 
 // per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
@@ -510,6 +513,16 @@ struct ApplyLaunch {
     if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported) {
       if (L.reg_kernel) {
         const int64_t nb = b1 - b0;
+        if constexpr (P == 2) {
+          if (L.edges.ptr && L.elast_recompute) {
+            auto kr = neg ? k_apply_reg_elast<P, true, 2> : k_apply_reg_elast<P, false, 2>;
+            kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.edges.ptr, b0, b1, L.lam,
+                                                         L.mu);
+            NNMG_CHECK_LAUNCH();
+            count_launch();
+            return;
+          }
+        }
         auto kr = neg ? k_apply_reg_elast<P, true> : k_apply_reg_elast<P, false>;
         kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.lam, L.mu);
         NNMG_CHECK_LAUNCH();

@@ -47,6 +47,9 @@ APPLY_VARIANTS = [
     ("op_3d_el_q2", {"NNMG_APPLY_KERNEL": "pencil"}),
     ("op_3d_el_q2", {"NNMG_APPLY_KERNEL": "pencil", "NNMG_APPLY_SPLIT": "2"}),
     ("op_3d_el_q1", {"NNMG_APPLY_KERNEL": "pencil"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_RECOMPUTE": "1"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_RECOMPUTE": "0"}),
+    ("op_ref_cube3d_el", {"NNMG_ELAST_RECOMPUTE": "1"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_SPLIT": "1"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "1", "NNMG_APPLY_SPLIT": "4"}),
