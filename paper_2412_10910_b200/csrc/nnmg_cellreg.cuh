@@ -115,10 +115,37 @@ struct CellReg {
   // Laplace only.  Returns the thread's cell energy sum_l u_l (A_K u)_l.
   // GEO 0: stored G;  GEO 1: G recomputed from the cell's edge vectors held in
   // registers (naive per point);  GEO 2: recomputed, sum-factorised (3D)
+  // GEO 3 (3D): stored G streamed through shared memory by TMA bulk copies,
+  // one z-slice (N1^2 points x NG x CB doubles) per copy, two slots per warp
+  // with an mbarrier each: the G loads of the point loop become shared-memory
+  // reads whose data were in flight since the gather.  `wsm` = this warp's
+  // WARP_SMEM bytes.
+  static constexpr int SLICE_Q = DIM == 3 ? N1 * N1 : NLOC;
+  static constexpr unsigned SLICE_BYTES = unsigned(SLICE_Q) * NG * CB * sizeof(double);
+  static constexpr size_t WARP_SMEM = 2 * size_t(SLICE_BYTES) + 16;
+
   template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class Src>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
-                                               int64_t blk, int lane, const double* __restrict__ edges = nullptr) {
+                                               int64_t blk, int lane, const double* __restrict__ edges = nullptr,
+                                               double* wsm = nullptr) {
+    double* gbuf = wsm;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wsm + 2 * SLICE_Q * NG * CB);
+    const double* gchunk = geo + blk * (int64_t)NLOC * NG * CB;
+    if constexpr (GEO == 3) {
+      static_assert(DIM == 3, "slice staging is 3D");
+      if (lane == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_proxy_async();
+#pragma unroll
+        for (int s = 0; s < 2 && s < N1; ++s) {
+          mbar_expect_tx(&mbar[s], SLICE_BYTES);
+          tma_load_1d(gbuf + s * SLICE_Q * NG * CB, gchunk + s * SLICE_Q * NG * CB, SLICE_BYTES, &mbar[s]);
+        }
+      }
+      __syncwarp();
+    }
     double E[GEO == 1 ? NE : 1];
     if constexpr (GEO == 1) {
       const double* eb = edges + blk * (int64_t)NE * CB + lane;
@@ -234,10 +261,20 @@ struct CellReg {
 #pragma unroll
       for (int q = 0; q < NLOC; ++q) {
         const int qx = q % N1, qy = (q / N1) % N1, qz = DIM == 3 ? q / (N1 * N1) : 0;
+        if constexpr (GEO == 3) {
+          if (q % SLICE_Q == 0) {
+            // slice qz lands in slot qz & 1, completion phase qz >> 1
+            mbar_wait(&mbar[qz & 1], (qz >> 1) & 1);
+          }
+        }
         point(qx, qy, qz, [&](double gx, double gy, double gz, double& fx, double& fy, double& fz) {
           double gg[NG];
           if constexpr (GEO == 1) {
             recompute_g(tab, E, qx, qy, qz, gg);
+          } else if constexpr (GEO == 3) {
+            const double* G = gbuf + ((qz & 1) * SLICE_Q + q % SLICE_Q) * NG * CB + lane;
+#pragma unroll
+            for (int k = 0; k < NG; ++k) gg[k] = G[k * CB];
           } else {
             const double* G = g0 + q * NG * CB;
 #pragma unroll
@@ -252,6 +289,18 @@ struct CellReg {
             fy = gg[1] * gx + gg[2] * gy;
           }
         });
+        if constexpr (GEO == 3) {
+          if (q % SLICE_Q == SLICE_Q - 1 && qz + 2 < N1) {
+            // every lane has read slot qz & 1: refill it with slice qz + 2
+            __syncwarp();
+            if (lane == 0) {
+              fence_proxy_async();
+              mbar_expect_tx(&mbar[qz & 1], SLICE_BYTES);
+              tma_load_1d(gbuf + (qz & 1) * SLICE_Q * NG * CB, gchunk + (qz + 2) * SLICE_Q * NG * CB, SLICE_BYTES,
+                          &mbar[qz & 1]);
+            }
+          }
+        }
       }
     }
     // back to the nodal basis: S^T sweeps

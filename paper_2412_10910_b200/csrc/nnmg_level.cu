@@ -310,6 +310,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       L->recompute_mod = rm ? atoi(rm) : 0;
       const char* rn = getenv("NNMG_RECOMPUTE_NUM");
       L->recompute_num = rn ? atoi(rn) : 1;
+      const char* rt = getenv("NNMG_REG_TMA");
+      L->reg_tma = rt ? atoi(rt) != 0 : false;
       const char* er = getenv("NNMG_ELAST_RECOMPUTE");
       L->elast_recompute = er ? atoi(er) != 0 : false;
       const char* rr = getenv("NNMG_REG_RECOMPUTE");
@@ -431,6 +433,20 @@ __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const doubl
   CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
 }
 
+// stored G streamed through shared memory by TMA bulk copies (3D, GEO 3)
+template <int D, int P, bool NEG>
+__global__ void __launch_bounds__(128, 1) k_apply_reg_tma(Tables tab, const double* __restrict__ src,
+                                                         double* __restrict__ dst, const int* __restrict__ idx,
+                                                         const double* __restrict__ geo, int64_t b0, int64_t b1) {
+  extern __shared__ __align__(16) double dsm[];
+  const int warp = threadIdx.x >> 5;
+  const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  if (blk >= b1) return;
+  double* wsm = dsm + warp * (CellReg<D, P>::WARP_SMEM / sizeof(double));
+  CellReg<D, P>::template run<true, false, NEG, 3>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31,
+                                                   nullptr, wsm);
+}
+
 // all blocks recompute G from edge vectors, sum-factorised along z-pencils (3D)
 template <int D, int P, bool NEG>
 __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const double* __restrict__ src,
@@ -490,6 +506,22 @@ struct ApplyLaunch {
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
         if constexpr (D == 3) {
+          if (L.reg_tma) {
+            constexpr size_t smem = kWarpsPerCta * CellReg<D, P>::WARP_SMEM;
+            static bool attr = false;
+            if (!attr) {
+              NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply_reg_tma<D, P, true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+              NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply_reg_tma<D, P, false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+              attr = true;
+            }
+            auto kr = neg ? k_apply_reg_tma<D, P, true> : k_apply_reg_tma<D, P, false>;
+            kr<<<g, 32 * kWarpsPerCta, smem, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1);
+            NNMG_CHECK_LAUNCH();
+            count_launch();
+            return;
+          }
           if (L.edges.ptr && L.reg_recompute) {
             auto kr = neg ? k_apply_reg_rc<D, P, true> : k_apply_reg_rc<D, P, false>;
             kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, b0, b1, L.edges.ptr);

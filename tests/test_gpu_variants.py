@@ -59,6 +59,8 @@ APPLY_VARIANTS = [
     ("op_3d_q3", {"NNMG_APPLY_RECOMPUTE": "1", "NNMG_APPLY_SPLIT": "2"}),
     ("op_3d_q2", {"NNMG_RECOMPUTE_MOD": "2"}),
     ("op_3d_q2", {"NNMG_REG_RECOMPUTE": "1"}),
+    ("op_3d_q2", {"NNMG_REG_TMA": "1"}),
+    ("op_3d_q1", {"NNMG_REG_TMA": "1"}),
     ("op_3d_q1", {"NNMG_REG_RECOMPUTE": "1"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "4"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "8"}),
