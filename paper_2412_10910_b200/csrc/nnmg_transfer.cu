@@ -25,33 +25,33 @@ struct TransferDispatch {
   void operator()() {
     constexpr int CBC = cells_per_block<D, P, NC>();
     const Level& C = *T.coarse;
-    const unsigned g = grid_for(T.ncc, kWarps);
+    const unsigned g = grid_for(T.nitems, kWarps);
     if (mode < 2) {
       constexpr int PPL = prolongate_ppl<D, P, NC>();
       auto kp = (T.prolong_ppl == 2 && PPL == 1) ? k_prolongate<D, P, NC, CBC, 2> : k_prolongate<D, P, NC, CBC, PPL>;
-      kp<<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
-                                   T.ncc);
+      kp<<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.nitems == T.ncc ? nullptr : T.item_cell.ptr,
+                                   T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems);
       NNMG_CHECK_LAUNCH();
       count_launch();
     } else {
       const int ch = T.chunk;
-      const int64_t nwarps = (T.ncc + ch - 1) / ch;
+      const int64_t nwarps = (T.nitems + ch - 1) / ch;
       if constexpr (ipow(P + 1, D) * NC <= 32) {
         if (T.restrict_kernel != 2) {
           auto k = T.restrict_kernel == 0 ? k_restrict_lane<D, P, NC, 1>
                    : T.restrict_kernel == 3 ? k_restrict_lane<D, P, NC, 3>
                                             : k_restrict_lane<D, P, NC, 2>;
-          k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr,
-                                                            T.ncc, ch, T.cellbuf.ptr);
+          k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr,
+                                                            T.nitems, ch, T.cellbuf.ptr);
         } else {
           constexpr int W = StagedRestrict<D, P, NC>::WARPS;
           k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
-              C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr, T.ncc, ch, T.cellbuf.ptr);
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
         }
       } else {
         constexpr int W = StagedRestrict<D, P, NC>::WARPS;
         k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
-            C.tab, in, T.cell_start.ptr, T.pt_dof.ptr, T.xhat.ptr, T.ncc, ch, T.cellbuf.ptr);
+            C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
       }
       NNMG_CHECK_LAUNCH();
       k_restrict_gather<<<grid_for(C.n_scalar, 256), 256, 0, s>>>(T.t_off.ptr, T.t_ent.ptr, T.cellbuf.ptr,
@@ -97,30 +97,62 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
     T->cell_start.upload(start);
     T->pt_dof.upload(pd);
     T->xhat.upload(xh);
+    // work items: a coarse cell's point range split into pieces of at most
+    // maxp points, so levels with few, large coarse cells (C4: ~1,400 points
+    // per cell; its middle level has only 512 coarse cells) still fill the GPU
+    // Split only levels with fewer coarse cells than ~16 warps per SM
+    // (measured on B200: splitting C4's fine level, 12,167 cells, costs
+    // 0.437 -> 0.470 ms in the restriction)
+    int maxp = 1 << 30;
+    if (ncc < int64_t(148) * 16) {
+      const int64_t want = int64_t(148) * 32;  // items to aim for
+      maxp = static_cast<int>(std::max<int64_t>(64, (npts + want - 1) / want));
+    }
+    if (const char* e = getenv("NNMG_TRANSFER_MAXP")) maxp = std::max(32, atoi(e));
+    std::vector<int> ipt(1, 0), icell, ifirst(ncc + 1, 0);
+    for (int64_t c = 0; c < ncc; ++c) {
+      const int n = start[c + 1] - start[c];
+      const int k = std::max(1, (n + maxp - 1) / maxp);
+      ifirst[c] = static_cast<int>(icell.size());
+      for (int j = 0; j < k; ++j) {
+        icell.push_back(static_cast<int>(c));
+        ipt.push_back(start[c] + static_cast<int>((int64_t(n) * (j + 1)) / k));
+      }
+    }
+    ifirst[ncc] = static_cast<int>(icell.size());
+    T->nitems = static_cast<int64_t>(icell.size());
+    T->item_pt.upload(ipt);
+    T->item_cell.upload(icell);
     // transposed coarse map for the restriction gather
     const int nloc = coarse->nloc;
     const int64_t nsc = coarse->n_scalar;
     std::vector<int> off(nsc + 1, 0);
+    // entries (item, l) of every work item of the cells holding coarse DoF g,
+    // in a fixed order (cell, local index, item): deterministic phase 2
     for (int64_t e = 0; e < ncc * nloc; ++e) {
       const int g = coarse->cell_dofs_host[e];
-      if (!coarse->scalar_constrained[g]) off[g + 1] += 1;
+      if (!coarse->scalar_constrained[g]) off[g + 1] += ifirst[e / nloc + 1] - ifirst[e / nloc];
     }
     for (int64_t g = 0; g < nsc; ++g) off[g + 1] += off[g];
+    NNMG_REQUIRE(int64_t(off[nsc]) < (int64_t(1) << 31) && T->nitems * nloc < (int64_t(1) << 31), kUnsupported,
+                 "restriction map exceeds 2^31 entries");
     std::vector<int> pos(off.begin(), off.end() - 1);
     std::vector<int> ent(off[nsc]);
     for (int64_t e = 0; e < ncc * nloc; ++e) {
       const int g = coarse->cell_dofs_host[e];
-      if (!coarse->scalar_constrained[g]) ent[pos[g]++] = static_cast<int>(e);
+      if (coarse->scalar_constrained[g]) continue;
+      const int64_t c = e / nloc, l = e % nloc;
+      for (int it = ifirst[c]; it < ifirst[c + 1]; ++it) ent[pos[g]++] = static_cast<int>(it * nloc + l);
     }
     T->t_off.upload(off);
     T->t_ent.upload(ent);
-    T->cellbuf.alloc(size_t(ncc) * nloc * T->ncomp);
+    T->cellbuf.alloc(size_t(T->nitems) * nloc * T->ncomp);
     // restriction: consecutive coarse cells per warp, so the point stream is
     // pipelined across cell boundaries; aim for >= ~4 warps per SM slot
     {
       const char* e = getenv("NNMG_RESTRICT_CHUNK");
       const int64_t target_warps = int64_t(148) * 16 * 4;
-      int ch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, ncc / target_warps)));
+      int ch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, T->nitems / target_warps)));
       if (e) ch = std::max(1, std::min(31, atoi(e)));
       T->chunk = ch;
       // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups

@@ -16,9 +16,12 @@ struct Transfer {
   int restrict_kernel = 1;  // variant for NLOC*NCOMP <= 32 (see transfer_create)
   int prolong_ppl = 1;      // 2: two points per lane also where one is the default
   DevBuf<int> cell_start;   // [ncc+1] CSR of points by owning coarse cell
+  int64_t nitems = 0;       // work items: pieces of a cell's point range (<= NNMG_TRANSFER_MAXP points)
+  DevBuf<int> item_pt;      // [nitems+1] point range of each item
+  DevBuf<int> item_cell;    // [nitems] owning coarse cell of each item
   DevBuf<int> pt_dof;       // [npts] fine scalar DoF (sorted by cell, then point order)
   DevBuf<double> xhat;      // [npts][dim]
-  DevBuf<double> cellbuf;   // [ncc][nloc][ncomp] restriction partial local vectors
+  DevBuf<double> cellbuf;   // [nitems][nloc][ncomp] restriction partial local vectors
   DevBuf<int> t_off, t_ent; // coarse DoF -> (cell*nloc + l) entries, fixed order
   DevBuf<int> no_point;     // fine scalar DoFs without a point (zero in P u_c)
 };

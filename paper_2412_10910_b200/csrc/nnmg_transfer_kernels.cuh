@@ -124,16 +124,18 @@ __host__ __device__ constexpr int prolongate_ppl() {
 template <int DIM, int PC, int NCOMP, int CBC, int PPL>
 __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && PC >= 3 ? 4 : 6)
     k_prolongate(Tables tab, const double* __restrict__ uc, double* __restrict__ uf, int accumulate,
-                 const int* __restrict__ cidx, const int* __restrict__ cell_start, const int* __restrict__ pt_dof,
-                 const double* __restrict__ xhat, int64_t ncc) {
+                 const int* __restrict__ cidx, const int* __restrict__ item_cell, const int* __restrict__ item_pt,
+                 const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t nitems) {
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
   __shared__ double su[kTransferWarps][NCOMP * NLOC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t cell = blockIdx.x * (int64_t)kTransferWarps + warp;
-  if (cell >= ncc) return;
+  const int64_t item = blockIdx.x * (int64_t)kTransferWarps + warp;
+  if (item >= nitems) return;
+  // item_cell == nullptr: one item per cell (saves a dependent load)
+  const int64_t cell = item_cell ? (int64_t)item_cell[item] : item;
   const int64_t blk = cell / CBC, cl = cell % CBC;
-  const int p0 = cell_start[cell], p1 = cell_start[cell + 1];
+  const int p0 = item_pt[item], p1 = item_pt[item + 1];
   constexpr int STEP = 32 * PPL;
   // first round's records are in flight while the coarse values are staged
   int dd[PPL];

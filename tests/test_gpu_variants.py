@@ -122,6 +122,26 @@ def test_transfer_variant_matches_reference(pkg, monkeypatch, name, kernel, chun
         assert np.array_equal(got, T.restrict(r))  # deterministic, bitwise
 
 
+@pytest.mark.parametrize("name,maxp,kernel", [(n, m, k) for n in ("tr_3d_q2", "tr_3d_q4_warp", "tr_3d_el_q2", "tr_2d_q2")
+                                               for m in ("32", "64") for k in ("1", "2")])
+def test_transfer_split_cells_match_reference(pkg, monkeypatch, name, maxp, kernel):
+    """Coarse cells split into work items of at most `maxp` points (small
+    levels): partial local vectors per item, summed in the fixed-order gather."""
+    monkeypatch.setenv("NNMG_TRANSFER_MAXP", maxp)
+    monkeypatch.setenv("NNMG_RESTRICT_KERNEL", kernel)
+    g = golden(name)
+    sc, sf, T = _transfer(pkg, g)
+    rng = np.random.default_rng(1)
+    uc = rng.standard_normal((3, sc.n_dofs))
+    rf = rng.standard_normal((3, sf.n_dofs))
+    for u, want in zip(uc, g["prolongate"]):
+        assert rel(T.prolongate(u), want) <= TOL
+    for r, want in zip(rf, g["restrict"]):
+        got = T.restrict(r)
+        assert rel(got, want) <= TOL
+        assert np.array_equal(got, T.restrict(r))
+
+
 @pytest.mark.parametrize("kernel,chunk", [("1", "1"), ("1", "4"), ("2", "3"), ("0", "7")])
 def test_restriction_with_pointless_coarse_cells(pkg, oracle, monkeypatch, kernel, chunk):
     """A coarse mesh finer than the fine one: most coarse cells own no fine
