@@ -471,6 +471,25 @@ __global__ void k_mark_rows(const int* __restrict__ rows, int64_t n, unsigned ch
   if (i < n) flag[rows[i]] = 1;
 }
 
+// the single-barrier kernel for the configured split / residency / owner warps
+template <int D, int P, int NC, int PH, int OWW>
+static void (*cg1_kernel(const Coarse& C))(Cg1Args) {
+  if constexpr (OWW > 0) {
+    return C.split == 0   ? k_coarse_cg1<D, P, NC, PH, true, 0, OWW>
+           : C.split == 8 ? k_coarse_cg1<D, P, NC, PH, true, 8, OWW>
+           : C.split == 4 ? k_coarse_cg1<D, P, NC, PH, true, 4, OWW>
+           : C.split == 2 ? k_coarse_cg1<D, P, NC, PH, true, 2, OWW>
+                          : k_coarse_cg1<D, P, NC, PH, true, 1, OWW>;
+  } else {
+    return C.split == 0   ? k_coarse_cg1<D, P, NC, PH, true, 0>
+           : C.split == 8 ? k_coarse_cg1<D, P, NC, PH, true, 8>
+           : C.split == 4 ? k_coarse_cg1<D, P, NC, PH, true, 4>
+           : C.split == 2 ? k_coarse_cg1<D, P, NC, PH, true, 2>
+           : C.mode == 1  ? k_coarse_cg1<D, P, NC, PH, true, 1>
+                          : k_coarse_cg1<D, P, NC, PH, false, 1>;
+  }
+}
+
 struct CgLaunch {
   Coarse& C;
   const double* b;
@@ -622,6 +641,24 @@ struct CgLaunch {
           try_split<D, P, NC, PH, 8>(L, nsm, max_split) || try_split<D, P, NC, PH, 4>(L, nsm, max_split) ||
               try_split<D, P, NC, PH, 2>(L, nsm, max_split) || try_balanced<D, P, NC, PH>(L, nsm);
         }
+        // a dedicated owner warp overlapping the owner updates with the cell
+        // phase (resident tables only); NNMG_COARSE_OWNER_WARPS=0/1
+        if (C.single_barrier && C.mode == 1) {
+          const char* eo = getenv("NNMG_COARSE_OWNER_WARPS");
+          const int want = eo ? atoi(eo) : (NC > 1 ? 1 : 0);
+          if (want > 0) {
+            auto ko = cg1_kernel<D, P, NC, PH, 1>(C);
+            NNMG_CUDA_TRY(cudaFuncSetAttribute(ko, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+            NNMG_CUDA_TRY(cudaFuncSetAttribute(ko, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                               cudaSharedmemCarveoutMaxShared));
+            int per_sm = 0;
+            NNMG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ko, C.block + 32, C.smem));
+            if (per_sm > 0 && int64_t(per_sm) * nsm >= C.nrank) {
+              C.owner_warps = 1;
+              C.block += 32;
+            }
+          }
+        }
       }
       if (C.nrank > 256) C.single_barrier = false;  // k_coarse_cg1 reduces <= 8 partials per lane
       if (C.single_barrier && C.mode != 2) {
@@ -680,12 +717,7 @@ struct CgLaunch {
       g.max_iter = C.max_iter;
       g.status = C.status.ptr;
       g.trace = C.trace.n ? C.trace.ptr : nullptr;
-      auto k1 = C.split == 0   ? k_coarse_cg1<D, P, NC, PH, true, 0>
-                : C.split == 8 ? k_coarse_cg1<D, P, NC, PH, true, 8>
-                : C.split == 4 ? k_coarse_cg1<D, P, NC, PH, true, 4>
-                : C.split == 2 ? k_coarse_cg1<D, P, NC, PH, true, 2>
-                : C.mode == 1  ? k_coarse_cg1<D, P, NC, PH, true, 1>
-                               : k_coarse_cg1<D, P, NC, PH, false, 1>;
+      auto k1 = C.owner_warps ? cg1_kernel<D, P, NC, PH, 1>(C) : cg1_kernel<D, P, NC, PH, 0>(C);
       void* p1[] = {&g};
       NNMG_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k1, dim3(C.nrank), dim3(C.block), p1, C.smem, s));
       count_launch();

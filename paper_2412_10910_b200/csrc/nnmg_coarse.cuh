@@ -19,6 +19,7 @@ struct Coarse {
   int split = 1;  // CTAs per cell block (single-barrier kernel); 0: balanced cell ranges
   bool resident = false;  // cell-block tables kept in shared memory
   int mode = 0;           // 0 pencil, 1 pencil resident, 2 register kernel
+  int owner_warps = 0;    // single-barrier kernel: dedicated owner warps (overlap owner updates with cells)
   int barrier = 0;        // 0 grid.sync, 1 all-to-all slots, 2 root broadcast (NNMG_COARSE_BARRIER)
   DevBuf<unsigned long long> trace;  // NNMG_COARSE_TRACE: per-phase timestamps of CTA 0
   size_t smem = 0;

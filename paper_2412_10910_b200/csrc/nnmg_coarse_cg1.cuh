@@ -111,15 +111,33 @@ __device__ __forceinline__ void warp_sum3(double& a, double& b, double& c, int n
   }
 }
 
-template <int D, int P, int NC, int PH, bool RES, int SPLIT>
-__global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_coarse_cg1(Cg1Args a) {
+// OWW > 0: OWW dedicated owner warps (threads 0 .. 32 OWW - 1) run the owner
+// updates of phase k while the cell threads (the following warps, their own
+// named barrier) run the cell kernel of the same phase.  The two touch
+// disjoint buffers within a phase (see the buffer rotation above), exactly as
+// the owner pass of one CTA and the cell phase of another already do.
+template <int D, int P, int NC, int PH, bool RES, int SPLIT, int OWW = 0>
+__global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS + 32 * OWW) k_coarse_cg1(Cg1Args a) {
   using CK = Cg1Kernel<D, P, NC, PH, SPLIT>;
+  static_assert(OWW == 0 || RES, "owner warps need the resident-table cell phase");
+  constexpr int OT = 32 * OWW;                        // owner threads
+  constexpr int CELLW = (CK::NTHREADS + 31) / 32 * 32;  // cell threads, warp-rounded (named barrier count)
   namespace cg = cooperative_groups;
   extern __shared__ double sm[];
   __shared__ double red[3 * 32];
   cg::grid_group grid = cg::this_grid();
   const int rank = blockIdx.x, nrank = gridDim.x;
   const int tid = threadIdx.x, nth = blockDim.x;
+  const bool owner_thread = OWW == 0 || tid < OT;
+  const bool cell_thread = OWW == 0 || tid >= OT;
+  const int ctid = tid - OT;                        // index among the cell threads
+  const int otid = OWW ? tid : tid, onth = OWW ? OT : nth;  // owner loop index / stride
+  auto csync = [] __device__() {
+    if constexpr (OWW > 0)
+      asm volatile("bar.sync 1, %0;" ::"n"(CELLW) : "memory");
+    else
+      __syncthreads();
+  };
   constexpr int64_t kGeoChunk = int64_t(CK::NLOC) * CK::NG * CK::SCB;
   constexpr int64_t kIdxChunk = int64_t(CK::NLOC) * CK::SCB;
   double* geo_s = sm + CK::SMEM / sizeof(double);
@@ -167,7 +185,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
   constexpr int KO = 4;
   constexpr bool kPrefetch = NC == 1;
   constexpr bool kFold = NC == 1;
-  const bool fits = kPrefetch && a.prefetch_owned && (i1 - i0) <= KO * (int64_t)nth;
+  const bool fits = owner_thread && kPrefetch && a.prefetch_owned && (i1 - i0) <= KO * (int64_t)onth;
   double rp[KO], wp[KO], so[KO], di[KO], pp[KO], xx[KO];
   bool cf[KO];
   auto load_owned = [&](int k, int64_t i) {
@@ -176,7 +194,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     const double* s = a.s[k & 1];
 #pragma unroll
     for (int j = 0; j < KO; ++j) {
-      const int64_t ii = i + j * (int64_t)nth;
+      const int64_t ii = i + j * (int64_t)onth;
       if (ii < i1) {
         rp[j] = __ldcg(r + ii);
         wp[j] = __ldcg(w + ii);
@@ -194,7 +212,14 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
   constexpr int N1 = CK::N1;
   int gi[N1];
   double gr[NC][N1], gw[NC][N1], gs[NC][N1], gd[NC][N1];
-  if constexpr (RES) CK::template pencil_dofs<true>(idx_s, 0, tid, 0, gi);
+  if constexpr (RES) {
+    if (cell_thread) {
+      CK::template pencil_dofs<true>(idx_s, 0, ctid, 0, gi);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N1; ++i) gi[i] = -1;
+    }
+  }
   auto gather = [&](int k) {
     const double* r = a.r[(k + 1) & 1];
     const double* w = a.w[(k + 2) % 3];
@@ -218,7 +243,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
       for (int c = 0; c < NC; ++c) gd[c][i] = gi[i] >= 0 ? __ldg(a.inv_diag + (int64_t)gi[i] * NC + c) : 0.0;
     gather(0);
   }
-  if (fits) load_owned(0, i0 + tid);
+  if (fits) load_owned(0, i0 + otid);
   double alpha = 0.0, beta = 0.0, gamma_old = 1.0, alpha_old = 1.0, target = 0.0;
   int status_it = a.max_iter, status_conv = 0, status_err = 0;
   for (int k = 0; k <= a.max_iter; ++k) {
@@ -236,8 +261,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
 #pragma unroll
         for (int c = 0; c < NC; ++c)  // = src(gi * NC + c), bit for bit
           v[c][i] = gi[i] >= 0 ? gd[c][i] * fma(-alpha, fma(beta, gs[c][i], gw[c][i]), gr[c][i]) : 0.0;
-      e = CK::template run_values<true>(a.tab, gi, v, a.w[wb], geo_s, 0, a.lam, a.mu, sm, tid,
-                                        [] __device__() { __syncthreads(); });
+      if (cell_thread) e = CK::template run_values<true>(a.tab, gi, v, a.w[wb], geo_s, 0, a.lam, a.mu, sm, ctid, csync);
     } else {
       for (int64_t u = rank; u < a.nblk * SPLIT; u += nrank)
         e += CK::run(a.tab, src, a.w[wb], a.idx, a.geo, u / SPLIT, a.lam, a.mu, sm, tid,
@@ -248,7 +272,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     // scatters into them): Laplace folds them into the owners' pass below,
     // elasticity keeps a separate spread-out pass (measured faster there)
     if constexpr (!kFold) {
-      for (int64_t q = (int64_t)rank * nth + tid; q < a.ncons; q += (int64_t)nrank * nth) {
+      for (int64_t q = (int64_t)rank * onth + otid; owner_thread && q < a.ncons; q += (int64_t)nrank * onth) {
         const int c = a.cdofs[q];
         const double uc = src(c);
         a.w[wb][c] = uc;
@@ -257,11 +281,11 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     }
     // owners: s_{k-1}, r_k, p_{k-1}, x_k; gamma_k, ||r_k||^2; zero w_{k+1}
     double g = 0.0, rr = 0.0;
-    for (int64_t i = i0 + tid; i < i1; i += KO * (int64_t)nth) {
+    for (int64_t i = i0 + otid; owner_thread && i < i1; i += KO * (int64_t)onth) {
       if (!fits) load_owned(k, i);
 #pragma unroll
       for (int j = 0; j < KO; ++j) {
-        const int64_t ii = i + j * (int64_t)nth;
+        const int64_t ii = i + j * (int64_t)onth;
         if (ii < i1) {
           const double sk1 = fma(beta, so[j], wp[j]);    // s_{k-1}
           const double rk = fma(-alpha, sk1, rp[j]);     // r_k
@@ -324,7 +348,7 @@ __global__ void __launch_bounds__(Cg1Kernel<D, P, NC, PH, SPLIT>::NTHREADS) k_co
     // the next phase's gather / owner prefetches (which queue many sectors)
     const double totv = (a.atomic_dots && tid < 3) ? __ldcg(a.part + (k % 3) * 4 + tid) : 0.0;
     if constexpr (RES) gather(k + 1);
-    if (fits) load_owned(k + 1, i0 + tid);
+    if (fits) load_owned(k + 1, i0 + otid);
     // every CTA reduces the per-CTA partials in the same fixed order
     __shared__ double tot[3];
     if (a.atomic_dots) {
