@@ -165,3 +165,40 @@ def test_restriction_with_pointless_coarse_cells(pkg, oracle, monkeypatch, kerne
         u = rng.standard_normal(sc.n_dofs)
         assert rel(T.restrict(r), OT.restrict(r)) <= TOL
         assert rel(T.prolongate(u), OT.prolongate(u)) <= TOL
+
+
+# device-resident coarse Jacobi-PCG (solvers.py:193-206): owner-warp and
+# dot-product variants against the oracle CG (same iterations +-1, residual)
+COARSE_VARIANTS = [{"NNMG_COARSE_OWNER_WARPS": "0", "NNMG_COARSE_ATOMIC_DOTS": "1"},
+                   {"NNMG_COARSE_OWNER_WARPS": "1", "NNMG_COARSE_ATOMIC_DOTS": "1"},
+                   {"NNMG_COARSE_OWNER_WARPS": "0", "NNMG_COARSE_ATOMIC_DOTS": "0"},
+                   {"NNMG_COARSE_OWNER_WARPS": "1", "NNMG_COARSE_ATOMIC_DOTS": "0"}]
+
+
+@pytest.mark.parametrize("name", ["op_2d_q2", "op_3d_q2", "op_3d_el_q2", "op_3d_q4"])
+@pytest.mark.parametrize("env", COARSE_VARIANTS, ids=lambda e: "ow{}-atomic{}".format(
+    e["NNMG_COARSE_OWNER_WARPS"], e["NNMG_COARSE_ATOMIC_DOTS"]))
+def test_coarse_cg_variants_match_oracle(pkg, oracle, monkeypatch, name, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = golden(name)
+    problem = str(g["problem"])
+    dim = g["mesh_vertices"].shape[1]
+    ncomp = dim if problem == "elasticity" else 1
+    d = dirichlet_arg(g["dirichlet"])
+    sp = _space(pkg, g, ncomp=ncomp, dirichlet=d)
+    op = (pkg.mfoperator.ElasticityOperator(sp, *tuple(g["lame"])) if problem == "elasticity"
+          else pkg.mfoperator.LaplaceOperator(sp))
+    cs = pkg.solvers.CoarseSolver(op, dense_limit=0)
+    b = np.random.default_rng(7).standard_normal(sp.n_dofs)
+    x = cs.solve(b)
+    its, conv = cs.status()[:2]
+    assert conv
+    assert np.linalg.norm(b - op.apply(x)) <= 1.1e-8 * np.linalg.norm(b)
+    om = oracle.OMesh(dim, g["mesh_vertices"], g["mesh_cells"], g["mesh_faces"])
+    osp = oracle.make_space(om, int(g["p"]), ncomp, d)
+    oop = oracle.OOperator(osp, problem, *tuple(g["lame"]))
+    oc = oracle.OCoarse(oop, dense_limit=0)
+    xo = oc.solve(b)
+    assert abs(its - oc.last_iterations) <= 1, (its, oc.last_iterations)
+    assert rel(x, xo) <= 1e-6
