@@ -114,15 +114,15 @@ __device__ __forceinline__ double contract(const double* __restrict__ U, const d
 }
 
 // points per lane per round: two (each staged coarse value read from shared
-// memory serves both) for scalar fields; measured on B200: C3 0.251 -> 0.195
-// ms, C4 (Q4) 0.365 -> 0.314 ms; the 3-component variant spills
+// memory serves both); measured on B200: C3 0.251 -> 0.195 ms, C4 (Q4) 0.365
+// -> 0.314 ms, C5 (3 components, 126 registers) 0.047 -> 0.045 ms
 template <int DIM, int PC, int NCOMP>
 __host__ __device__ constexpr int prolongate_ppl() {
-  return NCOMP == 1 ? 2 : 1;
+  return 2;
 }
 
 template <int DIM, int PC, int NCOMP, int CBC, int PPL>
-__global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && PC >= 3 ? 4 : 6)
+__global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NCOMP > 1) ? 4 : 6)
     k_prolongate(Tables tab, const double* __restrict__ uc, double* __restrict__ uf, int accumulate,
                  const int* __restrict__ cidx, const int* __restrict__ item_cell, const int* __restrict__ item_pt,
                  const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t nitems) {
