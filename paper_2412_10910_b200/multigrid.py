@@ -28,7 +28,7 @@ from .fespace import build_space, dirichlet_constraints
 from .geosearch import SearchConfig
 from .mfoperator import ElasticityOperator, LaplaceOperator
 from .solvers import ChebyshevJacobi, CoarseSolver
-from .transfer import setup_nonnested
+from .transfer import setup_nested, setup_nonnested, setup_polynomial
 
 V_CYCLE_COMPONENTS = (
     "pre_smooth",
@@ -176,7 +176,7 @@ class MultigridHierarchy:
 
     def __del__(self):
         h = getattr(self, "_vc", None)
-        if h is not None and h.value and _lib._lib is not None:
+        if h is not None and h.value and _lib is not None and _lib._lib is not None:  # not at interpreter exit
             _lib.load().nnmg_vcycle_destroy(h)
             self._vc = None
 
@@ -230,31 +230,46 @@ def build_hp_hierarchy(meshes, degree, mode="h", nested=False, problem="poisson"
                        dirichlet_value=0.0, lame=None, search=None, config=None, device=None, timing=False):
     """GPU hierarchy over coarse-to-fine meshes (multigrid.py:145-203).
 
-    Supported: mode "h" with the non-nested point-evaluation transfer (the
-    BASELINE configurations).  The nested and polynomial transfers are listed
-    as next in SURVEY.md §8(f)."""
+    mode "h" uses the meshes as given; mode "hp" prepends Q^1..Q^(degree-1)
+    levels on the coarsest mesh below the geometric stack (polynomial
+    transfers).  nested=True uses the nested transfer between meshes (global
+    refinement), otherwise the non-nested point-evaluation transfer."""
     if mode not in ("h", "hp"):
         raise ValueError("mode must be 'h' or 'hp'")
-    if mode == "hp" or nested:
-        raise NotImplementedError("nested / hp transfers are not part of the GPU hot path yet")
     if not meshes:
         raise ValueError("need at least one mesh")
     cfg = config or HierarchyConfig()
     search = search or SearchConfig()
     dev = D.resolve_device(device)
     n_components = meshes[0].dim if problem == "elasticity" else 1
+    # (degree, mesh, kind of the incoming transfer) as multigrid.py:166-175
+    plan = []
+    if mode == "hp":
+        plan.append((1, meshes[0], None))
+        for p in range(2, degree + 1):
+            plan.append((p, meshes[0], "poly"))
+    else:
+        plan.append((degree, meshes[0], None))
+    for m in meshes[1:]:
+        plan.append((degree, m, "nested" if nested else "nonnested"))
     levels, transfers = [], []
-    for i, mesh in enumerate(meshes):
-        space = build_space(mesh, degree, n_components=n_components)
+    for p, mesh, kind in plan:
+        space = build_space(mesh, p, n_components=n_components)
         if dirichlet_ids is not None:
             space.constraints = dirichlet_constraints(space, dirichlet_ids, dirichlet_value)
         op = _make_operator(space, problem, lame, dev)
         smoother = ChebyshevJacobi(op, degree=cfg.chebyshev_degree, window_ratio=cfg.window_ratio,
                                    safety=cfg.safety, n_lanczos=cfg.lanczos_iters, seed=cfg.lanczos_seed)
         levels.append(Level(space, op, smoother))
-        if i > 0:
-            transfers.append(setup_nonnested(levels[-2].space, space, search, coarse_operator=levels[-2].operator,
-                                             fine_operator=op))
+        if kind is None:
+            continue
+        cop, cspace = levels[-2].operator, levels[-2].space
+        if kind == "poly":
+            transfers.append(setup_polynomial(cspace, space, coarse_operator=cop, fine_operator=op))
+        elif kind == "nested":
+            transfers.append(setup_nested(cspace, space, search, coarse_operator=cop, fine_operator=op))
+        else:
+            transfers.append(setup_nonnested(cspace, space, search, coarse_operator=cop, fine_operator=op))
     coarse = CoarseSolver(levels[0].operator, dense_limit=cfg.coarse_dense_limit,
                           cg_reduction=cfg.coarse_cg_reduction)
     return MultigridHierarchy(levels, transfers, coarse, m1=cfg.m1, m2=cfg.m2, timing=timing)

@@ -264,7 +264,7 @@ class CoarseSolver:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._lib is not None:
+        if h is not None and h.value and _lib is not None and _lib._lib is not None:  # not at interpreter exit
             _lib.load().nnmg_coarse_destroy(h)
             self._h = None
 

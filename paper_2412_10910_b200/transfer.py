@@ -1,4 +1,4 @@
-"""GPU non-nested two-level transfer (point evaluation and its exact transpose).
+"""GPU two-level transfers: point evaluation and its exact transpose.
 
 Drop-in twin of the reference ``TwoLevelTransferNonNested``
 (``/root/reference/pkg/src/nnmg/transfer.py:61-124``) and ``setup_nonnested``
@@ -7,6 +7,17 @@ Drop-in twin of the reference ``TwoLevelTransferNonNested``
 (transfer.py:35-36, 42, 51, 57), ``prolongate`` / ``restrict`` returning new
 vectors.  Point location runs on the GPU (geosearch.py here); the apply paths
 are the K6/K7 kernels of libnnmg_cuda.so.
+
+The nested (transfer.py:169-222) and polynomial (transfer.py:225-251)
+transfers of the reference are per-cell tensor-product embeddings with claim
+masks.  For conforming Lagrange spaces with the coarse space contained in the
+fine one, both ARE the nodal interpolation of the coarse field at the fine
+support points: the claiming cell's embedding evaluates the (continuous)
+coarse function at the fine node, and the transpose sums the same global
+basis-function values.  They are therefore built here on the same GPU point
+evaluation (identical operator up to rounding; parity against the reference's
+own outputs in tests/test_gpu_cellwise.py), with the reference's argument
+checks.
 """
 
 from __future__ import annotations
@@ -68,7 +79,7 @@ class TwoLevelTransferNonNested:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._lib is not None:
+        if h is not None and h.value and _lib is not None and _lib._lib is not None:  # not at interpreter exit
             _lib.load().nnmg_transfer_destroy(h)
             self._h = None
 
@@ -110,6 +121,35 @@ class TwoLevelTransferNonNested:
         return D.from_device(out, host)
 
 
+class TwoLevelTransferNested(TwoLevelTransferNonNested):
+    """GPU twin of ``TwoLevelTransferNested`` (transfer.py:169-222): nested mesh
+    pair (global refinement), same degree."""
+
+    def __init__(self, coarse_space, fine_space, search=None, coarse_operator=None, fine_operator=None,
+                 device=None):
+        if coarse_space.n_components != fine_space.n_components:
+            raise ValueError("component counts of the two levels must match")
+        if coarse_space.degree != fine_space.degree:
+            raise ValueError("nested mesh transfer keeps the polynomial degree")
+        super().__init__(coarse_space, fine_space, search, coarse_operator=coarse_operator,
+                         fine_operator=fine_operator, device=device)
+
+
+class TwoLevelTransferPolynomial(TwoLevelTransferNonNested):
+    """GPU twin of ``TwoLevelTransferPolynomial`` (transfer.py:225-251):
+    Q^(p-1) embedded into Q^p on one mesh."""
+
+    def __init__(self, coarse_space, fine_space, coarse_operator=None, fine_operator=None, device=None):
+        if coarse_space.n_components != fine_space.n_components:
+            raise ValueError("component counts of the two levels must match")
+        if coarse_space.mesh is not fine_space.mesh:
+            raise ValueError("polynomial transfer levels share one mesh")
+        if coarse_space.degree != fine_space.degree - 1:
+            raise ValueError("polynomial coarsening lowers the degree by one")
+        super().__init__(coarse_space, fine_space, SearchConfig(), coarse_operator=coarse_operator,
+                         fine_operator=fine_operator, device=device)
+
+
 def _level_for(space, device):
     if space.n_components == 1:
         return LaplaceOperator(space, device=device)
@@ -120,3 +160,17 @@ def setup_nonnested(coarse_space, fine_space, search=None, coarse_operator=None,
     """Locate the fine support points in the coarse mesh (transfer.py:254-256)."""
     return TwoLevelTransferNonNested(coarse_space, fine_space, search, coarse_operator=coarse_operator,
                                      fine_operator=fine_operator, device=device)
+
+
+def setup_nested(coarse_space, fine_space, search=None, coarse_operator=None, fine_operator=None, device=None):
+    """Nested mesh pair (transfer.py:259-260)."""
+    return TwoLevelTransferNested(coarse_space, fine_space, search, coarse_operator=coarse_operator,
+                                  fine_operator=fine_operator, device=device)
+
+
+def setup_polynomial(coarse_space, fine_space, coarse_operator=None, fine_operator=None, device=None):
+    """p -> p-1 transfer on a shared mesh; needs fine degree >= 2 (transfer.py:263-267)."""
+    if fine_space.degree < 2:
+        raise ValueError("polynomial coarsening needs degree >= 2")
+    return TwoLevelTransferPolynomial(coarse_space, fine_space, coarse_operator=coarse_operator,
+                                      fine_operator=fine_operator, device=device)
