@@ -159,20 +159,24 @@ def compute_diagonal(op):
     return op.diagonal()
 
 
-def assemble_rhs(space, f=None, chunk=1 << 16):
-    """Load vector b_i = (f, phi_i), constrained entries zeroed (host setup;
-    body-load part of mfoperator.py:313-355).  f: constant, per-component
+def assemble_rhs(space, f=None, neumann=None, chunk=1 << 16):
+    """Load vector b_i = (f, phi_i) + (g, phi_i)_GammaN, constrained entries
+    zeroed (host setup, mfoperator.py:313-414).  f: constant, per-component
     constant sequence, or callable of batched points returning (npts,) or
-    (npts, ncomp)."""
+    (npts, ncomp).  neumann: {boundary id: g} with g a constant, a callable of
+    (points, outward unit normals), or ("normal", m) for the traction m n."""
     from .fespace import gauss_legendre
     from .mesh import tensor_points
 
     mesh = space.mesh
     dim, p, ncomp = mesh.dim, space.degree, space.n_components
     b = np.zeros(space.n_dofs)
-    if f is None:
-        return b
     bm = b.reshape(space.n_scalar_dofs, ncomp)
+    if neumann:
+        _add_neumann(space, neumann, bm)
+    if f is None:
+        b[space.constraints.dofs] = 0.0
+        return b
     q1, w1 = gauss_legendre(p + 1)
     qpts = tensor_points(q1, dim)
     wq = tensor_points(w1, dim).prod(axis=1)
@@ -203,6 +207,66 @@ def assemble_rhs(space, f=None, chunk=1 << 16):
                                     minlength=space.n_scalar_dofs)
     b[space.constraints.dofs] = 0.0
     return b
+
+
+def _add_neumann(space, neumann, bm):
+    """Boundary term (g, phi_i) over the faces whose id has an entry in
+    ``neumann`` (mfoperator.py:356-411): on face (j, s) of a cell (face id
+    2j + s) the Gauss-Legendre rule of the other reference axes; surface
+    element |dx/dt1| (2D) or |dx/dt1 x dx/dt2| (3D); outward unit normal
+    J^-T (+-e_j) normalised."""
+    from .fespace import gauss_legendre
+    from .mesh import tensor_points
+
+    mesh = space.mesh
+    dim, p, ncomp = mesh.dim, space.degree, space.n_components
+    known = set(int(i) for i in mesh.boundary_ids())
+    for bid in neumann:
+        if bid not in known:
+            raise ValueError(f"unknown boundary id {bid}")
+    q1, w1 = gauss_legendre(p + 1)
+    tq = q1[:, None] if dim == 2 else tensor_points(q1, 2)
+    tw = w1 if dim == 2 else tensor_points(w1, 2).prod(axis=1)
+    bf = np.asarray(mesh.boundary_faces)
+    cell_dofs = np.asarray(space.cell_dofs)
+    for face in np.unique(bf[:, 1]):
+        j, side = int(face) // 2, int(face) % 2
+        tdims = [k for k in range(dim) if k != j]
+        ref = np.empty((len(tq), dim))
+        ref[:, j] = float(side)
+        ref[:, tdims] = tq
+        # local basis values at the face points (x fastest)
+        tab = np.ones((len(ref), 1))
+        for k in range(dim):
+            tab = (tab[:, None, :] * space.shape1d.values(ref[:, k])[:, :, None]).reshape(len(ref), -1)
+        cw, cg = _corner_w(dim, ref), _corner_grad(dim, ref)
+        for bid, g in neumann.items():
+            cells = bf[(bf[:, 1] == face) & (bf[:, 2] == bid), 0]
+            if len(cells) == 0:
+                continue
+            X = mesh.vertices[mesh.cells[cells]]                       # (nf, 2^d, d)
+            J = np.einsum("pvb,cva->cpab", cg, X)                        # dx_a / dxhat_b
+            xq = np.einsum("pv,cvd->cpd", cw, X)
+            if dim == 2:
+                dA = np.linalg.norm(J[:, :, :, tdims[0]], axis=2)
+            else:
+                dA = np.linalg.norm(np.cross(J[:, :, :, tdims[0]], J[:, :, :, tdims[1]]), axis=2)
+            e = np.zeros(dim)
+            e[j] = 1.0 if side == 1 else -1.0
+            nrm = np.linalg.solve(np.swapaxes(J, 2, 3), np.broadcast_to(e, J.shape[:2] + (dim,))[..., None])[..., 0]
+            nrm /= np.linalg.norm(nrm, axis=2)[:, :, None]
+            if isinstance(g, tuple) and g[0] == "normal":
+                gv = float(g[1]) * nrm
+            elif callable(g):
+                gv = np.asarray(g(xq.reshape(-1, dim), nrm.reshape(-1, dim)), dtype=float)
+                gv = gv.reshape(len(cells), len(ref), -1)
+            else:
+                gv = np.full((len(cells), len(ref), 1), float(g))
+            contrib = np.einsum("fqc,ql->flc", gv * (dA * tw[None, :])[:, :, None], tab)
+            flat = cell_dofs[cells].ravel()
+            for c in range(ncomp):
+                bm[:, c] += np.bincount(flat, weights=contrib[:, :, min(c, gv.shape[2] - 1)].ravel(),
+                                        minlength=space.n_scalar_dofs)
 
 
 def _corner_w(dim, x):
