@@ -254,7 +254,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": "fp64 V-cycle GDoF/s", "value": rate, "unit": "GDoF/s", "n_gpus": 0,
         "steps": max(1, args.steps), "warmup": max(1, args.warmup), "ms_per_step": el / max(1, args.steps) * 1e3,
-        "higher_is_better": True, "scaling": "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8(d) meshes)",
         "config": {"workload": CONFIG_TEXT[cfg.name] + f" (CPU sample 1/{args.cpu_scale})", "config": cfg.name},
         "cpu_baseline": {"value": rate, "unit": "GDoF/s", "cores": procs, "kind": "port", "sample": sample},
@@ -512,7 +512,7 @@ def run_ours(args, cfg):
         line = {
             "metric": "fp64 V-cycle GDoF/s", "value": value, "unit": "GDoF/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded SURVEY §8(d) jittered meshes, f=1 load vector)",
             "config": {"workload": CONFIG_TEXT[cfg.name] + ("" if args.scale == 1 else f" at 1/{args.scale}"),
                        "config": cfg.name, "fine_dofs": n, "levels_dofs": [lev.operator.n_dofs for lev in H.levels],
