@@ -44,15 +44,6 @@ __device__ __forceinline__ void lagrange_pp(const Tables& tab, double t, double 
   }
 }
 
-// phi_g(t) for one runtime node index g (the cooperative evaluation below)
-template <int N1>
-__device__ __forceinline__ double lagrange_one(const Tables& tab, double t, int g) {
-  double v = tab.rdenom[g];
-#pragma unroll
-  for (int j = 0; j < N1; ++j) v *= (j == g) ? 1.0 : (t - tab.nodes[j]);
-  return v;
-}
-
 // Transposing warp reduction of 32 per-lane values (entries >= N are zero):
 // afterwards lane l holds sum over lanes of a[l].  Recursive halving, each step
 // keeps the half selected by the lane bit and adds the partner's copy of it:
