@@ -645,7 +645,10 @@ struct CgLaunch {
         // phase (resident tables only); NNMG_COARSE_OWNER_WARPS=0/1
         if (C.single_barrier && C.mode == 1) {
           const char* eo = getenv("NNMG_COARSE_OWNER_WARPS");
-          const int want = eo ? atoi(eo) : (NC > 1 ? 1 : 0);
+          // measured (us per iteration): C5 5.33 -> 4.63, C2 4.00 -> 3.93 with an owner
+          // warp; C3 6.59 -> 8.69 (290 owned DoFs per CTA are too many for one warp)
+          const int64_t owned = (L.n_dofs + C.nrank - 1) / C.nrank;
+          const int want = eo ? atoi(eo) : (owned <= 5 * 32 ? 1 : 0);
           if (want > 0) {
             auto ko = cg1_kernel<D, P, NC, PH, 1>(C);
             NNMG_CUDA_TRY(cudaFuncSetAttribute(ko, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
