@@ -99,13 +99,15 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
     T->xhat.upload(xh);
     // work items: a coarse cell's point range split into pieces of at most
     // maxp points, so levels with few, large coarse cells (C4: ~1,400 points
-    // per cell; its middle level has only 512 coarse cells) still fill the GPU
+    // per cell; its middle level has only 512 coarse cells) still fill the GPU.
     // Split only levels with fewer coarse cells than ~16 warps per SM
     // (measured on B200: splitting C4's fine level, 12,167 cells, costs
     // 0.437 -> 0.470 ms in the restriction)
+    int nsm = 148;
+    NNMG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, coarse->device));
     int maxp = 1 << 30;
-    if (ncc < int64_t(148) * 16) {
-      const int64_t want = int64_t(148) * 32;  // items to aim for
+    if (ncc < int64_t(nsm) * 16) {
+      const int64_t want = int64_t(nsm) * 32;  // items to aim for
       maxp = static_cast<int>(std::max<int64_t>(64, (npts + want - 1) / want));
     }
     if (const char* e = getenv("NNMG_TRANSFER_MAXP")) maxp = std::max(32, atoi(e));
@@ -151,13 +153,13 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
     // pipelined across cell boundaries; aim for >= ~4 warps per SM slot
     {
       const char* e = getenv("NNMG_RESTRICT_CHUNK");
-      const int64_t target_warps = int64_t(148) * 16 * 4;
+      const int64_t target_warps = int64_t(nsm) * 16 * 4;
       int ch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, T->nitems / target_warps)));
       if (e) ch = std::max(1, std::min(31, atoi(e)));
       T->chunk = ch;
-      // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups
       const char* pp = getenv("NNMG_PROLONG_PPL");
       T->prolong_ppl = pp ? atoi(pp) : 1;
+      // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups
       const char* k = getenv("NNMG_RESTRICT_KERNEL");
       T->restrict_kernel = k ? atoi(k) : 1;
     }
