@@ -9,8 +9,8 @@
 //   * 1D Lagrange values by prefix/suffix products (5 N1 - 6 ops per axis);
 //   * restriction weights factorised (v X2[i2]) X1[i1] X0[i0]: N1^d FMAs plus
 //     N1 + N1^2 products instead of 2 N1^d products;
-//   * cell-end reductions as a transposing shuffle reduction (31 shuffles for
-//     32 outputs) instead of a butterfly per output (5 per output).
+//   * cell-end reductions through shared memory in a fixed order instead of a
+//     butterfly per output (5 shuffles per output).
 #pragma once
 
 #include "nnmg_kernels.cuh"
@@ -42,29 +42,6 @@ __device__ __forceinline__ void lagrange_pp(const Tables& tab, double t, double 
     }
     out[N1 - 1] = tab.rdenom[N1 - 1] * pre;
   }
-}
-
-// Transposing warp reduction of 32 per-lane values (entries >= N are zero):
-// afterwards lane l holds sum over lanes of a[l].  Recursive halving, each step
-// keeps the half selected by the lane bit and adds the partner's copy of it:
-// 31 shuffles + 31 adds per lane, fixed order (deterministic).
-template <int N>
-__device__ __forceinline__ double transpose_reduce(double (&a)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool hi = lane & o;
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      if (i >= N && i + o >= N && o == 16) {
-        a[i] = 0.0;  // both halves are padding
-        continue;
-      }
-      const double keep = hi ? a[i + o] : a[i];
-      const double send = hi ? a[i] : a[i + o];
-      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  return a[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -308,9 +285,17 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
   const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
   const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
   zero_empty_cells(R, c0, NOUT, lane, cellbuf);
-  double acc[32];
+  // cell-end reduction through shared memory: 32 lanes x NOUT partials (odd
+  // row stride: conflict-free both ways), then lane l sums column l over the
+  // 32 lanes in a fixed order.  ~2 NOUT + 32 instructions per lane instead of
+  // the transposing shuffle reduction's ~15 per value (64-bit selects and
+  // shuffles, wrapped in warp-sync because the flush is conditional).
+  constexpr int RS = NOUT | 1;
+  __shared__ double red[kTransferWarps][32 * RS];
+  double* rw = red[warp];
+  double acc[NOUT];
 #pragma unroll
-  for (int o = 0; o < 32; ++o) acc[o] = 0.0;
+  for (int o = 0; o < NOUT; ++o) acc[o] = 0.0;
   stream_rounds<DIM, NCOMP, PPR>(
       R, pt_dof, xhat, rf, 32, lane, true,
       [&](const double (&xs)[PPR][DIM], const double (&vs)[PPR][NCOMP]) {
@@ -350,10 +335,19 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
         }
       },
       [&](int ci) {
-        const double r = transpose_reduce<NOUT>(acc, lane);
-        if (lane < NOUT) cellbuf[(c0 + ci) * NOUT + lane] = r;
 #pragma unroll
-        for (int o = 0; o < 32; ++o) acc[o] = 0.0;
+        for (int o = 0; o < NOUT; ++o) {
+          rw[lane * RS + o] = acc[o];
+          acc[o] = 0.0;
+        }
+        __syncwarp();
+        if (lane < NOUT) {
+          double r = 0.0;
+#pragma unroll
+          for (int sl = 0; sl < 32; ++sl) r += rw[sl * RS + lane];
+          cellbuf[(c0 + ci) * NOUT + lane] = r;
+        }
+        __syncwarp();
       });
 }
 
