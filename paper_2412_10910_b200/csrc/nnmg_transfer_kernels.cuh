@@ -6,7 +6,8 @@
 // FP64 instruction count decides these kernels on B200 (ncu: FP64 pipe 42-55%
 // busy while DRAM is far from peak), so the per-point arithmetic is kept at the
 // minimum of the tensor-product form:
-//   * 1D Lagrange values by prefix/suffix products (5 N1 - 6 ops per axis);
+//   * 1D Lagrange values by prefix/suffix products without the 1/denom factors
+//     (3 N1 - 5 ops per axis), which are applied per local DoF once per cell;
 //   * restriction weights factorised (v X2[i2]) X1[i1] X0[i0]: N1^d FMAs plus
 //     N1 + N1^2 products instead of 2 N1^d products;
 //   * cell-end reductions through shared memory in a fixed order instead of a
@@ -19,29 +20,45 @@ namespace nnmg {
 
 static constexpr int kTransferWarps = 4;  // coarse cells (one per warp) per thread block
 
-// phi_i(t) for the N1 Lobatto-node Lagrange polynomials (fespace.py:42-51):
-// rdenom_i * prod_{j<i} d_j * prod_{j>i} d_j, d_j = t - node_j
+// Unnormalised values prod_{j!=i} (t - node_j) (3 N1 - 5 ops per axis; the
+// end nodes are exactly 0 and 1, nnmg_common.cu).  The 1/denom factors are
+// per local DoF, so the kernels apply their tensor product once per cell
+// (staged coarse values, cell-end sums) instead of once per point.
 template <int N1>
-__device__ __forceinline__ void lagrange_pp(const Tables& tab, double t, double (&out)[N1]) {
+__device__ __forceinline__ void lagrange_un(const Tables& tab, double t, double (&out)[N1]) {
   if constexpr (N1 == 1) {
     out[0] = 1.0;
   } else {
     double d[N1];
+    d[0] = t;
 #pragma unroll
-    for (int j = 0; j < N1; ++j) d[j] = t - tab.nodes[j];
+    for (int j = 1; j < N1 - 1; ++j) d[j] = t - tab.nodes[j];
+    d[N1 - 1] = t - 1.0;
     double suf[N1];
     suf[N1 - 1] = d[N1 - 1];
 #pragma unroll
     for (int j = N1 - 2; j >= 1; --j) suf[j] = d[j] * suf[j + 1];
-    out[0] = tab.rdenom[0] * suf[1];
+    out[0] = suf[1];
     double pre = d[0];
 #pragma unroll
     for (int i = 1; i < N1 - 1; ++i) {
-      out[i] = (tab.rdenom[i] * pre) * suf[i + 1];
+      out[i] = pre * suf[i + 1];
       pre *= d[i];
     }
-    out[N1 - 1] = tab.rdenom[N1 - 1] * pre;
+    out[N1 - 1] = pre;
   }
+}
+
+// prod_j 1/denom[l_j] of local point l (x fastest)
+template <int DIM, int N1>
+__device__ __forceinline__ double lagrange_norm(const Tables& tab, int l) {
+  double r = tab.rdenom[l % N1];
+#pragma unroll
+  for (int j = 1; j < DIM; ++j) {
+    l /= N1;
+    r *= tab.rdenom[l % N1];
+  }
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -122,7 +139,8 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
   for (int l = lane; l < NLOC; l += 32) {
     const int g = cidx[(blk * NLOC + l) * CBC + cl];
 #pragma unroll
-    for (int c = 0; c < NCOMP; ++c) su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] : 0.0;
+    for (int c = 0; c < NCOMP; ++c)
+      su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] * lagrange_norm<DIM, N1>(tab, l) : 0.0;
   }
   __syncwarp();
   for (int base = p0; base < p1; base += STEP) {
@@ -132,7 +150,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
     for (int k = 0; k < PPL; ++k) {
       cd[k] = dd[k];
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) lagrange_pp<N1>(tab, xt[k][j], X[k][j]);
+      for (int j = 0; j < DIM; ++j) lagrange_un<N1>(tab, xt[k][j], X[k][j]);
     }
     if (base + STEP < p1) load(base + STEP);
 #pragma unroll
@@ -303,7 +321,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
         for (int k = 0; k < PPR; ++k) {
           double X[DIM][N1];
 #pragma unroll
-          for (int j = 0; j < DIM; ++j) lagrange_pp<N1>(tab, xs[k][j], X[j]);
+          for (int j = 0; j < DIM; ++j) lagrange_un<N1>(tab, xs[k][j], X[j]);
 #pragma unroll
           for (int c = 0; c < NCOMP; ++c) {
             if constexpr (DIM == 3) {
@@ -345,7 +363,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
           double r = 0.0;
 #pragma unroll
           for (int sl = 0; sl < 32; ++sl) r += rw[sl * RS + lane];
-          cellbuf[(c0 + ci) * NOUT + lane] = r;
+          cellbuf[(c0 + ci) * NOUT + lane] = r * lagrange_norm<DIM, N1>(tab, lane / NCOMP);
         }
         __syncwarp();
       });
@@ -417,7 +435,7 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
           double X[N1];
 #pragma unroll
           for (int j = 0; j < DIM; ++j) {
-            lagrange_pp<N1>(tab, xs[0][j], X);
+            lagrange_un<N1>(tab, xs[0][j], X);
 #pragma unroll
             for (int i = 0; i < N1; ++i) st[lane * REC + (j == 0 ? 0 : (j == DIM - 1 ? K::OZ : K::A)) + i] = X[i];
           }
@@ -481,7 +499,7 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
           double sum = 0.0;
 #pragma unroll
           for (int sl = 0; sl < SLOTS; ++sl) sum += red[(sl * G + plane) * PLANE + k];
-          cellbuf[(c0 + ci) * NOUT + o] = sum;
+          cellbuf[(c0 + ci) * NOUT + o] = sum * lagrange_norm<DIM, N1>(tab, o / NCOMP);
         }
         __syncwarp();
       });
