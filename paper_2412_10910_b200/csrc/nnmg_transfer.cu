@@ -37,12 +37,24 @@ struct TransferDispatch {
       const int ch = T.chunk;
       const int64_t nwarps = (T.nitems + ch - 1) / ch;
       if constexpr (ipow(P + 1, D) * NC <= 32) {
-        if (T.restrict_kernel != 2) {
-          auto k = T.restrict_kernel == 0 ? k_restrict_lane<D, P, NC, 1>
-                   : T.restrict_kernel == 3 ? k_restrict_lane<D, P, NC, 3>
-                                            : k_restrict_lane<D, P, NC, 2>;
+        // default: 3 points per lane and round in 3D (C3 0.176 -> 0.173 ms), 2 in 2D
+        // (C2 0.022 vs 0.025 ms with 3); 4 points measured slower in both
+        const int rk = T.restrict_kernel >= 0 ? T.restrict_kernel : (D == 3 ? 3 : 1);
+        if (rk != 2) {
+          auto k = rk == 0 ? k_restrict_lane<D, P, NC, 1>
+                   : rk == 3 ? k_restrict_lane<D, P, NC, 3>
+                             : k_restrict_lane<D, P, NC, 2>;
           k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr,
                                                             T.nitems, ch, T.cellbuf.ptr);
+        } else {
+          constexpr int W = StagedRestrict<D, P, NC>::WARPS;
+          k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
+        }
+      } else if constexpr (ipow(P + 1, D) * NC <= 81) {
+        if (T.restrict_wide) {
+          k_restrict_lane<D, P, NC, 1><<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
         } else {
           constexpr int W = StagedRestrict<D, P, NC>::WARPS;
           k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
@@ -159,9 +171,13 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
       T->chunk = ch;
       const char* pp = getenv("NNMG_PROLONG_PPL");
       T->prolong_ppl = pp ? atoi(pp) : 1;
-      // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups
+      // NLOC*NCOMP <= 32: 0 / 1 / 3 = lane-owned with 1 / 2 / 3 points per round, 2 = staged groups,
+      // unset = 3 in 3D, 1 in 2D
       const char* k = getenv("NNMG_RESTRICT_KERNEL");
-      T->restrict_kernel = k ? atoi(k) : 1;
+      T->restrict_kernel = k ? atoi(k) : -1;
+      // 32 < NLOC*NCOMP <= 81: 1 = lane-owned local vector, 0 = staged groups
+      const char* w = getenv("NNMG_RESTRICT_WIDE");
+      T->restrict_wide = w ? atoi(w) : 0;
     }
     // fine scalar DoFs without a transfer point: zeroed by the plain prolongation
     std::vector<uint8_t> has(fine->n_scalar, 0);

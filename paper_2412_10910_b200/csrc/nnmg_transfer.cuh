@@ -13,7 +13,8 @@ struct Transfer {
   int dim = 0, pc = 0, ncomp = 1;
   int64_t npts = 0, ncc = 0;
   int chunk = 1;            // coarse cells per warp in the restriction
-  int restrict_kernel = 1;  // variant for NLOC*NCOMP <= 32 (see transfer_create)
+  int restrict_kernel = -1;  // variant for NLOC*NCOMP <= 32 (see transfer_create; -1: by dimension)
+  int restrict_wide = 0;    // 32 < NLOC*NCOMP <= 81: lane-owned local vector instead of staged groups
   int prolong_ppl = 1;      // 2: two points per lane also where one is the default
   DevBuf<int> cell_start;   // [ncc+1] CSR of points by owning coarse cell
   int64_t nitems = 0;       // work items: pieces of a cell's point range (<= NNMG_TRANSFER_MAXP points)

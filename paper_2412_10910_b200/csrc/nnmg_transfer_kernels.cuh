@@ -285,9 +285,10 @@ __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __
   }
 }
 
-// NLOC*NCOMP <= 32 (Q1/Q2 scalar, 2D vector): a lane owns a point and the full
-// local vector in registers; a cell's lanes are combined by the transposing
-// shuffle reduction, lane l ending with output l.
+// A lane owns a point and the full local vector in registers (NLOC*NCOMP <=
+// 32: Q1/Q2 scalar, 2D vector; up to 81 with NNMG_RESTRICT_WIDE: 3D Q2
+// elasticity, Q3 scalar); a cell's lanes are combined through shared memory
+// at the cell end, 32 outputs at a time, lane l ending with output l of a tile.
 template <int DIM, int PC, int NCOMP, int PPR>
 __global__ void __launch_bounds__(kTransferWarps * 32)
     k_restrict_lane(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
@@ -296,19 +297,21 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
   constexpr int NOUT = NLOC * NCOMP;
-  static_assert(NOUT <= 32, "lane-owned local vector");
+  static_assert(NOUT <= 81, "lane-owned local vector");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = (blockIdx.x * (int64_t)kTransferWarps + warp) * chunk;
   if (c0 >= ncc) return;
   const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
   const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
   zero_empty_cells(R, c0, NOUT, lane, cellbuf);
-  // cell-end reduction through shared memory: 32 lanes x NOUT partials (odd
-  // row stride: conflict-free both ways), then lane l sums column l over the
-  // 32 lanes in a fixed order.  ~2 NOUT + 32 instructions per lane instead of
-  // the transposing shuffle reduction's ~15 per value (64-bit selects and
-  // shuffles, wrapped in warp-sync because the flush is conditional).
-  constexpr int RS = NOUT | 1;
+  // cell-end reduction through shared memory: 32 lanes x (up to 32) partials
+  // per tile (odd row stride: conflict-free both ways), then lane l sums
+  // column l over the 32 lanes in a fixed order.  ~2 NOUT + 32 instructions
+  // per lane and tile instead of the transposing shuffle reduction's ~15 per
+  // value (64-bit selects and shuffles, wrapped in warp-sync because the
+  // flush is conditional).
+  constexpr int TW = NOUT < 32 ? NOUT : 32;
+  constexpr int RS = TW | 1;
   __shared__ double red[kTransferWarps][32 * RS];
   double* rw = red[warp];
   double acc[NOUT];
@@ -354,18 +357,23 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
       },
       [&](int ci) {
 #pragma unroll
-        for (int o = 0; o < NOUT; ++o) {
-          rw[lane * RS + o] = acc[o];
-          acc[o] = 0.0;
-        }
-        __syncwarp();
-        if (lane < NOUT) {
-          double r = 0.0;
+        for (int t0 = 0; t0 < NOUT; t0 += TW) {
 #pragma unroll
-          for (int sl = 0; sl < 32; ++sl) r += rw[sl * RS + lane];
-          cellbuf[(c0 + ci) * NOUT + lane] = r * lagrange_norm<DIM, N1>(tab, lane / NCOMP);
+          for (int j = 0; j < TW; ++j)
+            if (t0 + j < NOUT) {
+              rw[lane * RS + j] = acc[t0 + j];
+              acc[t0 + j] = 0.0;
+            }
+          __syncwarp();
+          const int o = t0 + lane;
+          if (lane < TW && o < NOUT) {
+            double r = 0.0;
+#pragma unroll
+            for (int sl = 0; sl < 32; ++sl) r += rw[sl * RS + lane];
+            cellbuf[(c0 + ci) * NOUT + o] = r * lagrange_norm<DIM, N1>(tab, o / NCOMP);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       });
 }
 

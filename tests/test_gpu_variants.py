@@ -122,6 +122,25 @@ def test_transfer_variant_matches_reference(pkg, monkeypatch, name, kernel, chun
         assert np.array_equal(got, T.restrict(r))  # deterministic, bitwise
 
 
+@pytest.mark.parametrize("wide", ["0", "1"])
+@pytest.mark.parametrize("name,chunk", [("tr_3d_el_q2", c) for c in ("1", "3", "6")])
+def test_restriction_wide_lane_matches_reference(pkg, monkeypatch, name, chunk, wide):
+    """32 < NLOC*NCOMP <= 81 (3D Q2 elasticity: 81 outputs, three 32-output
+    tiles in the cell-end reduction): the lane-owned local vector with the tiled cell-end reduction
+    (NNMG_RESTRICT_WIDE=1) against the staged groups, both against the reference."""
+    monkeypatch.setenv("NNMG_RESTRICT_WIDE", wide)
+    monkeypatch.setenv("NNMG_RESTRICT_CHUNK", chunk)
+    g = golden(name)
+    sc, sf, T = _transfer(pkg, g)
+    rng = np.random.default_rng(1)
+    rng.standard_normal((3, sc.n_dofs))  # the golden draws the coarse inputs first
+    rf = rng.standard_normal((3, sf.n_dofs))
+    for r, want in zip(rf, g["restrict"]):
+        got = T.restrict(r)
+        assert rel(got, want) <= TOL
+        assert np.array_equal(got, T.restrict(r))
+
+
 @pytest.mark.parametrize("name,maxp,kernel", [(n, m, k) for n in ("tr_3d_q2", "tr_3d_q4_warp", "tr_3d_el_q2", "tr_2d_q2")
                                                for m in ("32", "64") for k in ("1", "2")])
 def test_transfer_split_cells_match_reference(pkg, monkeypatch, name, maxp, kernel):
