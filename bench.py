@@ -562,6 +562,13 @@ def run_distributed(args, cfg):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if "RANK" not in os.environ:  # plain `python bench.py --distributed`: a world of one
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", device_id=dev)
     from paper_2412_10910_b200 import _lib, distributed, fespace
 
