@@ -306,6 +306,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
         L->apply_geos = gs ? atoi(gs) != 0 : false;
       }
       L->reg_minb = m ? atoi(m) : 1;
+      const char* fc = getenv("NNMG_FUSE_CONSTRAINED");
+      L->fuse_constrained = fc ? atoi(fc) != 0 : true;
       const char* rm = getenv("NNMG_RECOMPUTE_MOD");
       L->recompute_mod = rm ? atoi(rm) : 0;
       const char* rn = getenv("NNMG_RECOMPUTE_NUM");
@@ -405,6 +407,23 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
   return L;
 }
 
+// Constrained rows of the apply (mfoperator.py:114-121, zero-in / identity-out),
+// fused into the cell kernels' prologue: the residual form (NEG) subtracts
+// src there, the plain form copies it; cell threads never scatter to these
+// rows, so there is no ordering between the two.
+template <bool NEG>
+__device__ __forceinline__ void constrained_rows(const int* __restrict__ cd, int64_t ncd,
+                                                 const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncd; i += nthr) {
+    const int c = cd[i];
+    if constexpr (NEG)
+      dst[c] -= src[c];
+    else
+      dst[c] = src[c];
+  }
+}
+
 // one warp per cell block, one thread per cell (register-resident kernel)
 // Hybrid geometry: cell blocks with blk % rmod == 0 recompute G from their
 // edge vectors (288 B/cell instead of 1296 B/cell of stored G), the others
@@ -420,7 +439,8 @@ template <int D, int P, int MINB, bool NEG, bool HYB>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const double* __restrict__ src, double* __restrict__ dst,
                                                    const int* __restrict__ idx, const double* __restrict__ geo,
                                                    int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod,
-                                                   int rnum) {
+                                                   int rnum, const int* __restrict__ cd, int64_t ncd) {
+  if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= b1) return;
   if constexpr (HYB) {
@@ -463,8 +483,9 @@ template <int P, bool NEG, int GEO = 0>
 __global__ void __launch_bounds__(96) k_apply_reg_elast(Tables tab, const double* __restrict__ src,
                                                         double* __restrict__ dst, const int* __restrict__ idx,
                                                         const double* __restrict__ geo, int64_t b0, int64_t b1,
-                                                        double lam, double mu) {
+                                                        double lam, double mu, const int* __restrict__ cd, int64_t ncd) {
   __shared__ double sm[CellRegElast<P>::SMEM_DOUBLES];
+  if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x;
   if (blk >= b1) return;
   CellRegElast<P>::template run<NEG, GEO>(tab, src, dst, idx, geo, blk, lam, mu, sm);
@@ -497,6 +518,9 @@ struct ApplyLaunch {
   int64_t b0, b1;
   cudaStream_t s;
   bool neg;
+  const int* cd = nullptr;  // constrained rows to fuse into the cell kernel (nullptr: caller handles them)
+  int64_t ncd = 0;
+  bool fused = false;       // set when the launched kernel handled them
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
@@ -536,7 +560,8 @@ struct ApplyLaunch {
                              : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false, false>
                                                 : k_apply_reg<D, P, 1, false, false>));
         kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
-                                            hyb ? L.recompute_mod : 0, L.recompute_num);
+                                            hyb ? L.recompute_mod : 0, L.recompute_num, cd, ncd);
+        fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;
@@ -549,14 +574,16 @@ struct ApplyLaunch {
           if (L.edges.ptr && L.elast_recompute) {
             auto kr = neg ? k_apply_reg_elast<P, true, 2> : k_apply_reg_elast<P, false, 2>;
             kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.edges.ptr, b0, b1, L.lam,
-                                                         L.mu);
+                                                         L.mu, nullptr, 0);
             NNMG_CHECK_LAUNCH();
             count_launch();
             return;
           }
         }
         auto kr = neg ? k_apply_reg_elast<P, true> : k_apply_reg_elast<P, false>;
-        kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.lam, L.mu);
+        kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.lam, L.mu, cd,
+                                                     ncd);
+        fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;
@@ -612,6 +639,18 @@ void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t 
   dispatch(L.dim, L.degree, L.ncomp, L.physics, f);
 }
 
+// all cells plus the constrained rows; returns false when the rows are left to the caller
+static bool launch_apply_all(const Level& L, const double* src, double* dst, cudaStream_t s, bool negate) {
+  if (L.nblk <= 0) return false;
+  ApplyLaunch f{L, src, dst, 0, L.nblk, s, negate};
+  if (L.fuse_constrained) {
+    f.cd = L.cdofs.ptr;
+    f.ncd = static_cast<int64_t>(L.cdofs.n);
+  }
+  dispatch(L.dim, L.degree, L.ncomp, L.physics, f);
+  return f.fused && f.ncd == static_cast<int64_t>(L.cdofs.n);
+}
+
 __global__ void k_sub_constrained(const int* __restrict__ cd, int64_t n, const double* __restrict__ src,
                                   double* __restrict__ dst) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -620,9 +659,9 @@ __global__ void k_sub_constrained(const int* __restrict__ cd, int64_t n, const d
 
 void level_apply_sub(Level& L, const double* src, double* dst, cudaStream_t s) {
   NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
-  launch_apply_cells(L, src, dst, 0, L.nblk, s, true);
+  const bool fused = launch_apply_all(L, src, dst, s, true);
   const int64_t n = static_cast<int64_t>(L.cdofs.n);
-  if (n) {
+  if (n && !fused) {
     k_sub_constrained<<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
     NNMG_CHECK_LAUNCH();
     count_launch();
@@ -654,8 +693,7 @@ void level_load_vector(Level& L, const double* f, double* b, cudaStream_t s) {
 void level_apply(Level& L, const double* src, double* dst, cudaStream_t s) {
   NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
   NNMG_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * L.n_dofs, s));
-  launch_apply_cells(L, src, dst, 0, L.nblk, s, false);
-  launch_copy_constrained(L, src, dst, s);
+  if (!launch_apply_all(L, src, dst, s, false)) launch_copy_constrained(L, src, dst, s);
 }
 
 struct DiagLaunch {

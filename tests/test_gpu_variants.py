@@ -65,6 +65,10 @@ APPLY_VARIANTS = [
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "4"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "8"}),
     ("op_3d_q3", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "4"}),
+    # constrained rows by the separate copy / subtract kernels instead of the cell kernels' prologue
+    ("op_3d_q2", {"NNMG_FUSE_CONSTRAINED": "0"}),
+    ("op_2d_q2", {"NNMG_FUSE_CONSTRAINED": "0"}),
+    ("op_3d_el_q2", {"NNMG_FUSE_CONSTRAINED": "0"}),
 ]
 
 
