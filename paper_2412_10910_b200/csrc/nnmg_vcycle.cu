@@ -6,11 +6,12 @@
 #include "nnmg_vector.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace nnmg {
 
 void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const double* b, const double* x0,
-                    double* x, double* work, cudaStream_t s) {
+                    double* x, double* work, cudaStream_t s, bool residual_out) {
   NNMG_REQUIRE(L.diag_ready, kInvalidArgument, "level diagonal not computed");
   const int64_t n = L.n_dofs;
   double* r = work;
@@ -34,6 +35,7 @@ void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const 
     cheb_update(n, L.inv_diag.ptr, rho * rho_old, 2.0 * rho / delta, r, d, x, s);
     rho_old = rho;
   }
+  if (residual_out) level_apply_sub(L, d, r, s);
 }
 
 VCycle::~VCycle() {
@@ -48,6 +50,7 @@ VCycle* vcycle_create(int n_levels, Level* const* levels, Transfer* const* trans
   try {
     V->m1 = m1;
     V->m2 = m2;
+    if (const char* e = getenv("NNMG_SMOOTHER_RESIDUAL")) V->smoother_residual = atoi(e) != 0;
     for (int l = 0; l < n_levels; ++l) {
       NNMG_REQUIRE(levels[l] != nullptr, kInvalidArgument, "null level");
       V->levels.push_back(levels[l]);
@@ -92,12 +95,18 @@ static void cycle(VCycle& V, int l, const double* f, double* x, cudaStream_t s) 
   Level& L = *V.levels[l];
   Transfer& T = *V.transfers[l - 1];
   double* w = V.work[l].ptr;
+  // the residual f - A x (multigrid.py:101) costs one apply either way; taken
+  // from the last sweep's recurrence it needs no copy of f (same apply count)
+  const bool rec = V.smoother_residual && V.m1 > 0;
   for (int k = 0; k < V.m1; ++k)
-    smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, k == 0 ? nullptr : x, x, w, s);
+    smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, k == 0 ? nullptr : x, x, w, s,
+                   rec && k == V.m1 - 1);
   if (V.m1 == 0) NNMG_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double) * L.n_dofs, s));
-  double* r = V.r[l].ptr;
-  NNMG_CUDA_TRY(cudaMemcpyAsync(r, f, sizeof(double) * L.n_dofs, cudaMemcpyDeviceToDevice, s));
-  level_apply_sub(L, x, r, s);
+  double* r = rec ? w : V.r[l].ptr;
+  if (!rec) {
+    NNMG_CUDA_TRY(cudaMemcpyAsync(r, f, sizeof(double) * L.n_dofs, cudaMemcpyDeviceToDevice, s));
+    level_apply_sub(L, x, r, s);
+  }
   transfer_restrict(T, r, V.f[l - 1].ptr, s);
   cycle(V, l - 1, V.f[l - 1].ptr, V.x[l - 1].ptr, s);
   transfer_prolongate(T, V.x[l - 1].ptr, x, true, s);

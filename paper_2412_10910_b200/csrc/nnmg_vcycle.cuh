@@ -8,8 +8,10 @@
 
 namespace nnmg {
 
+// residual_out: one more residual-form apply after the last step leaves
+// b - A x in work[0, n) (the recurrence keeps r = b - A (x - d))
 void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const double* b, const double* x0,
-                    double* x, double* work, cudaStream_t s);
+                    double* x, double* work, cudaStream_t s, bool residual_out = false);
 
 struct VCycle {
   std::vector<Level*> levels;        // coarsest first
@@ -21,6 +23,7 @@ struct VCycle {
   // per level: right-hand side and correction (coarse levels), residual, smoother work
   std::vector<DevBuf<double>> f, x, r, work;
   bool use_graph = false;
+  bool smoother_residual = true;  // residual after pre-smoothing from the smoother's recurrence (no b copy)
   struct Graph {
     const double* f;
     double* x;
