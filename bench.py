@@ -132,11 +132,21 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
+            # the sampler is live before the timed region starts (its first
+            # line takes ~0.1-0.3 s), so short regions still get the samples
+            # that bracket them
+            t_end = time.time() + 5.0
+            while time.time() < t_end and os.path.getsize(self.path) == 0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
+        self.elapsed = time.time() - self.t0
+        if self.proc is not None and self.elapsed < 0.1:
+            time.sleep(0.06)  # one more sample right at the end of a short region
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -161,8 +171,12 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f == "Active"})
-        return {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": rows[0][1], "reasons": reasons,
-                "samples": len(rows)}
+        out = {"sm_mhz": float(np.median([r[0] for r in rows])), "sm_max_mhz": rows[0][1], "reasons": reasons,
+               "samples": len(rows)}
+        if getattr(self, "elapsed", 1.0) < 0.1:
+            out["note"] = (f"timed region {self.elapsed * 1e3:.1f} ms, shorter than the 50 ms sampling interval: "
+                           "samples taken just before and after it")
+        return out
 
 
 # ---------------------------------------------------------------------------

@@ -11,7 +11,7 @@
 namespace nnmg {
 
 void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const double* b, const double* x0,
-                    double* x, double* work, cudaStream_t s, bool residual_out) {
+                    double* x, double* work, cudaStream_t s, bool residual_out, const double* t) {
   NNMG_REQUIRE(L.diag_ready, kInvalidArgument, "level diagonal not computed");
   const int64_t n = L.n_dofs;
   double* r = work;
@@ -21,7 +21,11 @@ void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const 
   const double sigma = theta / delta;
   // residual form: the apply scatters -A(.) straight into r (no zeroing pass,
   // no separate A d vector); same recurrence as solvers.py:94-107
-  if (x0 == nullptr) {
+  if (t != nullptr) {
+    // work[0, n) holds f - A x: r = f - A (x + t), x = (x + t) + d
+    level_apply_sub(L, t, r, s);
+    cheb_init_add(n, t, L.inv_diag.ptr, theta, r, d, x, s);
+  } else if (x0 == nullptr) {
     cheb_init(n, b, nullptr, L.inv_diag.ptr, theta, r, d, x, s);
   } else {
     NNMG_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -51,6 +55,7 @@ VCycle* vcycle_create(int n_levels, Level* const* levels, Transfer* const* trans
     V->m1 = m1;
     V->m2 = m2;
     if (const char* e = getenv("NNMG_SMOOTHER_RESIDUAL")) V->smoother_residual = atoi(e) != 0;
+    if (const char* e = getenv("NNMG_POST_FROM_RESIDUAL")) V->post_from_residual = atoi(e) != 0;
     for (int l = 0; l < n_levels; ++l) {
       NNMG_REQUIRE(levels[l] != nullptr, kInvalidArgument, "null level");
       V->levels.push_back(levels[l]);
@@ -109,8 +114,18 @@ static void cycle(VCycle& V, int l, const double* f, double* x, cudaStream_t s) 
   }
   transfer_restrict(T, r, V.f[l - 1].ptr, s);
   cycle(V, l - 1, V.f[l - 1].ptr, V.x[l - 1].ptr, s);
-  transfer_prolongate(T, V.x[l - 1].ptr, x, true, s);
-  for (int k = 0; k < V.m2; ++k) smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s);
+  if (rec && V.m2 > 0 && V.post_from_residual) {
+    // the first post-smoothing sweep starts from the residual still in w:
+    // f - A (x + P e_c) = (f - A x) - A (P e_c), no copy of f; the
+    // correction is added inside the sweep's first vector kernel
+    double* t = V.r[l].ptr;
+    transfer_prolongate(T, V.x[l - 1].ptr, t, false, s);
+    smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s, false, t);
+    for (int k = 1; k < V.m2; ++k) smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s);
+  } else {
+    transfer_prolongate(T, V.x[l - 1].ptr, x, true, s);
+    for (int k = 0; k < V.m2; ++k) smoother_sweep(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s);
+  }
 }
 
 void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s) {

@@ -9,9 +9,12 @@
 namespace nnmg {
 
 // residual_out: one more residual-form apply after the last step leaves
-// b - A x in work[0, n) (the recurrence keeps r = b - A (x - d))
+// b - A x in work[0, n) (the recurrence keeps r = b - A (x - d)).
+// t != nullptr: work[0, n) already holds b - A x on entry and the sweep
+// starts from x + t (x0 == x, t added in the first vector kernel).
 void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const double* b, const double* x0,
-                    double* x, double* work, cudaStream_t s, bool residual_out = false);
+                    double* x, double* work, cudaStream_t s, bool residual_out = false,
+                    const double* t = nullptr);
 
 struct VCycle {
   std::vector<Level*> levels;        // coarsest first
@@ -24,6 +27,7 @@ struct VCycle {
   std::vector<DevBuf<double>> f, x, r, work;
   bool use_graph = false;
   bool smoother_residual = true;  // residual after pre-smoothing from the smoother's recurrence (no b copy)
+  bool post_from_residual = true; // first post-smoothing sweep starts from that residual (no b copy)
   struct Graph {
     const double* f;
     double* x;

@@ -54,6 +54,28 @@ __global__ void k_cheb_init(int64_t n, const double* __restrict__ b, const doubl
   x[i] = x0 ? x0[i] + di : di;
 }
 
+// post-smoothing start from the pre-smoothing residual: r already holds
+// f - A (x + t) (t = the prolongated correction, not yet added to x):
+// d = inv_diag*r/theta; x = (x + t) + d, the same roundings as x += t
+// followed by k_cheb_init
+__global__ void k_cheb_init_add(int64_t n, const double* __restrict__ t, const double* __restrict__ inv_diag,
+                                double theta, const double* __restrict__ r, double* __restrict__ d,
+                                double* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = inv_diag[i] * r[i] / theta;
+  d[i] = di;
+  x[i] = (x[i] + t[i]) + di;
+}
+
+void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double theta, const double* r, double* d,
+                   double* x, cudaStream_t s) {
+  if (!n) return;
+  k_cheb_init_add<<<grid_for(n), kBS, 0, s>>>(n, t, inv_diag, theta, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
 // r already holds r - A d: d = c1 d + c2 inv_diag r; x += d
 __global__ void k_cheb_update(int64_t n, const double* __restrict__ inv_diag, double c1, double c2,
                               const double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {

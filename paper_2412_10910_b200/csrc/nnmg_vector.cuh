@@ -12,6 +12,8 @@ void cheb_start(int64_t n, const double* b, const double* ax, const double* x0, 
                 double* r, double* d, double* x, cudaStream_t s);
 void cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
                double* x, cudaStream_t s);
+void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double theta, const double* r, double* d,
+                   double* x, cudaStream_t s);
 void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_diag, double theta, double* r,
                double* d, double* x, cudaStream_t s);
 void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,

@@ -237,11 +237,13 @@ def test_hierarchy_vcycle_and_solve_match_reference(pkg, tag):
         assert rel(xc[::sc], g["coarse_random_x"]) <= 1e-7
 
 
-@pytest.mark.parametrize("smoother_residual", ["1", "0"])
-def test_vcycle_timing_rows_and_graph_replay(pkg, monkeypatch, smoother_residual):
-    """Native executor (residual from the smoother recurrence, or f - A x
-    explicitly) and its graph replay against the Python recursion."""
+@pytest.mark.parametrize("smoother_residual,post", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_vcycle_timing_rows_and_graph_replay(pkg, monkeypatch, smoother_residual, post):
+    """Native executor (residual from the smoother recurrence or f - A x
+    explicitly; post-smoothing started from that residual or from a copy of
+    f) and its graph replay against the Python recursion."""
     monkeypatch.setenv("NNMG_SMOOTHER_RESIDUAL", smoother_residual)
+    monkeypatch.setenv("NNMG_POST_FROM_RESIDUAL", post)
     g, cfg, H, b = _hierarchy(pkg, "C2_s8", timing=True)
     H.v_cycle(b)
     comps = {(lvl, c) for lvl, c, _, _ in H.timing_rows()}
