@@ -26,7 +26,8 @@ void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const 
     level_apply_sub(L, t, r, s);
     cheb_init_add(n, t, L.inv_diag.ptr, theta, r, d, x, s);
   } else if (x0 == nullptr) {
-    cheb_init(n, b, nullptr, L.inv_diag.ptr, theta, r, d, x, s);
+    // x = d is folded into the first update when there is one
+    cheb_init(n, b, nullptr, L.inv_diag.ptr, theta, r, d, degree > 1 ? nullptr : x, s);
   } else {
     NNMG_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     level_apply_sub(L, x0, r, s);
@@ -36,7 +37,8 @@ void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const 
   for (int k = 0; k < degree - 1; ++k) {
     level_apply_sub(L, d, r, s);
     const double rho = 1.0 / (2.0 * sigma - rho_old);
-    cheb_update(n, L.inv_diag.ptr, rho * rho_old, 2.0 * rho / delta, r, d, x, s);
+    cheb_update(n, L.inv_diag.ptr, rho * rho_old, 2.0 * rho / delta, r, d, x, s,
+                k == 0 && x0 == nullptr && t == nullptr);
     rho_old = rho;
   }
   if (residual_out) level_apply_sub(L, d, r, s);

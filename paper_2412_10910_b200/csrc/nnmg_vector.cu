@@ -51,7 +51,7 @@ __global__ void k_cheb_init(int64_t n, const double* __restrict__ b, const doubl
   }
   const double di = inv_diag[i] * ri / theta;
   d[i] = di;
-  x[i] = x0 ? x0[i] + di : di;
+  if (x) x[i] = x0 ? x0[i] + di : di;  // x == nullptr: x = d is left to the first update
 }
 
 // post-smoothing start from the pre-smoothing residual: r already holds
@@ -77,13 +77,17 @@ void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double th
 }
 
 // r already holds r - A d: d = c1 d + c2 inv_diag r; x += d
+// (x_is_d: x was never written and equals the old d, so x = d_old + d_new:
+// the same rounding, one vector read and one write fewer)
 __global__ void k_cheb_update(int64_t n, const double* __restrict__ inv_diag, double c1, double c2,
-                              const double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
+                              const double* __restrict__ r, double* __restrict__ d, double* __restrict__ x,
+                              int x_is_d) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double di = c1 * d[i] + c2 * (inv_diag[i] * r[i]);
+  const double dold = d[i];
+  const double di = c1 * dold + c2 * (inv_diag[i] * r[i]);
   d[i] = di;
-  x[i] += di;
+  x[i] = (x_is_d ? dold : x[i]) + di;
 }
 
 void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_diag, double theta, double* r,
@@ -95,9 +99,9 @@ void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_d
 }
 
 void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool x_is_d) {
   if (!n) return;
-  k_cheb_update<<<grid_for(n), kBS, 0, s>>>(n, inv_diag, c1, c2, r, d, x);
+  k_cheb_update<<<grid_for(n), kBS, 0, s>>>(n, inv_diag, c1, c2, r, d, x, x_is_d ? 1 : 0);
   NNMG_CHECK_LAUNCH();
   count_launch();
 }

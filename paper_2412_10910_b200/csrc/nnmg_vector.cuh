@@ -17,7 +17,7 @@ void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double th
 void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_diag, double theta, double* r,
                double* d, double* x, cudaStream_t s);
 void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,
-                 cudaStream_t s);
+                 cudaStream_t s, bool x_is_d = false);
 void axpby(int64_t n, double alpha, const double* x, double beta, double* y, cudaStream_t s);
 void sub(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
 void mul(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
