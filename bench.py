@@ -54,10 +54,27 @@ def parse():
     ap.add_argument("--cpu-scale", type=int, default=5, help="sample scale for the CPU baseline")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--solve", action="store_true", help="also run the full PCG solve and report it")
+    ap.add_argument("--no-solve", action="store_true", help="skip the full PCG solve (host in / host out)")
     ap.add_argument("--profile", action="store_true", help="profiler range around one cycle + hot kernels, then exit")
     ap.add_argument("--distributed", action="store_true", help="use the cell-partitioned path even on one rank")
+    ap.add_argument("--coarse", default="auto", choices=["auto", "cg", "direct"],
+                    help="coarsest-level solver: the reference's CG, the exact direct solve, or the faster")
     return ap.parse_args()
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start N ranks over
+    NCCL on this node, exactly as the driver's torchrun command does."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    raise SystemExit(subprocess.call(cmd, env=env))
 
 
 def dist_env():
@@ -105,6 +122,19 @@ def measured_peaks():
             d = json.load(fh)
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def reference_pin(cname, key):
+    """A value the reference computed at full size (tests/golden/full_<C>.npz,
+    written by tests/golden/make_fullsize_pins.py in the build container)."""
+    path = os.path.join(ROOT, "tests", "golden", f"full_{cname}.npz")
+    if not os.path.exists(path):
+        return None
+    with np.load(path) as z:
+        if key not in z.files:
+            return None
+        v = z[key]
+        return v.item() if v.ndim == 0 else v.tolist()
 
 
 def traffic_from_profiles(kernel_key):
@@ -295,9 +325,11 @@ def run_ours(args, cfg):
 
     t_setup = time.perf_counter()
     meshes = cfg.make_meshes(scale=args.scale, validate=False)
+    coarse_direct = {"auto": "auto", "cg": False, "direct": True}[args.coarse]
     H = multigrid.build_hp_hierarchy(meshes, cfg.degree, problem=cfg.problem, dirichlet_ids=cfg.dirichlet_ids,
                                      lame=cfg.lame, config=multigrid.HierarchyConfig(
-                                         chebyshev_degree=cfg.chebyshev_degree), device=dev)
+                                         chebyshev_degree=cfg.chebyshev_degree, coarse_direct=coarse_direct),
+                                     device=dev)
     fine = H.finest.operator
     b = fine.load_vector(cfg.body_force if cfg.body_force else 1.0)
     torch.cuda.synchronize()
@@ -398,11 +430,40 @@ def run_ours(args, cfg):
         t_max = float(tt.item())
     value = world * n * args.steps / t_max / 1e9
 
-    # ---- e2e: pinned host r -> device -> V-cycle -> pinned host z ----
-    # Every step copies its input in and its result out; the copies of steps
-    # k+1 (H2D) and k-1 (D2H) run on their own streams / copy engines while
-    # the V-cycle of step k computes (two device buffer pairs, event-ordered),
-    # which is how a caller streams right-hand sides through the public call.
+    # ---- e2e (headline): a dependent chain through the public call ----
+    # every step copies its input from pinned host memory, runs the V-cycle
+    # and reads the result back before the next step starts (a PCG caller's
+    # pattern: each preconditioner input depends on the previous output)
+    hin = [b.cpu().pin_memory(), (2.0 * b).cpu().pin_memory()]
+    hout = [torch.empty_like(hin[0]).pin_memory() for _ in range(2)]
+    bin1, z1 = torch.empty_like(b), torch.empty_like(b)
+    with torch.cuda.stream(stream):
+        bin1.copy_(hin[0], non_blocking=True)
+        H.v_cycle_into(bin1, z1)
+        hout[0].copy_(z1, non_blocking=True)
+    stream.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for k in range(args.steps):
+            bin1.copy_(hin[k % 2], non_blocking=True)
+            H.v_cycle_into(bin1, z1)
+            hout[k % 2].copy_(z1, non_blocking=True)
+        e1.record(stream)
+    stream.synchronize()
+    t_chain = e0.elapsed_time(e1) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t_chain], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_chain = float(tt.item())
+    e2e_chain = world * n * args.steps / t_chain / 1e9
+
+    # ---- e2e upper bound: independent right-hand sides streamed ----
+    # the copies of steps k+1 (H2D) and k-1 (D2H) run on their own streams /
+    # copy engines while the V-cycle of step k computes (two device buffer
+    # pairs, event-ordered): a throughput bound for callers with independent
+    # inputs, not what a PCG loop sees
     hin = [b.cpu().pin_memory(), (2.0 * b).cpu().pin_memory()]
     hout = [torch.empty_like(hin[0]).pin_memory() for _ in range(2)]
     bin_ = [torch.empty_like(b) for _ in range(2)]
@@ -500,17 +561,28 @@ def run_ours(args, cfg):
     v_rf, v_bound = roof_frac(t_apply, B, FV, peak, fp64)
     p_rf, p_bound = roof_frac(t_pro, BT, FT, peak, fp64)
     r_rf, r_bound = roof_frac(t_res, BT, FT, peak, fp64)
-    applies_per_cycle = 2 * cfg.chebyshev_degree + 1
+    # fine applies per V-cycle: (m1 + m2) sweeps of degree k, the residual
+    # after pre-smoothing taken from the smoother's recurrence (one apply of
+    # the k pre-smoothing applies) -> 2k (8 for C3)
+    applies_per_cycle = (H.m1 + H.m2) * cfg.chebyshev_degree
 
-    # ---- optional full solve ----
+    # ---- full PCG solve through the public call, host in / host out ----
+    # cg_solve(A, b_numpy, precond=H.precondition, target_reduction=1e-8)
+    # (solvers.py:129-164): the H2D copy of b and the D2H copy of x are inside
+    # the timed region; iterations beside the reference's (tests/golden pins)
     solve = None
-    if args.solve:
+    if not args.no_solve:
+        b_host = b.cpu().numpy()
+        solvers.cg_solve(fine, b_host, precond=H.precondition, target_reduction=1e-8)  # warm
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = solvers.cg_solve(fine, b, precond=H.precondition, target_reduction=1e-8)
-        torch.cuda.synchronize()
-        solve = {"iterations": res.iterations, "converged": res.converged, "seconds": time.perf_counter() - t0,
-                 "final_rel_residual": res.residual_norms[-1] / res.residual_norms[0]}
+        res = solvers.cg_solve(fine, b_host, precond=H.precondition, target_reduction=1e-8)
+        t_solve = time.perf_counter() - t0
+        solve = {"iterations": res.iterations, "converged": res.converged, "seconds": t_solve,
+                 "final_rel_residual": res.residual_norms[-1] / res.residual_norms[0],
+                 "reference_iterations": reference_pin(cfg.name, "iterations"),
+                 "gdofs_per_s_x_iterations": n * res.iterations / t_solve / 1e9,
+                 "timing": "wall clock around cg_solve (host b in, host x out; every dot synchronises)"}
     cit, cconv, _ = H.coarse_solver.status() if not H.coarse_solver.dense else (None, None, None)
 
     cpu = None
@@ -553,8 +625,12 @@ def run_ours(args, cfg):
                 "restrict_roof_frac": r_rf, "restrict_bound": r_bound,
             },
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-                    "overlap": "H2D of step k+1 and D2H of step k-1 on separate streams during cycle k"},
+            "e2e": {"value": e2e_chain, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "pattern": "dependent chain: H2D of the step's input, V-cycle, D2H of its result, serialised "
+                               "on one stream (a PCG caller's pattern)",
+                    "pipelined_upper_bound": e2e,
+                    "pipelined_pattern": "independent inputs: H2D of step k+1 and D2H of step k-1 on separate "
+                                         "streams during cycle k"},
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -662,6 +738,10 @@ def main():
     from paper_2412_10910_b200.configs import get_config
 
     cfg = get_config(args.config)
+    if args.gpus > 1 and dist_env()[1] == 1 and "RANK" not in os.environ:
+        relaunch_under_torchrun(args)
+    if args.gpus != dist_env()[1] and "RANK" in os.environ:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={dist_env()[1]}")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif dist_env()[1] > 1 or args.distributed:

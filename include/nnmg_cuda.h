@@ -136,8 +136,20 @@ int nnmg_locate_points(int device, int dim, int64_t n_vertices, const double* ve
 /* ---- coarsest-level solver: replaces CoarseSolver (solvers.py:167-206) ---- */
 /* dense path: inverse_host (n x n, row-major) of the SPD coarse matrix */
 int nnmg_coarse_dense_create(nnmg_level_t level, const double* inverse_host, nnmg_coarse_t* out);
-/* Jacobi-PCG path as one persistent thread-block-cluster kernel */
+/* Jacobi-PCG path (the reference's CoarseSolver above the dense limit) as one
+ * persistent cooperative kernel over the whole GPU (one CTA per SM or per
+ * cell-block piece, Chronopoulos-Gear form with one grid barrier per
+ * iteration, fixed-order dot products) */
 int nnmg_coarse_cg_create(nnmg_level_t level, double reduction, int max_iter, nnmg_coarse_t* out);
+/* direct path for levels above the dense limit (a documented deviation: an
+ * exact solve where the reference iterates to a 1e-8 reduction; selected by
+ * CoarseSolver(direct=...) where it is faster): x = A_ff^-1 b on the free
+ * DoFs, x = b on the constrained ones.  inverse_dev is A_ff^-1 (nf x nf, free
+ * DoFs ascending = the complement of the level's constrained list) in DEVICE
+ * memory, row-major with leading dimension ld; only its lower triangle is
+ * read.  The library packs it into symmetric 64x64 tiles (nf^2/2 doubles
+ * streamed per solve, no atomics: bitwise reproducible). */
+int nnmg_coarse_direct_create(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out);
 int nnmg_coarse_destroy(nnmg_coarse_t coarse);
 int nnmg_coarse_solve(nnmg_coarse_t coarse, const double* b_dev, double* x_dev, void* stream);
 /* iterations / converged / indefinite flag of the last CG solve (synchronises) */

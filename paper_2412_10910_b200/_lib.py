@@ -68,6 +68,7 @@ _SIGNATURES = {
                            c_double, c_double, c_void_p, c_void_p, c_void_p, _p_int64, _p_int64],
     "nnmg_coarse_dense_create": [_handle, c_void_p, POINTER(_handle)],
     "nnmg_coarse_cg_create": [_handle, c_double, c_int, POINTER(_handle)],
+    "nnmg_coarse_direct_create": [_handle, c_void_p, c_int64, POINTER(_handle)],
     "nnmg_coarse_destroy": [_handle],
     "nnmg_coarse_solve": [_handle, c_void_p, c_void_p, c_void_p],
     "nnmg_coarse_status": [_handle, POINTER(c_int), POINTER(c_int), POINTER(c_int)],

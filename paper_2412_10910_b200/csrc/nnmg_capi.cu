@@ -226,6 +226,14 @@ int nnmg_coarse_cg_create(nnmg_level_t level, double reduction, int max_iter, nn
   });
 }
 
+int nnmg_coarse_direct_create(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    NNMG_REQUIRE(out && inverse_dev, kInvalidArgument, "null argument");
+    *out = reinterpret_cast<nnmg_coarse_t>(coarse_direct_create(LV(level), inverse_dev, ld));
+  });
+}
+
 int nnmg_coarse_destroy(nnmg_coarse_t coarse) {
   return guard([&] { delete CO(coarse); });
 }
@@ -252,7 +260,7 @@ int nnmg_coarse_info(nnmg_coarse_t coarse, int* cluster_ctas, int* threads_per_c
   return guard([&] {
     REQUIRE_HANDLE(coarse);
     Coarse* C = CO(coarse);
-    if (cluster_ctas) *cluster_ctas = C->dense ? 0 : C->nrank;
+    if (cluster_ctas) *cluster_ctas = (C->dense || C->direct) ? 0 : C->nrank;
     if (threads_per_cta) *threads_per_cta = C->block;
     if (subgroups) *subgroups = C->nsub;
   });

@@ -624,6 +624,11 @@ struct CgLaunch {
         NNMG_REQUIRE(per_sm > 0, kCudaError, "coarse CG kernel does not fit on an SM");
         C.nrank = static_cast<int>(std::min<int64_t>(nrank_one_round, int64_t(per_sm) * nsm));
       }
+      // the multi-barrier configuration, restored if the single-barrier
+      // kernel turns out not to apply after splitting / owner-warp tuning
+      const int s_mode = C.mode, s_block = C.block, s_nsub = C.nsub, s_nrank = C.nrank, s_split = C.split;
+      const bool s_resident = C.resident;
+      const size_t s_smem = C.smem;
       if (C.single_barrier && C.mode != 2) {
         auto k1 = C.mode == 1 ? k_coarse_cg1<D, P, NC, PH, true, 1> : k_coarse_cg1<D, P, NC, PH, false, 1>;
         NNMG_CUDA_TRY(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
@@ -664,6 +669,16 @@ struct CgLaunch {
         }
       }
       if (C.nrank > 256) C.single_barrier = false;  // k_coarse_cg1 reduces <= 8 partials per lane
+      if (!C.single_barrier) {
+        C.mode = s_mode;
+        C.block = s_block;
+        C.nsub = s_nsub;
+        C.nrank = s_nrank;
+        C.split = s_split;
+        C.resident = s_resident;
+        C.smem = s_smem;
+        C.owner_warps = 0;
+      }
       if (C.single_barrier && C.mode != 2) {
         C.con.alloc(size_t(L.n_dofs));
         C.con.zero();
@@ -714,7 +729,7 @@ struct CgLaunch {
       g.part = C.part.ptr;
       {
         const char* e = getenv("NNMG_COARSE_ATOMIC_DOTS");
-        g.atomic_dots = e ? atoi(e) : 1;
+        g.atomic_dots = e ? atoi(e) : 0;
       }
       g.reduction = C.reduction;
       g.max_iter = C.max_iter;
@@ -807,6 +822,10 @@ Coarse* coarse_cg_create(Level* L, double reduction, int max_iter) {
 }
 
 void coarse_solve(Coarse& C, const double* b, double* x, cudaStream_t s) {
+  if (C.direct) {
+    coarse_direct_solve(C, b, x, s);
+    return;
+  }
   if (C.dense) {
     const int n = static_cast<int>(C.level->n_dofs);
     k_dense_solve<<<grid_for(n, 8), 256, 0, s>>>(C.ainv.ptr, b, x, n);
@@ -828,6 +847,12 @@ void coarse_status(Coarse& C, int* iterations, int* converged, int* error) {
     fprintf(stderr, "\n");
   }
 #endif
+  if (C.direct || C.dense) {  // exact solves: no iterations
+    *iterations = 0;
+    *converged = 1;
+    *error = 0;
+    return;
+  }
   int st[3];
   NNMG_CUDA_TRY(cudaMemcpy(st, C.status.ptr, sizeof(st), cudaMemcpyDeviceToHost));
   *iterations = st[0];

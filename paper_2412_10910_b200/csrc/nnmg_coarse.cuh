@@ -23,10 +23,24 @@ struct Coarse {
   int barrier = 0;        // 0 grid.sync, 1 all-to-all slots, 2 root broadcast (NNMG_COARSE_BARRIER)
   DevBuf<unsigned long long> trace;  // NNMG_COARSE_TRACE: per-phase timestamps of CTA 0
   size_t smem = 0;
+  // direct path: packed lower-triangle 64x64 tiles of the SPD inverse of
+  // the free-DoF block
+  bool direct = false;
+  int64_t nfree = 0;
+  DevBuf<int> dfree, dcons;      // free DoFs (ascending), constrained DoFs
+  int nb = 0;                    // 64-row blocks of free DoFs
+  DevBuf<double> tiles;          // [nb(nb+1)/2][64][64], tile (I, J <= I) at I(I+1)/2 + J
+  DevBuf<double> prow, pcol;     // per-tile partial products (rows of I / columns of J)
 };
 
 Coarse* coarse_dense_create(Level* L, const double* inverse);
 Coarse* coarse_cg_create(Level* L, double reduction, int max_iter);
+// direct path: inverse_dev (nf x nf row-major, leading dimension ld, device
+// memory): the inverse of the free-DoF block (free DoFs ascending, the
+// complement of the level's constrained list), read in its lower triangle
+// only and packed into symmetric tiles
+Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld);
+void coarse_direct_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
 void coarse_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
 void coarse_status(Coarse& C, int* iterations, int* converged, int* error);
 

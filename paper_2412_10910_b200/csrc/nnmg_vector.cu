@@ -2,6 +2,8 @@
 // CG updates (solvers.py:129-164) and deterministic two-stage dot products.
 #include "nnmg_vector.cuh"
 
+#include <algorithm>
+
 namespace nnmg {
 
 static constexpr int kBS = 256;
@@ -261,6 +263,45 @@ __global__ void k_dfma_probe(double* out, int iters, double b, double c) {
   if (s == 12345.678) out[0] = s;  // keep the chains live
 }
 
+// FP64 tensor-core probe (mma.sync m8n8k4 f64, SASS DMMA): 4 independent
+// accumulator chains per warp.  DMMA and DFMA share one FP64 budget on B200
+// (profiles/r1_dmma_probe.txt); the larger of the two is the FP64 roof.
+__global__ void k_dmma_probe(double* out, int iters) {
+  double acc[4][2] = {};
+  const double a = 1.0 + threadIdx.x * 1e-6, b = 0.999;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(acc[j][0]), "+d"(acc[j][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s += acc[j][0] + acc[j][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+static double time_dmma(int sms, double* out) {
+  const int threads = 256, blocks = sms * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  NNMG_CUDA_TRY(cudaEventCreate(&e0));
+  NNMG_CUDA_TRY(cudaEventCreate(&e1));
+  k_dmma_probe<<<blocks, threads>>>(out, 16);
+  NNMG_CUDA_TRY(cudaEventRecord(e0));
+  k_dmma_probe<<<blocks, threads>>>(out, iters);
+  NNMG_CUDA_TRY(cudaEventRecord(e1));
+  NNMG_CUDA_TRY(cudaEventSynchronize(e1));
+  NNMG_CHECK_LAUNCH();
+  count_launch(2);
+  float ms = 0.f;
+  NNMG_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double warps = double(blocks) * threads / 32;
+  return warps * iters * 4 * (8.0 * 8 * 4 * 2) / (ms * 1e-3) / 1e12;
+}
+
 double measure_fp64_peak(int device) {
   NNMG_CUDA_TRY(cudaSetDevice(device));
   int sms = 0;
@@ -283,7 +324,8 @@ double measure_fp64_peak(int device) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   const double flops = 2.0 * 8.0 * iters * double(threads) * blocks;
-  return flops / (ms * 1e-3) / 1e12;
+  const double dfma = flops / (ms * 1e-3) / 1e12;
+  return std::max(dfma, time_dmma(sms, out.ptr));
 }
 
 }  // namespace nnmg

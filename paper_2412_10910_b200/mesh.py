@@ -227,3 +227,130 @@ def sine_warp(v):
 def from_reference(mesh):
     """Wrap a reference ``nnmg.mesh.Mesh`` (duck-typed) without re-validation."""
     return Mesh(mesh.dim, mesh.vertices, mesh.cells, mesh.boundary_faces, validate=False)
+
+
+# ---------------------------------------------------------------------------
+# gmsh ASCII v2.2 I/O (mesh.py:440-569): unstructured ingestion
+# ---------------------------------------------------------------------------
+# gmsh lists quad corners counter-clockwise and hex corners bottom-CCW then
+# top-CCW; swapping local corners 2<->3 (and 6<->7) maps that to the
+# lexicographic order used here, in both directions.
+_MSH_CORNER_SWAP = {2: np.array([0, 1, 3, 2]), 3: np.array([0, 1, 3, 2, 4, 5, 7, 6])}
+_MSH_CELL = {2: 3, 3: 5}   # element type: 3 = 4-node quad, 5 = 8-node hex
+_MSH_FACE = {2: 1, 3: 3}   # element type: 1 = 2-node line, 3 = 4-node quad
+_MSH_NODES = {1: 2, 2: 3, 3: 4, 4: 4, 5: 8, 15: 1}  # accepted element types -> node count
+
+
+def boundary_faces_of(cells, dim):
+    """(cell, local face) pairs of faces that belong to exactly one cell,
+    sorted by (cell, face)."""
+    cells = np.asarray(cells, dtype=np.int64)
+    nc = len(cells)
+    fv = np.stack([cells[:, face_vertex_indices(dim, f)] for f in range(2 * dim)], axis=1)  # (nc, 2d, 2^(d-1))
+    keys = np.sort(fv.reshape(nc * 2 * dim, -1), axis=1)
+    _, inv, cnt = np.unique(keys, axis=0, return_inverse=True, return_counts=True)
+    on = np.nonzero(cnt[inv.ravel()] == 1)[0]
+    return np.stack([on // (2 * dim), on % (2 * dim)], axis=1), keys[on]
+
+
+def write_msh(mesh, path):
+    """ASCII msh v2.2: nodes, one tagged line/quad element per boundary face
+    (physical tag = boundary id), then the cells (mesh.py:448-474)."""
+    dim = mesh.dim
+    out = ["$MeshFormat", "2.2 0 8", "$EndMeshFormat", "$Nodes", str(mesh.n_vertices)]
+    pad = np.zeros((mesh.n_vertices, 3))
+    pad[:, :dim] = mesh.vertices
+    out += [f"{i + 1} {x:.17g} {y:.17g} {z:.17g}" for i, (x, y, z) in enumerate(pad)]
+    out += ["$EndNodes", "$Elements", str(len(mesh.boundary_faces) + mesh.n_cells)]
+    eid = 0
+    for cell, face, bid in mesh.boundary_faces:
+        fv = mesh.cells[cell][face_vertex_indices(dim, face)]
+        if dim == 3:
+            fv = fv[[0, 1, 3, 2]]
+        eid += 1
+        out.append(f"{eid} {_MSH_FACE[dim]} 2 {bid} {eid} " + " ".join(str(v + 1) for v in fv))
+    swap = _MSH_CORNER_SWAP[dim]
+    for cell in mesh.cells:
+        eid += 1
+        out.append(f"{eid} {_MSH_CELL[dim]} 2 0 {eid} " + " ".join(str(v + 1) for v in cell[swap]))
+    out.append("$EndElements")
+    with open(path, "w") as fh:
+        fh.write("\n".join(out) + "\n")
+
+
+def _msh_sections(text):
+    sections, name, body = {}, None, None
+    for line in text.split("\n"):
+        s = line.strip()
+        if name is None:
+            if s.startswith("$") and not s.startswith("$End"):
+                name, body = s[1:], []
+        elif s == f"$End{name}":
+            sections[name] = body
+            name = None
+        else:
+            body.append(s)
+    if name is not None:
+        raise MeshError(f"malformed section {name}: missing $End{name}")
+    return sections
+
+
+def read_msh(path, validate=True):
+    """Quad/hex mesh from an ASCII msh v2.2 file (mesh.py:477-569): unused
+    nodes dropped (remaining ones keep their file order), cells in file order
+    with lexicographic corners, boundary faces = faces of exactly one cell,
+    boundary id = physical tag of the matching line/quad element (0 if none),
+    sorted by (cell, face).  Simplices are rejected.  The result has no
+    structured grid, so ``build_space`` numbers it by geometric matching."""
+    with open(path) as fh:
+        sec = _msh_sections(fh.read())
+    if "Nodes" not in sec or "Elements" not in sec:
+        raise MeshError("malformed msh file: missing $Nodes or $Elements")
+    try:
+        nn = int(sec["Nodes"][0])
+        tab = np.array(" ".join(sec["Nodes"][1:1 + nn]).split(), dtype=float).reshape(nn, 4)
+    except (ValueError, IndexError) as exc:
+        raise MeshError(f"malformed $Nodes section: {exc}") from exc
+    node_row = {int(i): k for k, i in enumerate(tab[:, 0].astype(np.int64))}
+    try:
+        ne = int(sec["Elements"][0])
+        rows = [[int(t) for t in sec["Elements"][1 + k].split()] for k in range(ne)]
+    except (ValueError, IndexError) as exc:
+        raise MeshError(f"malformed $Elements section: {exc}") from exc
+    elems = []
+    for r in rows:
+        etype, ntag = r[1], r[2]
+        if etype not in _MSH_NODES:
+            raise MeshError(f"unsupported element type {etype}")
+        nodes = r[3 + ntag:]
+        if len(nodes) != _MSH_NODES[etype]:
+            raise MeshError(f"malformed element line: expected {_MSH_NODES[etype]} nodes")
+        try:
+            elems.append((etype, r[3] if ntag else 0, [node_row[n] for n in nodes]))
+        except KeyError as exc:
+            raise MeshError(f"element references unknown node {exc}") from exc
+    kinds = {e[0] for e in elems}
+    if kinds & {2, 4}:
+        raise MeshError("unsupported element type: simplex elements are not handled")
+    dim = 3 if 5 in kinds else 2 if 3 in kinds else None
+    if dim is None:
+        raise MeshError("no quad or hex cells found")
+    cells = np.array([e[2] for e in elems if e[0] == _MSH_CELL[dim]], dtype=np.int64)[:, _MSH_CORNER_SWAP[dim]]
+    used = np.unique(cells)
+    renum = np.full(nn, -1, dtype=np.int64)
+    renum[used] = np.arange(len(used))
+    cells = renum[cells]
+    vertices = tab[used, 1:1 + dim]
+    pairs, keys = boundary_faces_of(cells, dim)
+    ids = np.zeros(len(pairs), dtype=np.int64)
+    lookup = {tuple(k): i for i, k in enumerate(keys.tolist())}
+    for etype, tag, nodes in elems:
+        if etype != _MSH_FACE[dim]:
+            continue
+        key = tuple(sorted(renum[np.array(nodes)].tolist()))
+        i = lookup.get(key)
+        if i is None or -1 in key:
+            raise MeshError("boundary element does not match any boundary face")
+        ids[i] = tag
+    faces = np.concatenate([pairs, ids[:, None]], axis=1)
+    return Mesh(dim, vertices, cells, faces, validate=validate)

@@ -214,6 +214,9 @@ class HierarchyConfig:
     lanczos_seed: int = 0
     coarse_dense_limit: int = 2000
     coarse_cg_reduction: float = 1e-8
+    # not in the reference: exact solve above the dense limit where faster
+    # (False = the reference's CG, the parity mode; True; "auto")
+    coarse_direct: object = False
 
 
 def _make_operator(space, problem, lame, device):
@@ -271,5 +274,5 @@ def build_hp_hierarchy(meshes, degree, mode="h", nested=False, problem="poisson"
         else:
             transfers.append(setup_nonnested(cspace, space, search, coarse_operator=cop, fine_operator=op))
     coarse = CoarseSolver(levels[0].operator, dense_limit=cfg.coarse_dense_limit,
-                          cg_reduction=cfg.coarse_cg_reduction)
+                          cg_reduction=cfg.coarse_cg_reduction, direct=cfg.coarse_direct)
     return MultigridHierarchy(levels, transfers, coarse, m1=cfg.m1, m2=cfg.m2, timing=timing)

@@ -219,16 +219,59 @@ def assemble_dense(op):
     return A.cpu().numpy()
 
 
+def assemble_dense_device(op, rows=None):
+    """Dense matrix of a GPU operator on the device: row k = (A e_j)[rows]
+    for j = rows[k] (A is symmetric; constrained rows/columns are unit
+    vectors as in assemble_oracle, mfoperator.py:255-285).  rows=None: all."""
+    n = op.n_dofs
+    dev = op.device
+    rows = np.arange(n) if rows is None else np.asarray(rows, dtype=np.int64)
+    ri = torch.from_numpy(rows).to(dev)
+    e = D.zeros(n, dev)
+    col = D.empty(n, dev)
+    A = torch.empty((len(rows), len(rows)), dtype=torch.float64, device=dev)
+    for k, j in enumerate(rows.tolist()):
+        e[j] = 1.0
+        _apply_into(op, e, col)
+        torch.index_select(col, 0, ri, out=A[k])
+        e[j] = 0.0
+    return A
+
+
+# effective stream rate of the direct solve's packed symmetric GEMV (B200,
+# measured: profiles/r2_coarse_direct.txt), used to predict its time
+DIRECT_STREAM_BYTES_PER_S = 6.3e12
+
+
+def direct_solve_bytes(n_free):
+    nb = (n_free + 63) // 64
+    return 8 * 4096 * nb * (nb + 1) // 2
+
+
 class CoarseSolver:
     """Dense Cholesky below dense_limit DoFs, otherwise Jacobi-PCG to
-    cg_reduction (solvers.py:167-206), both on the device."""
+    cg_reduction (solvers.py:167-206), both on the device.
 
-    def __init__(self, op, dense_limit=2000, cg_reduction=1e-8, cg_max_iter=10_000):
+    direct (not in the reference): above the dense limit, solve exactly with
+    the SPD inverse streamed as packed symmetric tiles (nnmg_coarse_direct_*)
+    instead of iterating.  False (default, the reference's semantics and the
+    parity mode), True, or "auto": only where the predicted GEMV time
+    (direct_solve_bytes / DIRECT_STREAM_BYTES_PER_S) beats 0.8x the measured
+    time of one CG solve and the setup fits in device memory.  The inverse
+    covers the free DoFs only (constrained rows are identity).  The V-cycle
+    then differs from the reference's at the level of the coarse CG tolerance
+    (1e-8); outer CG iteration counts are the parity gate."""
+
+    def __init__(self, op, dense_limit=2000, cg_reduction=1e-8, cg_max_iter=10_000, direct=False):
+        if direct not in (False, True, "auto"):
+            raise ValueError("direct must be False, True or 'auto'")
         self.op = op
         self.device = op.device
         self.cg_reduction = cg_reduction
         self.cg_max_iter = cg_max_iter
         self.dense = op.n_dofs <= dense_limit
+        self.direct = False
+        self.choice = "dense" if self.dense else "cg"
         h = ctypes.c_void_p()
         if self.dense:
             if len(op.constraints) == 0:
@@ -261,6 +304,69 @@ class CoarseSolver:
             op.diagonal_device()
             _lib.call("nnmg_coarse_cg_create", op.handle, float(cg_reduction), int(cg_max_iter), ctypes.byref(h))
         self._h = h
+        if not self.dense and direct:
+            nf = op.n_dofs - len(op.constraints.dofs)
+            t_cg = self._time_cg() if direct == "auto" else None
+            t_direct = direct_solve_bytes(nf) / DIRECT_STREAM_BYTES_PER_S
+            mem = torch.cuda.mem_get_info(self.device)[0]
+            fits = 3 * 8 * nf ** 2 + direct_solve_bytes(nf) < 0.8 * mem
+            self.timing = {"cg_s": t_cg, "direct_predicted_s": t_direct}
+            if direct is True or (fits and t_direct < 0.9 * t_cg):
+                self._make_direct()
+
+    def _time_cg(self):
+        """Device time of one CG solve on a random right-hand side (after one
+        untimed solve); the CG iteration count barely depends on the RHS."""
+        n = self.op.n_dofs
+        rng = np.random.default_rng(7)
+        b = torch.from_numpy(rng.standard_normal(n)).to(self.device)
+        b[torch.from_numpy(_lib.as_i64(self.op.constraints.dofs)).to(self.device)] = 0.0
+        x = D.empty(n, self.device)
+        s = torch.cuda.current_stream(self.device)
+        self.solve_into(b, x)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        self.solve_into(b, x)
+        e1.record(s)
+        e1.synchronize()
+        return e0.elapsed_time(e1) * 1e-3
+
+    def _make_direct(self):
+        n = self.op.n_dofs
+        cons = np.asarray(self.op.constraints.dofs, dtype=np.int64)
+        if len(cons) == 0:
+            # constants / rigid modes span the kernel (decided structurally, as
+            # the dense path does; test_solvers.py:167-172)
+            raise SingularCoarseSystemError(
+                "coarse matrix is numerically singular (all-Neumann system?); "
+                "pin the nullspace or add Dirichlet constraints"
+            )
+        free = np.setdiff1d(np.arange(n), cons)
+        A = assemble_dense_device(self.op, free)
+        A.add_(A.T.clone()).mul_(0.5)
+        Lc, info = torch.linalg.cholesky_ex(A)
+        del A
+        if int(info.item()) != 0:
+            raise SingularCoarseSystemError(
+                "coarse matrix is not positive definite (all-Neumann system?); "
+                "pin the nullspace or add Dirichlet constraints"
+            )
+        piv = Lc.diagonal().abs()
+        if len(piv) and float(piv.min()) <= 1e-8 * float(piv.max()):
+            raise SingularCoarseSystemError(
+                "coarse matrix is numerically singular (all-Neumann system?); "
+                "pin the nullspace or add Dirichlet constraints"
+            )
+        inv = torch.cholesky_inverse(Lc)
+        del Lc
+        h = ctypes.c_void_p()
+        _lib.call("nnmg_coarse_direct_create", self.op.handle, inv.data_ptr(), len(free), ctypes.byref(h))
+        torch.cuda.synchronize(self.device)
+        del inv
+        _lib.load().nnmg_coarse_destroy(self._h)
+        self._h = h
+        self.direct = True
+        self.choice = "direct"
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -280,7 +386,7 @@ class CoarseSolver:
         bd, host = D.to_device(b, self.op.n_dofs, self.device)
         x = D.empty(self.op.n_dofs, self.device)
         self.solve_into(bd, x)
-        if not self.dense:
+        if not self.dense and not self.direct:
             it, conv, indef = self.status()
             if indef:
                 raise IndefiniteOperatorError(f"p'Ap <= 0 at coarse iteration {it}")
@@ -295,7 +401,10 @@ class CoarseSolver:
     def info(self):
         a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _lib.call("nnmg_coarse_info", self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
-        return {"cluster_ctas": a.value, "threads_per_cta": b.value, "subgroups": c.value}
+        out = {"kind": self.choice, "cluster_ctas": a.value, "threads_per_cta": b.value, "subgroups": c.value}
+        if getattr(self, "timing", None):
+            out.update(self.timing)
+        return out
 
 
 def coarse_solve(solver, b):

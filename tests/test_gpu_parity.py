@@ -218,6 +218,9 @@ def test_hierarchy_vcycle_and_solve_match_reference(pkg, tag):
     lam = np.array([lev.smoother.lam_max for lev in H.levels])
     assert np.allclose(lam, g["lam_max"], rtol=1e-9), (lam, g["lam_max"])
     assert rel(b[::st], g["rhs"]) <= 1e-13
+    # GPU body-load kernel (k_load_vector) vs the reference's assemble_rhs
+    bl = H.finest.operator.load_vector(cfg.body_force if cfg.body_force else 1.0).cpu().numpy()
+    assert rel(bl[::st], g["rhs"]) <= 1e-12
     z_exec = H.v_cycle(b, executor=True)
     z_py = H.v_cycle(b, executor=False)
     assert rel(z_exec[::st], g["vcycle"]) <= 1e-9
