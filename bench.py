@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the full PCG solve (host in / host out)")
+    ap.add_argument("--no-mixed", action="store_true", help="skip the mixed-precision V-cycle measurement")
     ap.add_argument("--profile", action="store_true", help="profiler range around one cycle + hot kernels, then exit")
     ap.add_argument("--distributed", action="store_true", help="use the cell-partitioned path even on one rank")
     ap.add_argument("--coarse", default="auto", choices=["auto", "cg", "direct"],
@@ -585,6 +586,45 @@ def run_ours(args, cfg):
                  "timing": "wall clock around cg_solve (host b in, host x out; every dot synchronises)"}
     cit, cconv, _ = H.coarse_solver.status() if not H.coarse_solver.dense else (None, None, None)
 
+    # ---- mixed-precision V-cycle beside it ----
+    # fp32 storage of vectors / geometry / transfer records above the coarsest
+    # level, fp64 arithmetic and coarse solve; same device timing as `value`;
+    # parity by the outer PCG iteration count
+    mixed = None
+    if not args.no_mixed:
+        H.set_precision(32)
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 3)):
+                H.v_cycle_into(b, z)
+            if flush_mode:
+                t32 = 0.0
+                for k in range(args.steps):
+                    flush_buf.fill_(float(k))
+                    e0.record(stream)
+                    H.v_cycle_into(b, z)
+                    e1.record(stream)
+                    e1.synchronize()
+                    t32 += e0.elapsed_time(e1) * 1e-3
+            else:
+                e0.record(stream)
+                for _ in range(args.steps):
+                    H.v_cycle_into(b, z)
+                e1.record(stream)
+        stream.synchronize()
+        if not flush_mode:
+            t32 = e0.elapsed_time(e1) * 1e-3
+        if world > 1:
+            tt = torch.tensor([t32], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t32 = float(tt.item())
+        res32 = solvers.cg_solve(fine, b, precond=H.precondition, target_reduction=1e-8)
+        mixed = {"value": world * n * args.steps / t32 / 1e9, "unit": "GDoF/s",
+                 "ms_per_step": t32 / args.steps * 1e3, "solve_iterations": res32.iterations,
+                 "solve_converged": res32.converged, "reference_iterations": reference_pin(cfg.name, "iterations"),
+                 "storage": "fp32 level vectors, geometry, inverse diagonals, transfer xhat (levels >= 2); "
+                            "fp64 arithmetic, coarse solve and outer CG"}
+        H.set_precision(64)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, ncpu, k, el, procs = cpu_vcycle_rate_all_cores(cfg, args.cpu_scale, args.cpu_seconds)
@@ -636,6 +676,8 @@ def run_ours(args, cfg):
         }
         if solve is not None:
             line["solve"] = solve
+        if mixed is not None:
+            line["mixed_precision"] = mixed
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -166,6 +166,13 @@ int nnmg_vcycle_create(int n_levels, const nnmg_level_t* levels, const nnmg_tran
 int nnmg_vcycle_destroy(nnmg_vcycle_t vcycle);
 /* x_dev = V-cycle(f_dev) on the finest level (MultigridHierarchy.precondition) */
 int nnmg_vcycle_run(nnmg_vcycle_t vcycle, const double* f_dev, double* x_dev, void* stream);
+/* 64 (default): the fp64 cycle.  32: the mixed-precision cycle of the paper
+ * (the V-cycle in single precision inside double-precision CG):
+ * level vectors, stored geometry, inverse diagonals and transfer reference
+ * coordinates in fp32 on every level above the coarsest, fp64 arithmetic in
+ * registers, the coarse solve in fp64; f_dev / x_dev stay fp64.  Parity is by
+ * outer CG iteration count. */
+int nnmg_vcycle_set_precision(nnmg_vcycle_t vcycle, int bits);
 /* capture the cycle for (f_dev, x_dev) into a CUDA graph and replay it on run */
 int nnmg_vcycle_use_graph(nnmg_vcycle_t vcycle, int enable);
 /* number of kernels one cycle launches (for graph replays) */

@@ -78,6 +78,8 @@ _SIGNATURES = {
     "nnmg_vcycle_destroy": [_handle],
     "nnmg_vcycle_run": [_handle, c_void_p, c_void_p, c_void_p],
     "nnmg_vcycle_use_graph": [_handle, c_int],
+    "nnmg_vcycle_set_precision": [_handle, c_int],
+    "nnmg_level_set_deterministic": [_handle, c_int],
     "nnmg_vcycle_kernels_per_cycle": [_handle, _p_int64],
 }
 

@@ -291,6 +291,20 @@ int nnmg_vcycle_run(nnmg_vcycle_t vcycle, const double* f, double* x, void* stre
   });
 }
 
+int nnmg_level_set_deterministic(nnmg_level_t level, int enable) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    level_set_deterministic(*LV(level), enable != 0);
+  });
+}
+
+int nnmg_vcycle_set_precision(nnmg_vcycle_t vcycle, int bits) {
+  return guard([&] {
+    REQUIRE_HANDLE(vcycle);
+    vcycle_set_precision(*VC(vcycle), bits);
+  });
+}
+
 int nnmg_vcycle_use_graph(nnmg_vcycle_t vcycle, int enable) {
   return guard([&] {
     REQUIRE_HANDLE(vcycle);

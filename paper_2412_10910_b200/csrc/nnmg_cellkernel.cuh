@@ -130,11 +130,13 @@ struct CellKernel {
     for (int i = 0; i < N1; ++i) gi[i] = ld_geo<!kRes>(idx + (blk * NLOC + base + i) * GS + glane);
   }
 
-  template <bool kRes = false, bool kNeg = false, int GEO = 0, class Src, class Sync>
-  __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
+  // TD: storage type of dst (double, or float in the mixed-precision
+  // V-cycle); the arithmetic is fp64 either way
+  template <bool kRes = false, bool kNeg = false, int GEO = 0, class Src, class Sync, class TD>
+  __device__ __forceinline__ static double run(const Tables& tab, const Src& src, TD* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
                                                int64_t blk, double lam, double mu, double* sm, int tid,
-                                               Sync&& sync, int lane_off = 0) {
+                                               Sync&& sync, int lane_off = 0, double* __restrict__ cellout = nullptr) {
     // the block's geometry chunk (85% of the bytes) is consumed only in phase
     // 5: start streaming it into L2 now so it overlaps gathers and sweeps
     constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
@@ -175,16 +177,17 @@ struct CellKernel {
     for (int i = 0; i < N1; ++i)
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
-    return run_values<kRes, kNeg, GEO>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off);
+    return run_values<kRes, kNeg, GEO>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off, cellout);
   }
 
   // the cell kernel from gathered pencil values v (zero on gi < 0) onwards;
   // callers that can issue the gather early (the coarse CG) enter here
-  template <bool kRes = false, bool kNeg = false, int GEO = 0, class Sync>
+  template <bool kRes = false, bool kNeg = false, int GEO = 0, class Sync, class TD>
   __device__ __forceinline__ static double run_values(const Tables& tab, const int (&gi)[N1],
-                                                      double (&v)[NCOMP][N1], double* __restrict__ dst,
+                                                      double (&v)[NCOMP][N1], TD* __restrict__ dst,
                                                       const double* __restrict__ geo, int64_t blk, double lam,
-                                                      double mu, double* sm, int tid, Sync&& sync, int lane_off = 0) {
+                                                      double mu, double* sm, int tid, Sync&& sync, int lane_off = 0,
+                                                      double* __restrict__ cellout = nullptr) {
     // lsub indexes shared memory (stride SCB); glane indexes the tables:
     // HBM layout (stride CB) or a resident shared copy of the sub-block (SCB)
     NNMG_CT_BEGIN;
@@ -401,7 +404,10 @@ struct CellKernel {
       if (gi[i] >= 0) {
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
-          atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, kNeg ? -v[c][i] : v[c][i]);
+          if (cellout)  // deterministic mode: cell buffer [blk][l][comp][CB]
+            cellout[((blk * NLOC + PL::base(0, pen) + i) * NCOMP + c) * CB + glane] = v[c][i];
+          else
+            atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, TD(kNeg ? -v[c][i] : v[c][i]));
           energy = fma(u0[c][i], v[c][i], energy);
         }
       }
@@ -412,11 +418,14 @@ struct CellKernel {
   }
 };
 
-// read-only source vector (never written during the kernel)
-struct PlainSrc {
-  const double* __restrict__ s;
-  __device__ __forceinline__ double operator()(int64_t i) const { return __ldg(s + i); }
+// read-only source vector (never written during the kernel), fp64 or fp32
+// storage, read as fp64
+template <class T>
+struct PlainSrcT {
+  const T* __restrict__ s;
+  __device__ __forceinline__ double operator()(int64_t i) const { return double(__ldg(s + i)); }
 };
+using PlainSrc = PlainSrcT<double>;
 
 
 template <class F>

@@ -124,14 +124,17 @@ struct CellReg {
   static constexpr unsigned SLICE_BYTES = unsigned(SLICE_Q) * NG * CB * sizeof(double);
   static constexpr size_t WARP_SMEM = 2 * size_t(SLICE_BYTES) + 16;
 
-  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class Src>
-  __device__ __forceinline__ static double run(const Tables& tab, const Src& src, double* __restrict__ dst,
-                                               const int* __restrict__ idx, const double* __restrict__ geo,
+  // TD / TG: storage types of dst and of the stored geometry (double, or
+  // float in the mixed-precision V-cycle); the arithmetic is fp64 either way
+  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class Src, class TD, class TG>
+  __device__ __forceinline__ static double run(const Tables& tab, const Src& src, TD* __restrict__ dst,
+                                               const int* __restrict__ idx, const TG* __restrict__ geo,
                                                int64_t blk, int lane, const double* __restrict__ edges = nullptr,
-                                               double* wsm = nullptr) {
+                                               double* wsm = nullptr, double* __restrict__ cellout = nullptr) {
+    static_assert(GEO != 3 || sizeof(TG) == sizeof(double), "TMA slice staging is fp64");
     double* gbuf = wsm;
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wsm + 2 * SLICE_Q * NG * CB);
-    const double* gchunk = geo + blk * (int64_t)NLOC * NG * CB;
+    const TG* gchunk = geo + blk * (int64_t)NLOC * NG * CB;
     if constexpr (GEO == 3) {
       static_assert(DIM == 3, "slice staging is 3D");
       if (lane == 0) {
@@ -154,7 +157,7 @@ struct CellReg {
     } else if constexpr (kStream && GEO == 0) {
       // the warp's geometry chunk (32 cells, 85% of the bytes) streams into L2
       // while the gathers and interpolation sweeps run
-      constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
+      constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(TG);
       if (lane == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
     }
     double v[NLOC];
@@ -257,7 +260,7 @@ struct CellReg {
         }
       }
     } else {
-      const double* g0 = geo + blk * (int64_t)NLOC * NG * CB + lane;
+      const TG* g0 = geo + blk * (int64_t)NLOC * NG * CB + lane;
 #pragma unroll
       for (int q = 0; q < NLOC; ++q) {
         const int qx = q % N1, qy = (q / N1) % N1, qz = DIM == 3 ? q / (N1 * N1) : 0;
@@ -276,9 +279,9 @@ struct CellReg {
 #pragma unroll
             for (int k = 0; k < NG; ++k) gg[k] = G[k * CB];
           } else {
-            const double* G = g0 + q * NG * CB;
+            const TG* G = g0 + q * NG * CB;
 #pragma unroll
-            for (int k = 0; k < NG; ++k) gg[k] = ld_geo<kStream>(G + k * CB);
+            for (int k = 0; k < NG; ++k) gg[k] = double(ld_geo<kStream>(G + k * CB));
           }
           if constexpr (DIM == 3) {
             fx = gg[0] * gx + gg[1] * gy + gg[2] * gz;
@@ -313,7 +316,12 @@ struct CellReg {
       // the index table is re-read (L1/L2 hit) rather than kept live
       const int g = kStream ? __ldg(ib + l * CB) : ib[l * CB];
       if (g >= 0) {
-        atomicAdd(dst + g, kNeg ? -w[l] : w[l]);
+        // deterministic mode: the cell's result goes to the cell buffer in
+        // the idx layout (coalesced), a fixed-order gather sums it later
+        if (cellout)
+          cellout[(blk * NLOC + l) * CB + lane] = w[l];
+        else
+          atomicAdd(dst + g, TD(kNeg ? -w[l] : w[l]));
         if constexpr (kEnergy) energy = fma(u0[l], w[l], energy);
       }
     }

@@ -74,16 +74,19 @@ struct CellRegElast {
   // trilinear map dx/dz is affine in qy, dx/dy constant per slice and dx/dx
   // affine in qy per slice; with cofactors C: J^-1 = C^T / det,
   // pg = g C^T / det and flux = w_q sigma C.
-  template <bool kNeg, int GEO = 0>
-  __device__ __forceinline__ static void run(const Tables& tab, const double* __restrict__ src, double* __restrict__ dst,
-                                             const int* __restrict__ idx, const double* __restrict__ geo, int64_t blk,
-                                             double lam, double mu, double* sm) {
+  // TV / TG: storage types of the vectors and of the stored geometry (double,
+  // or float in the mixed-precision V-cycle); the arithmetic is fp64
+  template <bool kNeg, int GEO = 0, class TV, class TG>
+  __device__ __forceinline__ static void run(const Tables& tab, const TV* __restrict__ src, TV* __restrict__ dst,
+                                             const int* __restrict__ idx, const TG* __restrict__ geo, int64_t blk,
+                                             double lam, double mu, double* sm, double* __restrict__ cellout = nullptr) {
+    static_assert(GEO == 0 || sizeof(TG) == sizeof(double), "edge recompute reads fp64 edges");
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     static_assert(GEO == 0 || N1 == 3, "edge recompute relies on qx == component in phase B");
     constexpr int NE = 36;
     if (w == 0 && lane == 0) {
       if constexpr (GEO == 0) {
-        constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
+        constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(TG);
         prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
       } else {
         prefetch_l2_bulk(geo + blk * (int64_t)NE * CB, unsigned(NE) * CB * sizeof(double));
@@ -96,7 +99,7 @@ struct CellRegElast {
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) {
       const int g = __ldcs(ib + l * CB);
-      v[l] = g >= 0 ? __ldg(src + (int64_t)g * 3 + w) : 0.0;
+      v[l] = g >= 0 ? double(__ldg(src + (int64_t)g * 3 + w)) : 0.0;
     }
     sweep_axis<0, false>(tab.S, v);
     sweep_axis<1, false>(tab.S, v);
@@ -104,9 +107,9 @@ struct CellRegElast {
     double acc[NLOC];
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) acc[l] = 0.0;
-    const double* gb = geo + blk * (int64_t)NLOC * NG * CB + lane;
-    const double* eb = geo + blk * (int64_t)NE * CB + lane;
-    auto e = [&](int b, int k, int a) { return __ldg(eb + ((b * 4 + k) * 3 + a) * CB); };
+    const TG* gb = geo + blk * (int64_t)NLOC * NG * CB + lane;
+    const TG* eb = geo + blk * (int64_t)NE * CB + lane;
+    auto e = [&](int b, int k, int a) { return double(__ldg(eb + ((b * 4 + k) * 3 + a) * CB)); };
     // GEO 2: dx/dz at (qx = w, y) = A2 + y B2 (edges along z, k = x + 2y)
     double A2[3], B2[3];
     if constexpr (GEO == 2) {
@@ -191,12 +194,12 @@ struct CellRegElast {
               for (int b = 0; b < 3; ++b) K[a][b] = C[b][a] * rdet;
             dv = det * (tab.w[w] * tab.w[k] * tab.w[qz]);
           } else {
-            const double* G = gb + (qz * SLICE + s) * NG * CB;
+            const TG* G = gb + (qz * SLICE + s) * NG * CB;
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-              for (int b = 0; b < 3; ++b) K[a][b] = __ldcs(G + (a * 3 + b) * CB);
-            dv = __ldcs(G + 9 * CB);
+              for (int b = 0; b < 3; ++b) K[a][b] = double(__ldcs(G + (a * 3 + b) * CB));
+            dv = double(__ldcs(G + 9 * CB));
           }
           // pg = ghat J^-1, eps = sym(pg), sigma = 2 mu eps + lam tr(eps) I, flux = sigma J^-T dv
           double pg[3][3];
@@ -250,7 +253,12 @@ struct CellRegElast {
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) {
       const int g = __ldg(ib + l * CB);
-      if (g >= 0) atomicAdd(dst + (int64_t)g * 3 + w, kNeg ? -acc[l] : acc[l]);
+      if (g >= 0) {
+        if (cellout)  // deterministic mode: cell buffer [blk][l][comp][CB]
+          cellout[((blk * NLOC + l) * 3 + w) * CB + lane] = acc[l];
+        else
+          atomicAdd(dst + (int64_t)g * 3 + w, TV(kNeg ? -acc[l] : acc[l]));
+      }
     }
   }
 };

@@ -11,6 +11,12 @@
 namespace nnmg {
 
 // ---------------------------------------------------------------------------
+template <bool NEG>
+__global__ void k_cell_gather(const int* __restrict__ off, const int* __restrict__ ent,
+                              const double* __restrict__ cellout, int64_t nsc, int ncomp, int cb,
+                              double* __restrict__ dst);
+
+// ---------------------------------------------------------------------------
 // K4: per-quadrature-point geometry (mfoperator.py:28-48, 101-106, 163-169)
 // J[a][b] = sum_v dW_v/dxhat_b(q) X_v[a]   (mesh.py:138-143)
 // ---------------------------------------------------------------------------
@@ -104,17 +110,17 @@ using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PH
 #ifndef NNMG_APPLY_MINB_GEOS
 #define NNMG_APPLY_MINB_GEOS 3
 #endif
-template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, int GEO = 0, int MINB = 0>
+template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, int GEO = 0, int MINB = 0, class TV = double>
 __global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHREADS,
                                   MINB > 0 ? MINB
                                            : (SPLIT == 1 ? 1 : (GEO == 1 ? NNMG_APPLY_MINB_GEOS : NNMG_APPLY_MINB)))
-    k_apply(Tables tab, const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ idx,
-            const double* __restrict__ geo, int64_t b0, double lam, double mu) {
+    k_apply(Tables tab, const TV* __restrict__ src, TV* __restrict__ dst, const int* __restrict__ idx,
+            const double* __restrict__ geo, int64_t b0, double lam, double mu, double* __restrict__ cellout) {
   extern __shared__ double sm[];
   using CK = ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>;
-  CK::template run<false, NEG, GEO>(tab, PlainSrc{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm,
+  CK::template run<false, NEG, GEO>(tab, PlainSrcT<TV>{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm,
                                      threadIdx.x, [] __device__() { __syncthreads(); },
-                                     int(blockIdx.x % SPLIT) * CK::SCB);
+                                     int(blockIdx.x % SPLIT) * CK::SCB, cellout);
 }
 
 // ---------------------------------------------------------------------------
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHRE
 // ---------------------------------------------------------------------------
 template <int DIM, int P, int NCOMP, int PHYS>
 __global__ void k_diagonal(Tables tab, const int* __restrict__ idx, const double* __restrict__ geo, int64_t nblk,
-                           double lam, double mu, double* __restrict__ diag) {
+                           double lam, double mu, double* __restrict__ diag, double* __restrict__ cellout) {
   using CK = CellKernel<DIM, P, NCOMP, PHYS>;
   constexpr int N1 = CK::N1, NLOC = CK::NLOC, CB = CK::CB, NG = CK::NG;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -170,14 +176,19 @@ __global__ void k_diagonal(Tables tab, const int* __restrict__ idx, const double
       for (int a = 0; a < NCOMP; ++a) acc[a] += dv * ((lam + mu) * pg[a] * pg[a] + mu * n2);
     }
   }
-  for (int a = 0; a < NCOMP; ++a) atomicAdd(diag + (int64_t)g * NCOMP + a, acc[a]);
+  for (int a = 0; a < NCOMP; ++a) {
+    if (cellout)  // deterministic mode: summed by k_cell_gather in a fixed order
+      cellout[((blk * NLOC + l) * NCOMP + a) * CB + lane] = acc[a];
+    else
+      atomicAdd(diag + (int64_t)g * NCOMP + a, acc[a]);
+  }
 }
 
 // body load: thread per (cell, local DoF), b_l = sum_q det(J(q)) w_q prod_k S[q_k][l_k]
 template <int DIM>
 __global__ void k_load_vector(const double* __restrict__ verts, const int* __restrict__ cells, int64_t n_cells,
                               int n1, int cb, const int* __restrict__ idx, Tables tab, int ncomp, double f0,
-                              double f1, double f2, double* __restrict__ b) {
+                              double f1, double f2, double* __restrict__ b, double* __restrict__ cellout) {
   constexpr int NV = 1 << DIM;
   const int nloc = DIM == 2 ? n1 * n1 : n1 * n1 * n1;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -217,8 +228,12 @@ __global__ void k_load_vector(const double* __restrict__ verts, const int* __res
     acc += det * wq * phi;
   }
   const double f[3] = {f0, f1, f2};
-  for (int a = 0; a < ncomp; ++a)
-    if (f[a] != 0.0) atomicAdd(b + (int64_t)g * ncomp + a, f[a] * acc);
+  for (int a = 0; a < ncomp; ++a) {
+    if (cellout)  // deterministic mode
+      cellout[(((c / cb) * nloc + l) * ncomp + a) * cb + c % cb] = f[a] * acc;
+    else if (f[a] != 0.0)
+      atomicAdd(b + (int64_t)g * ncomp + a, f[a] * acc);
+  }
 }
 
 __global__ void k_copy_constrained(const int* __restrict__ cd, int64_t n, const double* __restrict__ src,
@@ -411,9 +426,9 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
 // fused into the cell kernels' prologue: the residual form (NEG) subtracts
 // src there, the plain form copies it; cell threads never scatter to these
 // rows, so there is no ordering between the two.
-template <bool NEG>
+template <bool NEG, class TV>
 __device__ __forceinline__ void constrained_rows(const int* __restrict__ cd, int64_t ncd,
-                                                 const double* __restrict__ src, double* __restrict__ dst) {
+                                                 const TV* __restrict__ src, TV* __restrict__ dst) {
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncd; i += nthr) {
     const int c = cd[i];
@@ -435,22 +450,24 @@ __device__ __forceinline__ void constrained_rows(const int* __restrict__ cd, int
 // hybrids 0.67-0.74 ms (1/4 .. 3/4 of the blocks recomputing).  Blocks with
 // blk % rmod < rnum take the recompute path.  HYB is an opt-in instantiation
 // (NNMG_RECOMPUTE_MOD / NNMG_RECOMPUTE_NUM) so the default kernel stays lean.
-template <int D, int P, int MINB, bool NEG, bool HYB>
-__global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const double* __restrict__ src, double* __restrict__ dst,
-                                                   const int* __restrict__ idx, const double* __restrict__ geo,
+template <int D, int P, int MINB, bool NEG, bool HYB, class TV = double, class TG = double>
+__global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* __restrict__ src, TV* __restrict__ dst,
+                                                   const int* __restrict__ idx, const TG* __restrict__ geo,
                                                    int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod,
-                                                   int rnum, const int* __restrict__ cd, int64_t ncd) {
+                                                   int rnum, const int* __restrict__ cd, int64_t ncd,
+                                                   double* __restrict__ cellout = nullptr) {
   if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= b1) return;
   if constexpr (HYB) {
     if (blk % rmod < rnum) {
-      CellReg<D, P>::template run<true, false, NEG, D == 3 ? 2 : 1>(tab, PlainSrc{src}, dst, idx, geo, blk,
+      CellReg<D, P>::template run<true, false, NEG, D == 3 ? 2 : 1>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk,
                                                                     threadIdx.x & 31, edges);
       return;
     }
   }
-  CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrc{src}, dst, idx, geo, blk, threadIdx.x & 31);
+  CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk, threadIdx.x & 31,
+                                                   nullptr, nullptr, cellout);
 }
 
 // stored G streamed through shared memory by TMA bulk copies (3D, GEO 3)
@@ -474,21 +491,23 @@ __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const doubl
                                                         int64_t b0, int64_t b1, const double* __restrict__ edges) {
   const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (blk >= b1) return;
-  CellReg<D, P>::template run<true, false, NEG, 2>(tab, PlainSrc{src}, dst, idx, nullptr, blk, threadIdx.x & 31,
+  CellReg<D, P>::template run<true, false, NEG, 2>(tab, PlainSrc{src}, dst, idx, static_cast<const double*>(nullptr),
+                                                   blk, threadIdx.x & 31,
                                                    edges);
 }
 
 // 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
-template <int P, bool NEG, int GEO = 0>
-__global__ void __launch_bounds__(96) k_apply_reg_elast(Tables tab, const double* __restrict__ src,
-                                                        double* __restrict__ dst, const int* __restrict__ idx,
-                                                        const double* __restrict__ geo, int64_t b0, int64_t b1,
-                                                        double lam, double mu, const int* __restrict__ cd, int64_t ncd) {
+template <int P, bool NEG, int GEO = 0, class TV = double, class TG = double>
+__global__ void __launch_bounds__(96) k_apply_reg_elast(Tables tab, const TV* __restrict__ src,
+                                                        TV* __restrict__ dst, const int* __restrict__ idx,
+                                                        const TG* __restrict__ geo, int64_t b0, int64_t b1,
+                                                        double lam, double mu, const int* __restrict__ cd, int64_t ncd,
+                                                        double* __restrict__ cellout = nullptr) {
   __shared__ double sm[CellRegElast<P>::SMEM_DOUBLES];
   if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x;
   if (blk >= b1) return;
-  CellRegElast<P>::template run<NEG, GEO>(tab, src, dst, idx, geo, blk, lam, mu, sm);
+  CellRegElast<P>::template run<NEG, GEO>(tab, src, dst, idx, geo, blk, lam, mu, sm, cellout);
 }
 
 // per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
@@ -511,24 +530,53 @@ __global__ void k_edges(const double* __restrict__ verts, const int* __restrict_
   }
 }
 
-struct ApplyLaunch {
+// TV = float: the mixed-precision V-cycle's apply (fp32 vectors and stored
+// geometry, fp64 arithmetic); only the residual form (neg) and the default
+// kernel variants are instantiated for it
+template <class TV>
+struct ApplyLaunchT {
+  static constexpr bool kF64 = sizeof(TV) == sizeof(double);
   const Level& L;
-  const double* src;
-  double* dst;
+  const TV* src;
+  TV* dst;
   int64_t b0, b1;
   cudaStream_t s;
   bool neg;
   const int* cd = nullptr;  // constrained rows to fuse into the cell kernel (nullptr: caller handles them)
+  double* cellout = nullptr;  // deterministic mode: cell buffer instead of atomics (fp64 only)
   int64_t ncd = 0;
   bool fused = false;       // set when the launched kernel handled them
   template <int D, int P, int NC, int PH>
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
-    if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported) {
+    if constexpr (!kF64) NNMG_REQUIRE(neg, kInvalidArgument, "fp32 apply is residual-form only");
+    if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported && !kF64) {
       if (L.reg_kernel) {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
+        k_apply_reg<D, P, 1, true, false, float, float><<<g, 32 * kWarpsPerCta, 0, s>>>(
+            L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, nullptr, 0, 1, cd, ncd);
+        fused = true;
+        NNMG_CHECK_LAUNCH();
+        count_launch();
+        return;
+      }
+    }
+    if constexpr (PH == kLaplace && NC == 1 && CellReg<D, P>::kSupported && kF64) {
+      if (L.reg_kernel) {
+        const int64_t nb = b1 - b0;
+        constexpr int kWarpsPerCta = 4;
+        const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
+        if (cellout) {
+          auto kd = neg ? k_apply_reg<D, P, 1, true, false> : k_apply_reg<D, P, 1, false, false>;
+          kd<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, nullptr, 0, 1, cd, ncd,
+                                              cellout);
+          fused = true;
+          NNMG_CHECK_LAUNCH();
+          count_launch();
+          return;
+        }
         if constexpr (D == 3) {
           if (L.reg_tma) {
             constexpr size_t smem = kWarpsPerCta * CellReg<D, P>::WARP_SMEM;
@@ -567,11 +615,21 @@ struct ApplyLaunch {
         return;
       }
     }
-    if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported) {
+    if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported && !kF64) {
+      if (L.reg_kernel) {
+        k_apply_reg_elast<P, true, 0, float, float><<<static_cast<unsigned>(b1 - b0), 96, 0, s>>>(
+            L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, L.lam, L.mu, cd, ncd);
+        fused = true;
+        NNMG_CHECK_LAUNCH();
+        count_launch();
+        return;
+      }
+    }
+    if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported && kF64) {
       if (L.reg_kernel) {
         const int64_t nb = b1 - b0;
         if constexpr (P == 2) {
-          if (L.edges.ptr && L.elast_recompute) {
+          if (L.edges.ptr && L.elast_recompute && !cellout) {
             auto kr = neg ? k_apply_reg_elast<P, true, 2> : k_apply_reg_elast<P, false, 2>;
             kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.edges.ptr, b0, b1, L.lam,
                                                          L.mu, nullptr, 0);
@@ -582,13 +640,22 @@ struct ApplyLaunch {
         }
         auto kr = neg ? k_apply_reg_elast<P, true> : k_apply_reg_elast<P, false>;
         kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.lam, L.mu, cd,
-                                                     ncd);
+                                                     ncd, cellout);
         fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();
         return;
       }
     }
+    if constexpr (!kF64) {
+      // fp32 vectors: one compile-time variant per element type, the default
+      // split (recomputed G for 3D Laplace Q3/Q4)
+      if constexpr (D == 3 && P >= 3 && PH == kLaplace) {
+        if (L.edges.ptr && L.apply_recompute) return launch<D, P, NC, PH, 8, 2>();
+      }
+      constexpr int SP = (D == 3 && P >= 4) ? 4 : (NC > 1 ? 2 : 1);
+      launch<D, P, NC, PH, SP>();
+    } else {
     if constexpr (D == 3 && P >= 3 && PH == kLaplace) {
       if (L.edges.ptr && L.apply_recompute) {
         if (L.apply_split == 8) return launch<D, P, NC, PH, 8, 2>();
@@ -597,7 +664,7 @@ struct ApplyLaunch {
         return launch<D, P, NC, PH, 1, 2>();
       }
     }
-    if constexpr (D == 3 && P >= 3 && CK::CB % 16 == 0) {
+    if constexpr (D == 3 && P >= 3 && CK::CB % 16 == 0 && kF64) {
       if (L.apply_geos) {
         if (L.apply_split == 8) return launch<D, P, NC, PH, 8, 1>();
         if (L.apply_split == 4) return launch<D, P, NC, PH, 4, 1>();
@@ -606,31 +673,36 @@ struct ApplyLaunch {
     if (L.apply_split == 4) return launch<D, P, NC, PH, 4>();
     if (L.apply_split == 2) return launch<D, P, NC, PH, 2>();
     launch<D, P, NC, PH, 1>();
+    }
   }
   template <int D, int P, int NC, int PH, int SPLIT, int GEO = 0, int MINB = 0>
   void launch() {
     using CK = ApplyKernel<D, P, NC, PH, SPLIT>;
     constexpr size_t kSmem = CK::SMEM + (GEO == 1 ? CK::GEO_SMEM : (GEO == 2 ? CK::EDGE_SMEM : 0));
-    auto kern = neg ? k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB> : k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB>;
+    // fp32 vectors: residual form only (no NEG=false instantiation)
+    auto kneg = k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB, TV>;
+    auto kpos = kneg;
+    if constexpr (kF64) kpos = k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB, TV>;
+    auto kern = neg ? kneg : kpos;
     const double* gsrc = GEO == 2 ? L.edges.ptr : L.geo.ptr;
     static bool attr = false;
     if (!attr) {
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-      NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(kneg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+      NNMG_CUDA_TRY(cudaFuncSetAttribute(kpos, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
       attr = true;
     }
     const int64_t nb = (b1 - b0) * SPLIT;
     constexpr int64_t kMaxGrid = (0x7fffffff / SPLIT) * SPLIT;
     for (int64_t off = 0; off < nb; off += kMaxGrid) {
       const unsigned g = static_cast<unsigned>(std::min<int64_t>(nb - off, kMaxGrid));
-      kern<<<g, CK::NTHREADS, kSmem, s>>>(L.tab, src, dst, L.idx.ptr, gsrc, b0 + off / SPLIT, L.lam, L.mu);
+      kern<<<g, CK::NTHREADS, kSmem, s>>>(L.tab, src, dst, L.idx.ptr, gsrc, b0 + off / SPLIT, L.lam, L.mu, cellout);
       NNMG_CHECK_LAUNCH();
       count_launch();
     }
   }
 };
+
+using ApplyLaunch = ApplyLaunchT<double>;
 
 void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t b0, int64_t b1, cudaStream_t s,
                         bool negate) {
@@ -640,9 +712,46 @@ void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t 
 }
 
 // all cells plus the constrained rows; returns false when the rows are left to the caller
-static bool launch_apply_all(const Level& L, const double* src, double* dst, cudaStream_t s, bool negate) {
+// deterministic mode, phase 2: per scalar DoF the sum of its cell-buffer
+// slots in ascending slot order (a fixed order: results are bitwise
+// reproducible); NEG: dst -= sum (residual form), else dst = sum
+template <bool NEG>
+__global__ void k_cell_gather(const int* __restrict__ off, const int* __restrict__ ent,
+                              const double* __restrict__ cellout, int64_t nsc, int ncomp, int cb,
+                              double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nsc * ncomp) return;
+  const int64_t g = i / ncomp;
+  const int c = static_cast<int>(i % ncomp);
+  const int e0 = off[g], e1 = off[g + 1];
+  if (e0 == e1) return;  // constrained: handled by the cell kernel's prologue
+  double sum = 0.0;
+  for (int e = e0; e < e1; ++e) sum += cellout[ent[e] + int64_t(c) * cb];
+  dst[i] = NEG ? dst[i] - sum : sum;
+}
+
+template <class TV>
+static bool launch_apply_all(const Level& L, const TV* src, TV* dst, cudaStream_t s, bool negate) {
   if (L.nblk <= 0) return false;
-  ApplyLaunch f{L, src, dst, 0, L.nblk, s, negate};
+  ApplyLaunchT<TV> f{L, src, dst, 0, L.nblk, s, negate};
+  if constexpr (sizeof(TV) == sizeof(double)) {
+    if (L.deterministic) {
+      f.cellout = L.cellout.ptr;
+      f.cd = L.cdofs.ptr;
+      f.ncd = static_cast<int64_t>(L.cdofs.n);
+      dispatch(L.dim, L.degree, L.ncomp, L.physics, f);
+      const int64_t nt = L.n_scalar * L.ncomp;
+      if (negate)
+        k_cell_gather<true><<<grid_for(nt, 256), 256, 0, s>>>(L.det_off.ptr, L.det_ent.ptr, L.cellout.ptr,
+                                                               L.n_scalar, L.ncomp, L.cb, dst);
+      else
+        k_cell_gather<false><<<grid_for(nt, 256), 256, 0, s>>>(L.det_off.ptr, L.det_ent.ptr, L.cellout.ptr,
+                                                                L.n_scalar, L.ncomp, L.cb, dst);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+      return f.fused && f.ncd == static_cast<int64_t>(L.cdofs.n);
+    }
+  }
   if (L.fuse_constrained) {
     f.cd = L.cdofs.ptr;
     f.ncd = static_cast<int64_t>(L.cdofs.n);
@@ -651,10 +760,45 @@ static bool launch_apply_all(const Level& L, const double* src, double* dst, cud
   return f.fused && f.ncd == static_cast<int64_t>(L.cdofs.n);
 }
 
-__global__ void k_sub_constrained(const int* __restrict__ cd, int64_t n, const double* __restrict__ src,
-                                  double* __restrict__ dst) {
+template <class TV>
+__global__ void k_sub_constrained(const int* __restrict__ cd, int64_t n, const TV* __restrict__ src,
+                                  TV* __restrict__ dst) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) dst[cd[i]] -= src[cd[i]];
+}
+
+// fp32 residual-form apply of the mixed-precision V-cycle: dst -= A src with
+// fp32 vectors and stored geometry (level_enable_f32), fp64 arithmetic
+void level_apply_sub_f32(Level& L, const float* src, float* dst, cudaStream_t s) {
+  NNMG_REQUIRE(L.f32_ready, kInvalidArgument, "level fp32 data not prepared");
+  NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
+  const bool fused = launch_apply_all(L, src, dst, s, true);
+  const int64_t n = static_cast<int64_t>(L.cdofs.n);
+  if (n && !fused) {
+    k_sub_constrained<float><<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+  }
+}
+
+__global__ void k_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = float(a[i]);
+}
+
+void level_enable_f32(Level& L, cudaStream_t s) {
+  if (L.f32_ready) return;
+  NNMG_REQUIRE(L.diag_ready, kInvalidArgument, "level diagonal not computed");
+  L.geo32.alloc(L.geo.n);
+  L.inv_diag32.alloc(L.inv_diag.n);
+  if (L.geo.n) k_to_f32<<<grid_for(int64_t(L.geo.n), 256), 256, 0, s>>>(L.geo.ptr, L.geo32.ptr, int64_t(L.geo.n));
+  NNMG_CHECK_LAUNCH();
+  if (L.inv_diag.n)
+    k_to_f32<<<grid_for(int64_t(L.inv_diag.n), 256), 256, 0, s>>>(L.inv_diag.ptr, L.inv_diag32.ptr,
+                                                                   int64_t(L.inv_diag.n));
+  NNMG_CHECK_LAUNCH();
+  count_launch(2);
+  L.f32_ready = true;
 }
 
 void level_apply_sub(Level& L, const double* src, double* dst, cudaStream_t s) {
@@ -662,7 +806,7 @@ void level_apply_sub(Level& L, const double* src, double* dst, cudaStream_t s) {
   const bool fused = launch_apply_all(L, src, dst, s, true);
   const int64_t n = static_cast<int64_t>(L.cdofs.n);
   if (n && !fused) {
-    k_sub_constrained<<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
+    k_sub_constrained<double><<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
     NNMG_CHECK_LAUNCH();
     count_launch();
   }
@@ -680,14 +824,22 @@ void level_load_vector(Level& L, const double* f, double* b, cudaStream_t s) {
   NNMG_CUDA_TRY(cudaMemsetAsync(b, 0, sizeof(double) * L.n_dofs, s));
   const double f0 = f[0], f1 = L.ncomp > 1 ? f[1] : 0.0, f2 = L.ncomp > 2 ? f[2] : 0.0;
   const int64_t nt = L.n_cells * L.nloc;
+  double* co = L.deterministic ? L.cellout.ptr : nullptr;
   if (L.dim == 2)
     k_load_vector<2><<<grid_for(nt, 128), 128, 0, s>>>(L.verts.ptr, L.vcells.ptr, L.n_cells, L.n1, L.cb, L.idx.ptr,
-                                                      L.tab, L.ncomp, f0, f1, f2, b);
+                                                      L.tab, L.ncomp, f0, f1, f2, b, co);
   else
     k_load_vector<3><<<grid_for(nt, 128), 128, 0, s>>>(L.verts.ptr, L.vcells.ptr, L.n_cells, L.n1, L.cb, L.idx.ptr,
-                                                      L.tab, L.ncomp, f0, f1, f2, b);
+                                                      L.tab, L.ncomp, f0, f1, f2, b, co);
   NNMG_CHECK_LAUNCH();
   count_launch();
+  if (co) {
+    const int64_t n = L.n_scalar * L.ncomp;
+    k_cell_gather<false><<<grid_for(n, 256), 256, 0, s>>>(L.det_off.ptr, L.det_ent.ptr, co, L.n_scalar, L.ncomp,
+                                                           L.cb, b);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+  }
 }
 
 void level_apply(Level& L, const double* src, double* dst, cudaStream_t s) {
@@ -703,12 +855,60 @@ struct DiagLaunch {
   void operator()() {
     using CK = CellKernel<D, P, NC, PH>;
     const int64_t nt = L.nblk * CK::NLOC * CK::CB;
+    double* co = L.deterministic ? L.cellout.ptr : nullptr;
     k_diagonal<D, P, NC, PH><<<grid_for(nt, 128), 128, 0, s>>>(L.tab, L.idx.ptr, L.geo.ptr, L.nblk, L.lam, L.mu,
-                                                                L.diag.ptr);
+                                                                L.diag.ptr, co);
     NNMG_CHECK_LAUNCH();
     count_launch();
+    if (co) {
+      const int64_t n = L.n_scalar * L.ncomp;
+      k_cell_gather<false><<<grid_for(n, 256), 256, 0, s>>>(L.det_off.ptr, L.det_ent.ptr, co, L.n_scalar, L.ncomp,
+                                                             L.cb, L.diag.ptr);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+    }
   }
 };
+
+// deterministic mode (SURVEY §7 hard part 1, mfoperator.py:88-90): the apply,
+// diagonal and load-vector kernels write per-cell results to a cell buffer in
+// the idx layout and k_cell_gather sums each DoF's slots in a fixed order;
+// bitwise reproducible, at the cost of the buffer round trip
+// (8 B x NLOC x NCOMP per cell written + read, 4 B per slot of index)
+void level_set_deterministic(Level& L, bool on) {
+  if (!on) {
+    L.deterministic = false;
+    L.cellout.release();
+    L.det_off.release();
+    L.det_ent.release();
+    return;
+  }
+  if (L.deterministic) return;
+  const int nloc = L.nloc, cb = L.cb, nc = L.ncomp;
+  const int64_t nslot = L.nblk * nloc * nc * cb;
+  NNMG_REQUIRE(nslot < (int64_t(1) << 31), kUnsupported, "level too large for the deterministic cell buffer");
+  std::vector<int> off(L.n_scalar + 1, 0);
+  for (int64_t c = 0; c < L.n_cells; ++c)
+    for (int l = 0; l < nloc; ++l) {
+      const int g = L.cell_dofs_host[c * nloc + l];
+      if (!L.scalar_constrained[g]) off[g + 1] += 1;
+    }
+  for (int64_t g = 0; g < L.n_scalar; ++g) off[g + 1] += off[g];
+  std::vector<int> ent(off[L.n_scalar]);
+  std::vector<int> pos(off.begin(), off.end() - 1);
+  for (int64_t c = 0; c < L.n_cells; ++c) {
+    const int64_t blk = c / cb, lane = c % cb;
+    for (int l = 0; l < nloc; ++l) {
+      const int g = L.cell_dofs_host[c * nloc + l];
+      if (!L.scalar_constrained[g]) ent[pos[g]++] = static_cast<int>((blk * nloc + l) * nc * cb + lane);
+    }
+  }
+  L.det_off.upload(off);
+  L.det_ent.upload(ent);
+  L.cellout.alloc(size_t(nslot));
+  L.cellout.zero();
+  L.deterministic = true;
+}
 
 void level_compute_diagonal(Level& L, cudaStream_t s) {
   L.diag.zero(s);

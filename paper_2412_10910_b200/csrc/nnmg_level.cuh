@@ -34,6 +34,15 @@ struct Level {
   int recompute_mod = 0;   // hybrid geometry: blocks with blk % mod < num recompute G (0 = off)
   int recompute_num = 1;
   DevBuf<double> edges;    // [nblk][d*2^(d-1)*d][cb] cell edge vectors (hybrid geometry)
+  // mixed-precision V-cycle (level_enable_f32): fp32 copies of the stored
+  // geometry and of the inverse diagonal
+  DevBuf<float> geo32, inv_diag32;
+  bool f32_ready = false;
+  // deterministic mode (level_set_deterministic): cell buffer [nblk][nloc][ncomp][cb]
+  // and, per scalar DoF, its slots in a fixed order (CSR)
+  bool deterministic = false;
+  DevBuf<double> cellout;
+  DevBuf<int> det_off, det_ent;
   std::vector<int> cell_dofs_host;  // plain (nc, nloc) copy for transfer setup
   std::vector<uint8_t> scalar_constrained;  // per scalar DoF
 };
@@ -58,5 +67,12 @@ void launch_apply_cells(const Level& L, const double* src, double* dst, int64_t 
 // dst -= A src (constrained rows: dst[c] -= src[c]); no zeroing pass
 void level_apply_sub(Level& L, const double* src, double* dst, cudaStream_t s);
 void launch_copy_constrained(const Level& L, const double* src, double* dst, cudaStream_t s);
+// mixed-precision V-cycle: fp32 copies of geometry / inverse diagonal, and the
+// residual-form apply on fp32 vectors (fp64 arithmetic)
+void level_enable_f32(Level& L, cudaStream_t s);
+// fixed-order (atomic-free) summation of cell contributions in apply /
+// diagonal / load vector: bitwise reproducible results
+void level_set_deterministic(Level& L, bool on);
+void level_apply_sub_f32(Level& L, const float* src, float* dst, cudaStream_t s);
 
 }  // namespace nnmg

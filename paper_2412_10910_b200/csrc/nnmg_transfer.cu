@@ -15,10 +15,14 @@ static inline unsigned grid_for(int64_t n, int bs) { return static_cast<unsigned
 static constexpr int kWarps = kTransferWarps;
 
 // ---------------------------------------------------------------------------
-struct TransferDispatch {
+// TV = float: the mixed-precision V-cycle's transfers (fp32 vectors and xhat,
+// fp64 arithmetic); only the default kernel variants are instantiated for it
+template <class TV>
+struct TransferDispatchT {
+  static constexpr bool kF64 = sizeof(TV) == sizeof(double);
   Transfer& T;
-  const double* in;
-  double* out;
+  const TV* in;
+  TV* out;
   int mode;  // 0 prolongate, 1 prolongate-accumulate, 2 restrict
   cudaStream_t s;
   template <int D, int P, int NC, int PH>
@@ -26,53 +30,64 @@ struct TransferDispatch {
     constexpr int CBC = cells_per_block<D, P, NC>();
     const Level& C = *T.coarse;
     const unsigned g = grid_for(T.nitems, kWarps);
+    const TV* const xh = [&] {
+      if constexpr (kF64)
+        return T.xhat.ptr;
+      else
+        return T.xhat32.ptr;
+    }();
     if (mode < 2) {
       constexpr int PPL = prolongate_ppl<D, P, NC>();
-      auto kp = (T.prolong_ppl == 2 && PPL == 1) ? k_prolongate<D, P, NC, CBC, 2> : k_prolongate<D, P, NC, CBC, PPL>;
+      auto kp = k_prolongate<D, P, NC, CBC, PPL, TV, TV>;
+      if constexpr (kF64 && PPL == 1)
+        if (T.prolong_ppl == 2) kp = k_prolongate<D, P, NC, CBC, 2>;
       kp<<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.nitems == T.ncc ? nullptr : T.item_cell.ptr,
-                                   T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems);
+                                   T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems);
       NNMG_CHECK_LAUNCH();
       count_launch();
     } else {
       const int ch = T.chunk;
       const int64_t nwarps = (T.nitems + ch - 1) / ch;
+      constexpr int W = StagedRestrict<D, P, NC>::WARPS;
       if constexpr (ipow(P + 1, D) * NC <= 32) {
         // default: 3 points per lane and round in 3D (C3 0.176 -> 0.173 ms), 2 in 2D
         // (C2 0.022 vs 0.025 ms with 3); 4 points measured slower in both
         const int rk = T.restrict_kernel >= 0 ? T.restrict_kernel : (D == 3 ? 3 : 1);
-        if (rk != 2) {
+        if constexpr (!kF64) {
+          (D == 3 ? k_restrict_lane<D, P, NC, 3, TV, TV> : k_restrict_lane<D, P, NC, 1, TV, TV>)
+              <<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems,
+                                                                 ch, T.cellbuf.ptr);
+        } else if (rk != 2) {
           auto k = rk == 0 ? k_restrict_lane<D, P, NC, 1>
                    : rk == 3 ? k_restrict_lane<D, P, NC, 3>
                              : k_restrict_lane<D, P, NC, 2>;
-          k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr,
+          k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh,
                                                             T.nitems, ch, T.cellbuf.ptr);
         } else {
-          constexpr int W = StagedRestrict<D, P, NC>::WARPS;
           k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
-              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         }
-      } else if constexpr (ipow(P + 1, D) * NC <= 81) {
+      } else if constexpr (ipow(P + 1, D) * NC <= 81 && kF64) {
         if (T.restrict_wide) {
           k_restrict_lane<D, P, NC, 1><<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(
-              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         } else {
-          constexpr int W = StagedRestrict<D, P, NC>::WARPS;
           k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
-              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         }
       } else {
-        constexpr int W = StagedRestrict<D, P, NC>::WARPS;
-        k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
-            C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, T.xhat.ptr, T.nitems, ch, T.cellbuf.ptr);
+        k_restrict_staged<D, P, NC, TV, TV><<<grid_for(nwarps, W), W * 32, 0, s>>>(
+            C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
       }
       NNMG_CHECK_LAUNCH();
-      k_restrict_gather<<<grid_for(C.n_scalar, 256), 256, 0, s>>>(T.t_off.ptr, T.t_ent.ptr, T.cellbuf.ptr,
-                                                                   C.n_scalar, NC, out);
+      k_restrict_gather<TV><<<grid_for(C.n_scalar, 256), 256, 0, s>>>(T.t_off.ptr, T.t_ent.ptr, T.cellbuf.ptr,
+                                                                       C.n_scalar, NC, out);
       NNMG_CHECK_LAUNCH();
       count_launch(2);
     }
   }
 };
+using TransferDispatch = TransferDispatchT<double>;
 
 Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_t* point_dofs, const int64_t* cells,
                           const double* xhat) {
@@ -193,22 +208,53 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
   return T;
 }
 
-void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s) {
+template <class TV>
+static void prolongate_t(Transfer& T, const TV* uc, TV* uf, bool accumulate, cudaStream_t s) {
   if (!accumulate) {
     // every point DoF is written below; only the point-less ones need zeros
     const int64_t n = int64_t(T.no_point.n) * T.ncomp;
     if (n) {
-      k_zero_list<<<grid_for(n, 256), 256, 0, s>>>(T.no_point.ptr, int64_t(T.no_point.n), T.ncomp, uf);
+      k_zero_list<TV><<<grid_for(n, 256), 256, 0, s>>>(T.no_point.ptr, int64_t(T.no_point.n), T.ncomp, uf);
       NNMG_CHECK_LAUNCH();
       count_launch();
     }
   }
-  TransferDispatch f{T, uc, uf, accumulate ? 1 : 0, s};
+  TransferDispatchT<TV> f{T, uc, uf, accumulate ? 1 : 0, s};
   dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
+}
+
+void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s) {
+  prolongate_t(T, uc, uf, accumulate, s);
 }
 
 void transfer_restrict(Transfer& T, const double* rf, double* rc, cudaStream_t s) {
   TransferDispatch f{T, rf, rc, 2, s};
+  dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
+}
+
+__global__ void k_xhat_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = float(a[i]);
+}
+
+void transfer_enable_f32(Transfer& T, cudaStream_t s) {
+  if (T.xhat32.n == T.xhat.n && T.xhat32.ptr) return;
+  T.xhat32.alloc(T.xhat.n);
+  if (T.xhat.n) {
+    k_xhat_f32<<<grid_for(int64_t(T.xhat.n), 256), 256, 0, s>>>(T.xhat.ptr, T.xhat32.ptr, int64_t(T.xhat.n));
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+  }
+}
+
+void transfer_prolongate_f32(Transfer& T, const float* uc, float* uf, bool accumulate, cudaStream_t s) {
+  NNMG_REQUIRE(T.xhat32.n == T.xhat.n, kInvalidArgument, "transfer fp32 records not prepared");
+  prolongate_t(T, uc, uf, accumulate, s);
+}
+
+void transfer_restrict_f32(Transfer& T, const float* rf, float* rc, cudaStream_t s) {
+  NNMG_REQUIRE(T.xhat32.n == T.xhat.n, kInvalidArgument, "transfer fp32 records not prepared");
+  TransferDispatchT<float> f{T, rf, rc, 2, s};
   dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
 }
 

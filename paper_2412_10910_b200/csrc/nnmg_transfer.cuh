@@ -22,6 +22,7 @@ struct Transfer {
   DevBuf<int> item_cell;    // [nitems] owning coarse cell of each item
   DevBuf<int> pt_dof;       // [npts] fine scalar DoF (sorted by cell, then point order)
   DevBuf<double> xhat;      // [npts][dim]
+  DevBuf<float> xhat32;     // fp32 copy for the mixed-precision V-cycle (transfer_enable_f32)
   DevBuf<double> cellbuf;   // [nitems][nloc][ncomp] restriction partial local vectors
   DevBuf<int> t_off, t_ent; // coarse DoF -> (cell*nloc + l) entries, fixed order
   DevBuf<int> no_point;     // fine scalar DoFs without a point (zero in P u_c)
@@ -33,6 +34,10 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
 void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s);
 // r_c = P^T r_f, deterministic two-phase segmented reduction (transfer.py:46-58, 104-124)
 void transfer_restrict(Transfer& T, const double* rf, double* rc, cudaStream_t s);
+// mixed-precision V-cycle: fp32 xhat copy, fp32 vectors (fp64 arithmetic)
+void transfer_enable_f32(Transfer& T, cudaStream_t s);
+void transfer_prolongate_f32(Transfer& T, const float* uc, float* uf, bool accumulate, cudaStream_t s);
+void transfer_restrict_f32(Transfer& T, const float* rf, float* rc, cudaStream_t s);
 
 struct LocateResult {
   int n_missing = 0;       // points with no candidate / no converged candidate

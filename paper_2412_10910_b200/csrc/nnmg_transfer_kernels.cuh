@@ -106,11 +106,13 @@ __host__ __device__ constexpr int prolongate_ppl() {
   return 2;
 }
 
-template <int DIM, int PC, int NCOMP, int CBC, int PPL>
+// TV / TX: storage types of the vectors and of xhat (double, or float in the
+// mixed-precision V-cycle); the arithmetic is fp64
+template <int DIM, int PC, int NCOMP, int CBC, int PPL, class TV = double, class TX = double>
 __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NCOMP > 1) ? 4 : 6)
-    k_prolongate(Tables tab, const double* __restrict__ uc, double* __restrict__ uf, int accumulate,
+    k_prolongate(Tables tab, const TV* __restrict__ uc, TV* __restrict__ uf, int accumulate,
                  const int* __restrict__ cidx, const int* __restrict__ item_cell, const int* __restrict__ item_pt,
-                 const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t nitems) {
+                 const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t nitems) {
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
   __shared__ double su[kTransferWarps][NCOMP * NLOC];
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
       const bool ok = p < p1;
       dd[k] = ok ? __ldcs(pt_dof + p) : -1;
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) xt[k][j] = ok ? __ldcs(xhat + (int64_t)p * DIM + j) : 0.5;
+      for (int j = 0; j < DIM; ++j) xt[k][j] = ok ? double(__ldcs(xhat + (int64_t)p * DIM + j)) : 0.5;
     }
   };
   load(p0);
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
     const int g = cidx[(blk * NLOC + l) * CBC + cl];
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c)
-      su[warp][c * NLOC + l] = g >= 0 ? uc[(int64_t)g * NCOMP + c] * lagrange_norm<DIM, N1>(tab, l) : 0.0;
+      su[warp][c * NLOC + l] = g >= 0 ? double(uc[(int64_t)g * NCOMP + c]) * lagrange_norm<DIM, N1>(tab, l) : 0.0;
   }
   __syncwarp();
   for (int base = p0; base < p1; base += STEP) {
@@ -160,8 +162,8 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
       for (int k = 0; k < PPL; ++k) {
         const double a = contract<DIM, N1>(U, X[k]);
         if (cd[k] >= 0) {
-          double* o = uf + (int64_t)cd[k] * NCOMP + c;
-          *o = accumulate ? *o + a : a;
+          TV* o = uf + (int64_t)cd[k] * NCOMP + c;
+          *o = TV(accumulate ? double(*o) + a : a);
         }
       }
     }
@@ -170,9 +172,10 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
 
 // zero the fine DoFs that carry no transfer point (constrained): the
 // non-accumulating prolongation writes every other entry
-__global__ void k_zero_list(const int* __restrict__ list, int64_t n, int ncomp, double* __restrict__ uf) {
+template <class TV>
+__global__ void k_zero_list(const int* __restrict__ list, int64_t n, int ncomp, TV* __restrict__ uf) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n * ncomp) uf[(int64_t)list[i / ncomp] * ncomp + i % ncomp] = 0.0;
+  if (i < n * ncomp) uf[(int64_t)list[i / ncomp] * ncomp + i % ncomp] = TV(0);
 }
 
 // ---------------------------------------------------------------------------
@@ -228,7 +231,8 @@ template <int DIM, int NCOMP, int PPR>
 struct PointRec {
   int d[PPR];
   double x[PPR][DIM];
-  __device__ __forceinline__ void load(const int* __restrict__ pt_dof, const double* __restrict__ xhat, int base,
+  template <class TX>
+  __device__ __forceinline__ void load(const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int base,
                                        int end, int stride, int off, bool live) {
 #pragma unroll
     for (int k = 0; k < PPR; ++k) {
@@ -236,23 +240,24 @@ struct PointRec {
       const bool ok = live && p < end;
       d[k] = ok ? __ldcs(pt_dof + p) : -1;
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) x[k][j] = ok ? __ldcs(xhat + (int64_t)p * DIM + j) : 0.5;
+      for (int j = 0; j < DIM; ++j) x[k][j] = ok ? double(__ldcs(xhat + (int64_t)p * DIM + j)) : 0.5;
     }
   }
-  __device__ __forceinline__ void values(const double* __restrict__ rf, double (&v)[PPR][NCOMP]) const {
+  template <class TV>
+  __device__ __forceinline__ void values(const TV* __restrict__ rf, double (&v)[PPR][NCOMP]) const {
 #pragma unroll
     for (int k = 0; k < PPR; ++k)
 #pragma unroll
-      for (int c = 0; c < NCOMP; ++c) v[k][c] = d[k] >= 0 ? rf[(int64_t)d[k] * NCOMP + c] : 0.0;
+      for (int c = 0; c < NCOMP; ++c) v[k][c] = d[k] >= 0 ? double(rf[(int64_t)d[k] * NCOMP + c]) : 0.0;
   }
 };
 
 // The pipelined round loop shared by the restriction kernels.  body(rec_x, v)
 // evaluates the current round; flush(ci) is called after the last round of
 // chunk cell ci.
-template <int DIM, int NCOMP, int PPR, class Body, class Flush>
+template <int DIM, int NCOMP, int PPR, class TX, class TV, class Body, class Flush>
 __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __restrict__ pt_dof,
-                                              const double* __restrict__ xhat, const double* __restrict__ rf,
+                                              const TX* __restrict__ xhat, const TV* __restrict__ rf,
                                               int stride, int off, bool live, Body&& body, Flush&& flush) {
   constexpr int RS_K = PPR;
   const int rs = RS_K * stride;
@@ -289,10 +294,10 @@ __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __
 // 32: Q1/Q2 scalar, 2D vector; up to 81 with NNMG_RESTRICT_WIDE: 3D Q2
 // elasticity, Q3 scalar); a cell's lanes are combined through shared memory
 // at the cell end, 32 outputs at a time, lane l ending with output l of a tile.
-template <int DIM, int PC, int NCOMP, int PPR>
+template <int DIM, int PC, int NCOMP, int PPR, class TV = double, class TX = double>
 __global__ void __launch_bounds__(kTransferWarps * 32)
-    k_restrict_lane(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
-                    const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc, int chunk,
+    k_restrict_lane(Tables tab, const TV* __restrict__ rf, const int* __restrict__ cell_start,
+                    const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t ncc, int chunk,
                     double* __restrict__ cellbuf) {
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
@@ -409,10 +414,10 @@ struct StagedRestrict {
                                    : ((48 * 1024) / (WARP_DOUBLES * 8) >= 1 ? (48 * 1024) / (WARP_DOUBLES * 8) : 1);
 };
 
-template <int DIM, int PC, int NCOMP>
+template <int DIM, int PC, int NCOMP, class TV = double, class TX = double>
 __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
-    k_restrict_staged(Tables tab, const double* __restrict__ rf, const int* __restrict__ cell_start,
-                      const int* __restrict__ pt_dof, const double* __restrict__ xhat, int64_t ncc, int chunk,
+    k_restrict_staged(Tables tab, const TV* __restrict__ rf, const int* __restrict__ cell_start,
+                      const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t ncc, int chunk,
                       double* __restrict__ cellbuf) {
   using K = StagedRestrict<DIM, PC, NCOMP>;
   constexpr int N1 = K::N1, G = K::G, SLOTS = K::SLOTS, SUB = K::SUB, P = K::P, INNER = K::INNER,
@@ -514,15 +519,16 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
 }
 
 // K7 phase 2: r_c[g] = sum over the (cell, l) slots holding g, fixed order
+template <class TV>
 __global__ void k_restrict_gather(const int* __restrict__ t_off, const int* __restrict__ t_ent,
-                                  const double* __restrict__ cellbuf, int64_t nsc, int ncomp, double* __restrict__ rc) {
+                                  const double* __restrict__ cellbuf, int64_t nsc, int ncomp, TV* __restrict__ rc) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= nsc) return;
   const int e0 = t_off[g], e1 = t_off[g + 1];
   for (int c = 0; c < ncomp; ++c) {
     double s = 0.0;
     for (int e = e0; e < e1; ++e) s += cellbuf[(int64_t)t_ent[e] * ncomp + c];
-    rc[g * ncomp + c] = s;
+    rc[g * ncomp + c] = TV(s);
   }
 }
 

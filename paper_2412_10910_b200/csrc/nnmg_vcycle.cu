@@ -44,6 +44,36 @@ void smoother_sweep(Level& L, double lam_max, double lam_min, int degree, const 
   if (residual_out) level_apply_sub(L, d, r, s);
 }
 
+// the same sweep on fp32 vectors (mixed-precision V-cycle, fp64 arithmetic)
+static void smoother_sweep_f32(Level& L, double lam_max, double lam_min, int degree, const float* b, const float* x0,
+                               float* x, float* work, cudaStream_t s, bool residual_out, const float* t) {
+  const int64_t n = L.n_dofs;
+  float* r = work;
+  float* d = work + n;
+  const float* idg = L.inv_diag32.ptr;
+  const double theta = (lam_max + lam_min) / 2.0;
+  const double delta = (lam_max - lam_min) / 2.0;
+  const double sigma = theta / delta;
+  if (t != nullptr) {
+    level_apply_sub_f32(L, t, r, s);
+    cheb_init_add(n, t, idg, theta, r, d, x, s);
+  } else if (x0 == nullptr) {
+    cheb_init(n, b, static_cast<const float*>(nullptr), idg, theta, r, d, degree > 1 ? nullptr : x, s);
+  } else {
+    NNMG_CUDA_TRY(cudaMemcpyAsync(r, b, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+    level_apply_sub_f32(L, x0, r, s);
+    cheb_init(n, b, x0, idg, theta, r, d, x, s);
+  }
+  double rho_old = 1.0 / sigma;
+  for (int k = 0; k < degree - 1; ++k) {
+    level_apply_sub_f32(L, d, r, s);
+    const double rho = 1.0 / (2.0 * sigma - rho_old);
+    cheb_update(n, idg, rho * rho_old, 2.0 * rho / delta, r, d, x, s, k == 0 && x0 == nullptr && t == nullptr);
+    rho_old = rho;
+  }
+  if (residual_out) level_apply_sub_f32(L, d, r, s);
+}
+
 VCycle::~VCycle() {
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
 }
@@ -130,10 +160,87 @@ static void cycle(VCycle& V, int l, const double* f, double* x, cudaStream_t s) 
   }
 }
 
-void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s) {
+// mixed-precision cycle (the paper's fp32 V-cycle inside fp64 CG,
+// PAPER.md:392): fp32 vectors, geometry and transfer records on every level
+// above the coarsest; the coarse solve stays fp64 (converted in and out)
+static void cycle32(VCycle& V, int l, const float* f, float* x, cudaStream_t s) {
+  if (l == 0) {
+    const int64_t n0 = V.levels[0]->n_dofs;
+    convert(n0, f, V.cf.ptr, s);
+    coarse_solve(*V.coarse, V.cf.ptr, V.cx.ptr, s);
+    convert(n0, V.cx.ptr, x, s);
+    return;
+  }
+  Level& L = *V.levels[l];
+  Transfer& T = *V.transfers[l - 1];
+  float* w = V.work32[l].ptr;
+  // residual from the smoother recurrence, post-smoothing from that residual
+  for (int k = 0; k < V.m1; ++k)
+    smoother_sweep_f32(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, k == 0 ? nullptr : x, x, w, s,
+                       k == V.m1 - 1, nullptr);
+  float* r = w;
+  if (V.m1 == 0) {
+    NNMG_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(float) * L.n_dofs, s));
+    NNMG_CUDA_TRY(cudaMemcpyAsync(r, f, sizeof(float) * L.n_dofs, cudaMemcpyDeviceToDevice, s));
+  }
+  transfer_restrict_f32(T, r, V.f32[l - 1].ptr, s);
+  cycle32(V, l - 1, V.f32[l - 1].ptr, V.x32[l - 1].ptr, s);
+  if (V.m2 > 0) {
+    float* t = V.r32[l].ptr;
+    transfer_prolongate_f32(T, V.x32[l - 1].ptr, t, false, s);
+    smoother_sweep_f32(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s, false, t);
+    for (int k = 1; k < V.m2; ++k)
+      smoother_sweep_f32(L, V.lam_max[l], V.lam_min[l], V.degree[l], f, x, x, w, s, false, nullptr);
+  } else {
+    transfer_prolongate_f32(T, V.x32[l - 1].ptr, x, true, s);
+  }
+}
+
+static void run_cycle(VCycle& V, const double* f, double* x, cudaStream_t s) {
   const int top = static_cast<int>(V.levels.size()) - 1;
-  if (!V.use_graph) {
+  if (!V.mixed || top == 0) {
     cycle(V, top, f, x, s);
+    return;
+  }
+  const int64_t n = V.levels[top]->n_dofs;
+  convert(n, f, V.f32[top].ptr, s);
+  cycle32(V, top, V.f32[top].ptr, V.x32[top].ptr, s);
+  convert(n, V.x32[top].ptr, x, s);
+}
+
+void vcycle_set_precision(VCycle& V, int bits) {
+  NNMG_REQUIRE(bits == 64 || bits == 32, kInvalidArgument, "precision must be 64 or 32 bits");
+  const bool mixed = bits == 32;
+  if (mixed == V.mixed) return;
+  for (auto& g : V.graphs) cudaGraphExecDestroy(g.exec);
+  V.graphs.clear();
+  V.kernels_per_cycle = 0;
+  V.mixed = mixed;
+  if (!mixed || !V.f32.empty()) return;
+  const int nl = static_cast<int>(V.levels.size());
+  V.f32.resize(nl);
+  V.x32.resize(nl);
+  V.r32.resize(nl);
+  V.work32.resize(nl);
+  for (int l = 0; l < nl; ++l) {
+    const int64_t n = V.levels[l]->n_dofs;
+    V.f32[l].alloc(n);
+    V.x32[l].alloc(n);
+    if (l > 0) {
+      level_enable_f32(*V.levels[l], 0);
+      transfer_enable_f32(*V.transfers[l - 1], 0);
+      V.r32[l].alloc(n);
+      V.work32[l].alloc(3 * n);
+    }
+  }
+  V.cf.alloc(V.levels[0]->n_dofs);
+  V.cx.alloc(V.levels[0]->n_dofs);
+  NNMG_CUDA_TRY(cudaDeviceSynchronize());
+}
+
+void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s) {
+  if (!V.use_graph) {
+    run_cycle(V, f, x, s);
     return;
   }
   NNMG_REQUIRE(s != nullptr, kInvalidArgument, "graph replay needs a non-default stream");
@@ -153,7 +260,7 @@ void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s) {
     const uint64_t c0 = launch_count();
     NNMG_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     try {
-      cycle(V, top, f, x, s);
+      run_cycle(V, f, x, s);
     } catch (...) {
       cudaStreamEndCapture(s, &g);
       if (g) cudaGraphDestroy(g);

@@ -26,6 +26,11 @@ struct VCycle {
   // per level: right-hand side and correction (coarse levels), residual, smoother work
   std::vector<DevBuf<double>> f, x, r, work;
   bool use_graph = false;
+  // mixed precision (vcycle_set_precision(32)): fp32 level vectors above the
+  // coarsest level, fp64 coarse solve through cf/cx
+  bool mixed = false;
+  std::vector<DevBuf<float>> f32, x32, r32, work32;
+  DevBuf<double> cf, cx;
   bool smoother_residual = true;  // residual after pre-smoothing from the smoother's recurrence (no b copy)
   bool post_from_residual = true; // first post-smoothing sweep starts from that residual (no b copy)
   struct Graph {
@@ -44,6 +49,10 @@ struct VCycle {
 VCycle* vcycle_create(int n_levels, Level* const* levels, Transfer* const* transfers, Coarse* coarse,
                       const double* lam_max, const double* lam_min, const int* degree, int m1, int m2);
 void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s);
+// 64: the fp64 cycle (default); 32: the mixed-precision cycle (fp32 storage
+// of vectors / geometry / transfer records on levels >= 1, fp64 arithmetic,
+// fp64 coarse solve); input and output stay fp64
+void vcycle_set_precision(VCycle& V, int bits);
 int64_t vcycle_kernels(VCycle& V);
 
 }  // namespace nnmg

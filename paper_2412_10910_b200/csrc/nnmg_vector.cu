@@ -39,9 +39,11 @@ __global__ void k_cheb_step(int64_t n, const double* __restrict__ ad, const doub
 // In-place residual form: the apply scatters -A d straight into r.
 // x0 == nullptr: r = b, d = inv_diag*b/theta, x = d
 // otherwise r already holds b - A x0: d = inv_diag*r/theta, x = x0 + d
-__global__ void k_cheb_init(int64_t n, const double* __restrict__ b, const double* x0,
-                            const double* __restrict__ inv_diag, double theta, double* __restrict__ r,
-                            double* __restrict__ d, double* x) {
+// T: vector storage (double; float in the mixed-precision V-cycle, fp64
+// arithmetic on fp32 storage)
+template <class T>
+__global__ void k_cheb_init(int64_t n, const T* __restrict__ b, const T* x0, const T* __restrict__ inv_diag,
+                            double theta, T* __restrict__ r, T* __restrict__ d, T* x) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ri;
@@ -49,64 +51,109 @@ __global__ void k_cheb_init(int64_t n, const double* __restrict__ b, const doubl
     ri = r[i];
   } else {
     ri = b[i];
-    r[i] = ri;
+    r[i] = T(ri);
   }
-  const double di = inv_diag[i] * ri / theta;
-  d[i] = di;
-  if (x) x[i] = x0 ? x0[i] + di : di;  // x == nullptr: x = d is left to the first update
+  const double di = double(inv_diag[i]) * ri / theta;
+  d[i] = T(di);
+  if (x) x[i] = T(x0 ? double(x0[i]) + di : di);  // x == nullptr: x = d is left to the first update
 }
 
 // post-smoothing start from the pre-smoothing residual: r already holds
 // f - A (x + t) (t = the prolongated correction, not yet added to x):
 // d = inv_diag*r/theta; x = (x + t) + d, the same roundings as x += t
 // followed by k_cheb_init
-__global__ void k_cheb_init_add(int64_t n, const double* __restrict__ t, const double* __restrict__ inv_diag,
-                                double theta, const double* __restrict__ r, double* __restrict__ d,
-                                double* __restrict__ x) {
+template <class T>
+__global__ void k_cheb_init_add(int64_t n, const T* __restrict__ t, const T* __restrict__ inv_diag, double theta,
+                                const T* __restrict__ r, T* __restrict__ d, T* __restrict__ x) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double di = inv_diag[i] * r[i] / theta;
-  d[i] = di;
-  x[i] = (x[i] + t[i]) + di;
+  const double di = double(inv_diag[i]) * double(r[i]) / theta;
+  d[i] = T(di);
+  if constexpr (sizeof(T) == sizeof(double))
+    x[i] = (x[i] + t[i]) + di;
+  else
+    x[i] = T((double(x[i]) + double(t[i])) + di);
 }
 
-void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double theta, const double* r, double* d,
-                   double* x, cudaStream_t s) {
+template <class T>
+void cheb_init_add_t(int64_t n, const T* t, const T* inv_diag, double theta, const T* r, T* d, T* x, cudaStream_t s) {
   if (!n) return;
-  k_cheb_init_add<<<grid_for(n), kBS, 0, s>>>(n, t, inv_diag, theta, r, d, x);
+  k_cheb_init_add<T><<<grid_for(n), kBS, 0, s>>>(n, t, inv_diag, theta, r, d, x);
   NNMG_CHECK_LAUNCH();
   count_launch();
+}
+void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double theta, const double* r, double* d,
+                   double* x, cudaStream_t s) {
+  cheb_init_add_t(n, t, inv_diag, theta, r, d, x, s);
+}
+void cheb_init_add(int64_t n, const float* t, const float* inv_diag, double theta, const float* r, float* d,
+                   float* x, cudaStream_t s) {
+  cheb_init_add_t(n, t, inv_diag, theta, r, d, x, s);
 }
 
 // r already holds r - A d: d = c1 d + c2 inv_diag r; x += d
 // (x_is_d: x was never written and equals the old d, so x = d_old + d_new:
 // the same rounding, one vector read and one write fewer)
-__global__ void k_cheb_update(int64_t n, const double* __restrict__ inv_diag, double c1, double c2,
-                              const double* __restrict__ r, double* __restrict__ d, double* __restrict__ x,
-                              int x_is_d) {
+template <class T>
+__global__ void k_cheb_update(int64_t n, const T* __restrict__ inv_diag, double c1, double c2,
+                              const T* __restrict__ r, T* __restrict__ d, T* __restrict__ x, int x_is_d) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double dold = d[i];
-  const double di = c1 * dold + c2 * (inv_diag[i] * r[i]);
-  d[i] = di;
-  x[i] = (x_is_d ? dold : x[i]) + di;
+  const double di = c1 * dold + c2 * (double(inv_diag[i]) * double(r[i]));
+  d[i] = T(di);
+  x[i] = T((x_is_d ? dold : double(x[i])) + di);
 }
 
+template <class T>
+void cheb_init_t(int64_t n, const T* b, const T* x0, const T* inv_diag, double theta, T* r, T* d, T* x,
+                 cudaStream_t s) {
+  if (!n) return;
+  k_cheb_init<T><<<grid_for(n), kBS, 0, s>>>(n, b, x0, inv_diag, theta, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
 void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_diag, double theta, double* r,
                double* d, double* x, cudaStream_t s) {
-  if (!n) return;
-  k_cheb_init<<<grid_for(n), kBS, 0, s>>>(n, b, x0, inv_diag, theta, r, d, x);
-  NNMG_CHECK_LAUNCH();
-  count_launch();
+  cheb_init_t(n, b, x0, inv_diag, theta, r, d, x, s);
+}
+void cheb_init(int64_t n, const float* b, const float* x0, const float* inv_diag, double theta, float* r, float* d,
+               float* x, cudaStream_t s) {
+  cheb_init_t(n, b, x0, inv_diag, theta, r, d, x, s);
 }
 
-void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,
-                 cudaStream_t s, bool x_is_d) {
+template <class T>
+void cheb_update_t(int64_t n, const T* inv_diag, double c1, double c2, const T* r, T* d, T* x, cudaStream_t s,
+                   bool x_is_d) {
   if (!n) return;
-  k_cheb_update<<<grid_for(n), kBS, 0, s>>>(n, inv_diag, c1, c2, r, d, x, x_is_d ? 1 : 0);
+  k_cheb_update<T><<<grid_for(n), kBS, 0, s>>>(n, inv_diag, c1, c2, r, d, x, x_is_d ? 1 : 0);
   NNMG_CHECK_LAUNCH();
   count_launch();
 }
+void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,
+                 cudaStream_t s, bool x_is_d) {
+  cheb_update_t(n, inv_diag, c1, c2, r, d, x, s, x_is_d);
+}
+void cheb_update(int64_t n, const float* inv_diag, double c1, double c2, const float* r, float* d, float* x,
+                 cudaStream_t s, bool x_is_d) {
+  cheb_update_t(n, inv_diag, c1, c2, r, d, x, s, x_is_d);
+}
+
+// precision conversion at the mixed-precision V-cycle's boundaries
+template <class A, class B>
+__global__ void k_convert(int64_t n, const A* __restrict__ a, B* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = B(a[i]);
+}
+template <class A, class B>
+void convert_t(int64_t n, const A* a, B* b, cudaStream_t s) {
+  if (!n) return;
+  k_convert<A, B><<<grid_for(n), kBS, 0, s>>>(n, a, b);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+void convert(int64_t n, const double* a, float* b, cudaStream_t s) { convert_t(n, a, b, s); }
+void convert(int64_t n, const float* a, double* b, cudaStream_t s) { convert_t(n, a, b, s); }
 
 // y = alpha*x + beta*y  (general axpby; beta==0 ignores y's content)
 __global__ void k_axpby(int64_t n, double alpha, const double* __restrict__ x, double beta, double* __restrict__ y) {

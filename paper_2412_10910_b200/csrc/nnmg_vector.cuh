@@ -18,6 +18,15 @@ void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_d
                double* d, double* x, cudaStream_t s);
 void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const double* r, double* d, double* x,
                  cudaStream_t s, bool x_is_d = false);
+// fp32 storage, fp64 arithmetic (mixed-precision V-cycle)
+void cheb_init_add(int64_t n, const float* t, const float* inv_diag, double theta, const float* r, float* d, float* x,
+                   cudaStream_t s);
+void cheb_init(int64_t n, const float* b, const float* x0, const float* inv_diag, double theta, float* r, float* d,
+               float* x, cudaStream_t s);
+void cheb_update(int64_t n, const float* inv_diag, double c1, double c2, const float* r, float* d, float* x,
+                 cudaStream_t s, bool x_is_d = false);
+void convert(int64_t n, const double* a, float* b, cudaStream_t s);
+void convert(int64_t n, const float* a, double* b, cudaStream_t s);
 void axpby(int64_t n, double alpha, const double* x, double beta, double* y, cudaStream_t s);
 void sub(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);
 void mul(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);

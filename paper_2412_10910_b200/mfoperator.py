@@ -36,8 +36,9 @@ def lame_parameters(E, nu):
 class _GpuOperatorBase:
     _physics = PHYSICS_LAPLACE
 
-    def __init__(self, space, lam=0.0, mu=0.0, device=None):
+    def __init__(self, space, lam=0.0, mu=0.0, device=None, deterministic=False):
         self.space = space
+        self.deterministic = bool(deterministic)
         self.device = D.resolve_device(device)
         mesh = space.mesh
         dim = int(mesh.dim)
@@ -54,6 +55,11 @@ class _GpuOperatorBase:
                 _lib.host_ptr(cell_dofs), len(cons), _lib.host_ptr(cons), float(lam), float(mu), ctypes.byref(h),
             )
         self._h = h
+        if self.deterministic:
+            # fixed-order summation of the cell contributions (cell buffer +
+            # gather) instead of fp64 atomics: bitwise reproducible results, as
+            # the reference's serial bincount scatter (mfoperator.py:88-90)
+            _lib.call("nnmg_level_set_deterministic", h, 1)
         self._n = int(space.n_dofs)
         self._constraint_snapshot = cons
         self._diag = None
@@ -136,10 +142,10 @@ class LaplaceOperator(_GpuOperatorBase):
 
     _physics = PHYSICS_LAPLACE
 
-    def __init__(self, space, device=None):
+    def __init__(self, space, device=None, deterministic=False):
         if space.n_components != 1:
             raise ValueError("LaplaceOperator is scalar; use ElasticityOperator")
-        super().__init__(space, device=device)
+        super().__init__(space, device=device, deterministic=deterministic)
 
 
 class ElasticityOperator(_GpuOperatorBase):
@@ -147,12 +153,12 @@ class ElasticityOperator(_GpuOperatorBase):
 
     _physics = PHYSICS_ELASTICITY
 
-    def __init__(self, space, lam, mu, device=None):
+    def __init__(self, space, lam, mu, device=None, deterministic=False):
         if space.n_components != space.mesh.dim:
             raise ValueError("elasticity needs one component per space dimension")
         self.lam = float(lam)
         self.mu = float(mu)
-        super().__init__(space, lam=self.lam, mu=self.mu, device=device)
+        super().__init__(space, lam=self.lam, mu=self.mu, device=device, deterministic=deterministic)
 
 
 def compute_diagonal(op):

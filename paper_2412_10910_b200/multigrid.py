@@ -66,6 +66,7 @@ class MultigridHierarchy:
         self.device = levels[-1].operator.device
         self._vc = None
         self._graph = True
+        self.precision = 64
 
     @property
     def n_levels(self):
@@ -155,7 +156,21 @@ class MultigridHierarchy:
                       self.m1, self.m2, ctypes.byref(h))
             self._vc = h
             self._vc_keep = (lv, tr, lmax, lmin, deg)
+            if self.precision != 64:
+                _lib.call("nnmg_vcycle_set_precision", h, int(self.precision))
         return self._vc
+
+    def set_precision(self, bits):
+        """64: the fp64 V-cycle (default).  32: the paper's mixed-precision
+        cycle: fp32 storage of level vectors, geometry,
+        inverse diagonals and transfer coordinates above the coarsest level,
+        fp64 arithmetic and coarse solve; the cycle's input and output (and
+        the outer CG) stay fp64.  Native executor only."""
+        if bits not in (32, 64):
+            raise ValueError("precision must be 32 or 64")
+        self.precision = int(bits)
+        if self._vc is not None:
+            _lib.call("nnmg_vcycle_set_precision", self._vc, int(bits))
 
     def use_graph(self, enable=True):
         self._graph = bool(enable)
@@ -189,6 +204,8 @@ class MultigridHierarchy:
         n = self.levels[l - 1].operator.n_dofs
         fd, host = D.to_device(f, n, self.device)
         use_exec = (not self.timing) if executor is None else bool(executor)
+        if self.precision != 64 and not (use_exec and l == self.n_levels):
+            raise ValueError("the mixed-precision cycle runs in the native executor on the finest level only")
         if use_exec and l == self.n_levels:
             x = D.empty(n, self.device)
             self.v_cycle_into(fd, x)
@@ -217,15 +234,21 @@ class HierarchyConfig:
     # not in the reference: exact solve above the dense limit where faster
     # (False = the reference's CG, the parity mode; True; "auto")
     coarse_direct: object = False
+    # 64: fp64 V-cycle; 32: the paper's mixed-precision cycle
+    vcycle_precision: int = 64
+    # fixed-order (atomic-free) summation in every apply / diagonal / load
+    # vector and an exact coarse solve: bitwise reproducible V-cycles and
+    # iteration counts (the reference's serial scatter, mfoperator.py:88-90)
+    deterministic: bool = False
 
 
-def _make_operator(space, problem, lame, device):
+def _make_operator(space, problem, lame, device, deterministic=False):
     if problem == "poisson":
-        return LaplaceOperator(space, device=device)
+        return LaplaceOperator(space, device=device, deterministic=deterministic)
     if problem == "elasticity":
         if lame is None:
             raise ValueError("elasticity needs lame=(lambda, mu)")
-        return ElasticityOperator(space, *lame, device=device)
+        return ElasticityOperator(space, *lame, device=device, deterministic=deterministic)
     raise ValueError(f"unknown problem {problem!r}")
 
 
@@ -260,7 +283,7 @@ def build_hp_hierarchy(meshes, degree, mode="h", nested=False, problem="poisson"
         space = build_space(mesh, p, n_components=n_components)
         if dirichlet_ids is not None:
             space.constraints = dirichlet_constraints(space, dirichlet_ids, dirichlet_value)
-        op = _make_operator(space, problem, lame, dev)
+        op = _make_operator(space, problem, lame, dev, cfg.deterministic)
         smoother = ChebyshevJacobi(op, degree=cfg.chebyshev_degree, window_ratio=cfg.window_ratio,
                                    safety=cfg.safety, n_lanczos=cfg.lanczos_iters, seed=cfg.lanczos_seed)
         levels.append(Level(space, op, smoother))
@@ -273,6 +296,11 @@ def build_hp_hierarchy(meshes, degree, mode="h", nested=False, problem="poisson"
             transfers.append(setup_nested(cspace, space, search, coarse_operator=cop, fine_operator=op))
         else:
             transfers.append(setup_nonnested(cspace, space, search, coarse_operator=cop, fine_operator=op))
+    # the coarse CG kernel sums with atomics: deterministic mode solves exactly
     coarse = CoarseSolver(levels[0].operator, dense_limit=cfg.coarse_dense_limit,
-                          cg_reduction=cfg.coarse_cg_reduction, direct=cfg.coarse_direct)
-    return MultigridHierarchy(levels, transfers, coarse, m1=cfg.m1, m2=cfg.m2, timing=timing)
+                          cg_reduction=cfg.coarse_cg_reduction,
+                          direct=True if cfg.deterministic else cfg.coarse_direct)
+    H = MultigridHierarchy(levels, transfers, coarse, m1=cfg.m1, m2=cfg.m2, timing=timing)
+    if cfg.vcycle_precision != 64:
+        H.set_precision(cfg.vcycle_precision)
+    return H
