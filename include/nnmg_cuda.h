@@ -80,6 +80,13 @@ int nnmg_level_residual(nnmg_level_t level, const double* f_dev, const double* x
 int nnmg_level_compute_diagonal(nnmg_level_t level, void* stream);
 int nnmg_level_diagonal(nnmg_level_t level, double* diag_dev, void* stream);
 
+/* deterministic mode (enable != 0): the apply, residual, diagonal and load
+ * vector sum each DoF's cell contributions in a fixed order (per-cell buffer
+ * + gather) instead of fp64 atomics, like the reference's serial bincount
+ * scatter (mfoperator.py:88-90): bitwise reproducible results at the cost of
+ * the buffer round trip.  Set before the diagonal is computed. */
+int nnmg_level_set_deterministic(nnmg_level_t level, int enable);
+
 /* b_dev = (f, phi_i) for a constant body load f_host[n_components],
  * constrained entries 0 (body-load part of assemble_rhs, mfoperator.py:313-355) */
 int nnmg_level_load_vector(nnmg_level_t level, const double* f_host, double* b_dev, void* stream);
@@ -109,6 +116,13 @@ int nnmg_axpby(int64_t n, double alpha, const double* x, double beta, double* y,
 int nnmg_sub(int64_t n, const double* a, const double* b, double* out, void* stream);
 int nnmg_mul(int64_t n, const double* a, const double* b, double* out, void* stream);
 int nnmg_cg_update(int64_t n, double alpha, const double* p, const double* ap, double* x, double* r, void* stream);
+
+/* ---- halo exchange of the distributed levels: pack
+ * dst[i] = src[idx[i]] into a send buffer, unpack dst[idx[i]] = src[i]
+ * (add = 0, ghost import) or dst[idx[i]] += src[i] (add != 0, export of ghost
+ * partial sums); idx entries distinct within one call; device pointers */
+int nnmg_halo_pack(int64_t n, const int64_t* idx, const double* src, double* dst, void* stream);
+int nnmg_halo_unpack(int64_t n, const int64_t* idx, const double* src, double* dst, int add, void* stream);
 
 /* ---- non-nested transfer: replaces TwoLevelTransferNonNested
  * (transfer.py:61-124).  point_dofs_host: fine scalar DoFs not fully

@@ -80,6 +80,8 @@ _SIGNATURES = {
     "nnmg_vcycle_use_graph": [_handle, c_int],
     "nnmg_vcycle_set_precision": [_handle, c_int],
     "nnmg_level_set_deterministic": [_handle, c_int],
+    "nnmg_halo_pack": [c_int64, c_void_p, c_void_p, c_void_p, c_void_p],
+    "nnmg_halo_unpack": [c_int64, c_void_p, c_void_p, c_void_p, c_int, c_void_p],
     "nnmg_vcycle_kernels_per_cycle": [_handle, _p_int64],
 }
 

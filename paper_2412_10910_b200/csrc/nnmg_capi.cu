@@ -291,6 +291,20 @@ int nnmg_vcycle_run(nnmg_vcycle_t vcycle, const double* f, double* x, void* stre
   });
 }
 
+int nnmg_halo_pack(int64_t n, const int64_t* idx, const double* src, double* dst, void* stream) {
+  return guard([&] {
+    NNMG_REQUIRE(n == 0 || (idx && src && dst), kInvalidArgument, "null argument");
+    gather_idx(n, idx, src, dst, S(stream));
+  });
+}
+
+int nnmg_halo_unpack(int64_t n, const int64_t* idx, const double* src, double* dst, int add, void* stream) {
+  return guard([&] {
+    NNMG_REQUIRE(n == 0 || (idx && src && dst), kInvalidArgument, "null argument");
+    scatter_idx(n, idx, src, dst, add != 0, S(stream));
+  });
+}
+
 int nnmg_level_set_deterministic(nnmg_level_t level, int enable) {
   return guard([&] {
     REQUIRE_HANDLE(level);

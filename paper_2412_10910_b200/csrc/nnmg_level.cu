@@ -608,7 +608,7 @@ struct ApplyLaunchT {
                              : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false, false>
                                                 : k_apply_reg<D, P, 1, false, false>));
         kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
-                                            hyb ? L.recompute_mod : 0, L.recompute_num, cd, ncd);
+                                            hyb ? L.recompute_mod : 0, L.recompute_num, cd, ncd, nullptr);
         fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();
@@ -632,7 +632,7 @@ struct ApplyLaunchT {
           if (L.edges.ptr && L.elast_recompute && !cellout) {
             auto kr = neg ? k_apply_reg_elast<P, true, 2> : k_apply_reg_elast<P, false, 2>;
             kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.edges.ptr, b0, b1, L.lam,
-                                                         L.mu, nullptr, 0);
+                                                         L.mu, nullptr, 0, nullptr);
             NNMG_CHECK_LAUNCH();
             count_launch();
             return;

@@ -139,6 +139,37 @@ void cheb_update(int64_t n, const float* inv_diag, double c1, double c2, const f
   cheb_update_t(n, inv_diag, c1, c2, r, d, x, s, x_is_d);
 }
 
+// K9 halo pack / unpack of the distributed levels: pack the
+// listed entries of a local vector into a contiguous send buffer, unpack a
+// receive buffer into the listed entries (copy for ghost import, add for the
+// export of ghost partial sums).  The indices of one list are distinct, so
+// the unpack has no write conflicts; lists of different peers are applied in
+// a fixed peer order by the caller.
+__global__ void k_gather_idx(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                             double* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+__global__ void k_scatter_idx(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                              double* __restrict__ dst, int add) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = idx[i];
+  dst[j] = add ? dst[j] + src[i] : src[i];
+}
+void gather_idx(int64_t n, const int64_t* idx, const double* src, double* dst, cudaStream_t s) {
+  if (!n) return;
+  k_gather_idx<<<grid_for(n), kBS, 0, s>>>(n, idx, src, dst);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+void scatter_idx(int64_t n, const int64_t* idx, const double* src, double* dst, bool add, cudaStream_t s) {
+  if (!n) return;
+  k_scatter_idx<<<grid_for(n), kBS, 0, s>>>(n, idx, src, dst, add ? 1 : 0);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
 // precision conversion at the mixed-precision V-cycle's boundaries
 template <class A, class B>
 __global__ void k_convert(int64_t n, const A* __restrict__ a, B* __restrict__ b) {

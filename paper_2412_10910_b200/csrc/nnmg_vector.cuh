@@ -25,6 +25,9 @@ void cheb_init(int64_t n, const float* b, const float* x0, const float* inv_diag
                float* x, cudaStream_t s);
 void cheb_update(int64_t n, const float* inv_diag, double c1, double c2, const float* r, float* d, float* x,
                  cudaStream_t s, bool x_is_d = false);
+// halo pack (dst[i] = src[idx[i]]) and unpack (dst[idx[i]] (+)= src[i])
+void gather_idx(int64_t n, const int64_t* idx, const double* src, double* dst, cudaStream_t s);
+void scatter_idx(int64_t n, const int64_t* idx, const double* src, double* dst, bool add, cudaStream_t s);
 void convert(int64_t n, const double* a, float* b, cudaStream_t s);
 void convert(int64_t n, const float* a, double* b, cudaStream_t s);
 void axpby(int64_t n, double alpha, const double* x, double beta, double* y, cudaStream_t s);

@@ -71,6 +71,18 @@ def partition_morton(mesh, n_ranks):
     return owner
 
 
+def partition_matching(mesh, fine_mesh, fine_owner, locate):
+    """Owner of each cell = owner of the fine cell containing its centroid
+    (metrics.py:41-46), so consecutive levels overlap spatially and the
+    transfers stay mostly rank-local.  ``locate(mesh, points)`` returns the
+    owning cells (the backend's point location)."""
+    cent = np.zeros((mesh.n_cells, mesh.dim))
+    for v in range(mesh.cells.shape[1]):
+        cent += mesh.vertices[mesh.cells[:, v]]
+    cent /= mesh.cells.shape[1]
+    return np.asarray(fine_owner)[np.asarray(locate(fine_mesh, cent))]
+
+
 def dof_owner_ranks(cell_dofs, cell_owner, n_scalar):
     """Rank of the lowest-index cell containing each scalar DoF."""
     nc, nloc = cell_dofs.shape
@@ -178,7 +190,38 @@ class HaloPlan:
     def to(self, device):
         self.send = {q: torch.from_numpy(v).to(device) for q, v in self.send.items()}
         self.recv = {q: torch.from_numpy(v).to(device) for q, v in self.recv.items()}
+        # persistent per-peer message buffers (no allocation per exchange;
+        # fixed addresses, so the exchange can live in a CUDA graph)
+        f64 = dict(dtype=torch.float64, device=device)
+        self.buf_send = {q: torch.empty(len(v), **f64) for q, v in self.send.items()}
+        self.buf_recv = {q: torch.empty(len(v), **f64) for q, v in self.recv.items()}
         return self
+
+
+def _pack(x, idx, out):
+    """out[i] = x[idx[i]]: the K9 pack kernel on the GPU, index_select on CPU."""
+    if x.is_cuda:
+        from . import _device as D
+        from . import _lib
+
+        _lib.call("nnmg_halo_pack", idx.numel(), idx.data_ptr(), x.data_ptr(), out.data_ptr(),
+                  D.stream_ptr(x.device))
+    else:
+        torch.index_select(x, 0, idx, out=out)
+
+
+def _unpack(x, idx, buf, add):
+    """x[idx[i]] = buf[i] (or +=): the K9 unpack kernel on the GPU."""
+    if x.is_cuda:
+        from . import _device as D
+        from . import _lib
+
+        _lib.call("nnmg_halo_unpack", idx.numel(), idx.data_ptr(), buf.data_ptr(), x.data_ptr(), 1 if add else 0,
+                  D.stream_ptr(x.device))
+    elif add:
+        x.index_add_(0, idx, buf)
+    else:
+        x.index_copy_(0, idx, buf)
 
 
 def _exchange(peers, sendbufs, recvbufs):
@@ -195,21 +238,22 @@ def _exchange(peers, sendbufs, recvbufs):
 
 def halo_import(plan, x):
     """Owner values -> ghost copies (x is a local vector)."""
-    send = {q: x.index_select(0, plan.send[q]) for q in plan.peers}
-    recv = {q: torch.empty(len(plan.recv[q]), dtype=x.dtype, device=x.device) for q in plan.peers}
-    _exchange(plan.peers, send, recv)
     for q in plan.peers:
-        x.index_copy_(0, plan.recv[q], recv[q])
+        _pack(x, plan.send[q], plan.buf_send[q])
+    _exchange(plan.peers, plan.buf_send, plan.buf_recv)
+    for q in plan.peers:
+        _unpack(x, plan.recv[q], plan.buf_recv[q], add=False)
 
 
 def halo_export_add(plan, y):
     """Ghost partial sums -> owners (added in fixed peer order)."""
     # for export the roles flip: we send what we hold as ghosts (plan.recv)
-    send = {q: y.index_select(0, plan.recv[q]) for q in plan.peers}
-    recv = {q: torch.empty(len(plan.send[q]), dtype=y.dtype, device=y.device) for q in plan.peers}
-    _exchange(plan.peers, send, recv)
+    # from the receive-side buffers and receive into the send-side ones
+    for q in plan.peers:
+        _pack(y, plan.recv[q], plan.buf_recv[q])
+    _exchange(plan.peers, plan.buf_recv, plan.buf_send)
     for q in sorted(plan.peers):
-        y.index_add_(0, plan.send[q], recv[q])
+        _unpack(y, plan.send[q], plan.buf_send[q], add=True)
 
 
 # ---------------------------------------------------------------------------
@@ -350,13 +394,17 @@ class DistHierarchy:
     """Distributed twin of MultigridHierarchy (multigrid.py:83-117): level 1
     replicated, levels >= 2 partitioned."""
 
-    def __init__(self, levels, transfers, coarse_solve, degree, window=10.0, m1=1, m2=1):
+    def __init__(self, levels, transfers, coarse_solve, degree, window=10.0, m1=1, m2=1, graph=True):
         self.levels = levels
         self.transfers = transfers
         self.coarse_solve = coarse_solve
         self.degree = degree
         self.window = window
         self.m1, self.m2 = m1, m2
+        # GPU: the whole distributed cycle (kernels, halo pack/unpack, NCCL
+        # point-to-point and the coarse all-reduce) captured as one CUDA graph
+        self.use_graph = bool(graph)
+        self._graph = None
 
     @property
     def finest(self):
@@ -376,7 +424,8 @@ class DistHierarchy:
             cur = x
         t = lev.bk.zeros(lev.n)
         lev.apply_into(x, t)
-        r = f - t
+        r = lev.bk.zeros(lev.n)
+        lev.bk.sub(f, t, r)
         rc = T.coarse.bk.zeros(T.coarse.n)
         T.restrict_into(r, rc)
         delta = self._v(l - 1, rc)
@@ -386,7 +435,32 @@ class DistHierarchy:
         return x
 
     def precondition(self, r):
+        """z = V-cycle(r).  On the GPU the cycle is captured once into a CUDA
+        graph (static input/output buffers; the returned tensor is reused by
+        the next call) and replayed; capture failures fall back to eager."""
+        if self.use_graph and r.is_cuda:
+            try:
+                return self._replay(r)
+            except RuntimeError:
+                self.use_graph = False
+                self._graph = None
         return self._v(len(self.levels), r)
+
+    def _replay(self, r):
+        if self._graph is None:
+            self._gin = r.clone()
+            side = torch.cuda.Stream(device=r.device)
+            side.wait_stream(torch.cuda.current_stream(r.device))
+            with torch.cuda.stream(side):
+                self._v(len(self.levels), self._gin)  # warm-up outside the capture
+            torch.cuda.current_stream(r.device).wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._gout = self._v(len(self.levels), self._gin)
+            self._graph = g
+        self._gin.copy_(r)
+        self._graph.replay()
+        return self._gout
 
 
 def dist_cg_solve(level, b, precond=None, target_reduction=1e-4, max_iter=1000):
@@ -409,8 +483,7 @@ def dist_cg_solve(level, b, precond=None, target_reduction=1e-4, max_iter=1000):
         if pap <= 0.0:
             raise RuntimeError(f"p'Ap = {pap:.3e} at iteration {k}")
         alpha = rz / pap
-        x = x + alpha * p
-        r = r - alpha * ap
+        bk.cg_update(alpha, p, ap, x, r)
         norm = float(np.sqrt(level.dot(r, r)))
         history.append(norm)
         if norm <= target:
@@ -419,7 +492,7 @@ def dist_cg_solve(level, b, precond=None, target_reduction=1e-4, max_iter=1000):
         rz_new = level.dot(r, z)
         beta = rz_new / rz
         rz = rz_new
-        p = z + beta * p
+        bk.axpby(1.0, z, beta, p)
     return x, max_iter, False, history
 
 
@@ -429,16 +502,31 @@ def dist_cg_solve(level, b, precond=None, target_reduction=1e-4, max_iter=1000):
 
 
 def build_distributed_hierarchy(spaces, backend, problem="poisson", lame=None, cheb_degree=4, window=10.0,
-                                search=None, m1=1, m2=1, partition=None):
+                                search=None, m1=1, m2=1, partition=None, policy="matching", graph=True):
     """spaces: global FESpaces coarsest first (replicated host data on every
-    rank).  Returns a DistHierarchy for this rank."""
+    rank).  Returns a DistHierarchy for this rank.  policy: "matching" (the
+    finest level Morton-split, each coarser partitioned level takes the owner
+    of the finer cell containing its centroid, metrics.py:41-46) or
+    "default" (Morton on every level, metrics.py:24-38)."""
+    if policy not in ("matching", "default"):
+        raise ValueError("policy must be 'matching' or 'default'")
     rank, world = dist.get_rank(), dist.get_world_size()
     nlev = len(spaces)
     owners = [None] * nlev
     dofown = [None] * nlev
-    for l in range(1, nlev):
+    for l in range(nlev - 1, 0, -1):
         sp = spaces[l]
-        owners[l] = partition[l] if partition is not None else partition_morton(sp.mesh, world)
+        if partition is not None:
+            owners[l] = partition[l]
+        elif policy == "matching" and l < nlev - 1:
+            owners[l] = partition_matching(sp.mesh, spaces[l + 1].mesh, owners[l + 1],
+                                           lambda m, pts: backend.locate(m, pts, None)[0])
+            if np.bincount(owners[l], minlength=world).min() == 0:
+                # a rank would own no cell of this level (coarse level with
+                # fewer cells than ranks in a region): Morton split instead
+                owners[l] = partition_morton(sp.mesh, world)
+        else:
+            owners[l] = partition_morton(sp.mesh, world)
         dofown[l] = dof_owner_ranks(np.asarray(sp.cell_dofs), owners[l], sp.n_scalar_dofs)
     # fine-side transfer records: this rank's owned points located in the coarse mesh
     recs = [None] * (nlev - 1)
@@ -505,7 +593,9 @@ def build_distributed_hierarchy(spaces, backend, problem="poisson", lame=None, c
         lt = backend.make_transfer(tc_space, fl.space, tc_op, fl.op, rec)
         transfers.append(DistTransfer(cl, fl, lt, backend, cimp, cexp))
     coarse = backend.make_coarse(levels[0].op)
-    return DistHierarchy(levels, transfers, coarse, cheb_degree, window, m1, m2)
+    H = DistHierarchy(levels, transfers, coarse, cheb_degree, window, m1, m2, graph=graph)
+    H.owners = owners
+    return H
 
 
 def _free(dofs, layout):
@@ -565,11 +655,21 @@ class GpuBackend:
     def make_coarse(self, op):
         from .solvers import CoarseSolver
 
-        cs = CoarseSolver(op)
+        cs = CoarseSolver(op, direct="auto")
+        self.coarse_solver = cs
         return lambda b, x: cs.solve_into(b, x)
 
     def dot(self, a, b):
         return self._ops.dot(a.contiguous(), b.contiguous())
+
+    def sub(self, a, b, out):
+        self._ops.sub(a, b, out)
+
+    def cg_update(self, alpha, p, ap, x, r):
+        self._ops.cg_update(alpha, p, ap, x, r)
+
+    def axpby(self, alpha, x, beta, y):
+        self._ops.axpby(alpha, x, beta, y)
 
     def cheb_start(self, b, ax, x0, inv_diag, theta, r, d, x):
         from . import _lib

@@ -59,6 +59,16 @@ class OracleBackend:
     def dot(self, a, b):
         return float((a * b).sum())
 
+    def sub(self, a, b, out):
+        torch.sub(a, b, out=out)
+
+    def cg_update(self, alpha, p, ap, x, r):
+        x.add_(alpha * p)
+        r.sub_(alpha * ap)
+
+    def axpby(self, alpha, x, beta, y):
+        y.mul_(beta).add_(alpha * x)
+
     def cheb_start(self, b, ax, x0, inv_diag, theta, r, d, x):
         r.copy_(b - ax if ax is not None else b)
         d.copy_(inv_diag * r / theta)

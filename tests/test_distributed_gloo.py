@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cname, scale, q):
+def _worker(rank, world, port, cname, scale, q, policy="matching"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -41,7 +41,8 @@ def _worker(rank, world, port, cname, scale, q):
             sp.constraints = fespace.dirichlet_constraints(sp, cfg.dirichlet_ids)
             spaces.append(sp)
         bk = OracleBackend()
-        DH = distributed.build_distributed_hierarchy(spaces, bk, cfg.problem, cfg.lame, cfg.chebyshev_degree)
+        DH = distributed.build_distributed_hierarchy(spaces, bk, cfg.problem, cfg.lame, cfg.chebyshev_degree,
+                                                     policy=policy)
         fine = DH.finest
         b_glob = assemble_rhs(spaces[-1], cfg.body_force if cfg.body_force else 1.0)
         u_glob = np.random.default_rng(0).standard_normal(len(b_glob))
@@ -79,12 +80,14 @@ def _worker(rank, world, port, cname, scale, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cname,scale", [("C2", 16), ("C3", 8), ("C5", 16)])
-def test_distributed_matches_oracle_world2(cname, scale):
+@pytest.mark.parametrize("cname,scale,world,policy", [("C2", 16, 2, "matching"), ("C3", 8, 2, "matching"),
+                                                     ("C5", 16, 2, "matching"), ("C3", 8, 2, "default"),
+                                                     ("C3", 8, 4, "matching")])
+def test_distributed_matches_oracle(cname, scale, world, policy):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, cname, scale, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cname, scale, q, policy)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=600)
@@ -97,7 +100,7 @@ def test_distributed_matches_oracle_world2(cname, scale):
     assert res["z"] <= 1e-9, res
     assert res["conv"] and abs(res["its"] - res["rits"]) <= 1, res
     assert res["x"] <= 1e-7, res
-    assert min(res["owned"][1:]) > 0  # both ranks own part of every partitioned level
+    assert min(res["owned"][1:]) > 0  # rank 0 owns part of every partitioned level
 
 
 def test_partition_morton_and_dof_owner():
@@ -115,3 +118,21 @@ def test_partition_morton_and_dof_owner():
         for g in sp.cell_dofs[c]:
             first[g] = min(first[g], c)
     assert np.array_equal(do, own[first])
+
+
+def test_partition_matching_follows_the_finer_level():
+    """metrics.py:41-46: each coarse cell takes the rank of the fine cell
+    containing its centroid; on nested box meshes that is the Morton owner
+    of its children."""
+    from paper_2412_10910_b200 import distributed, mesh
+
+    fine = mesh.structured_box_mesh((8, 8), [(0, 1), (0, 1)])
+    coarse = mesh.structured_box_mesh((4, 4), [(0, 1), (0, 1)])
+    fo = distributed.partition_morton(fine, 4)
+
+    def locate(m, pts):  # exact location on the uniform fine grid
+        ij = np.minimum((pts * 8).astype(int), 7)
+        return ij[:, 0] + 8 * ij[:, 1]
+
+    co = distributed.partition_matching(coarse, fine, fo, locate)
+    assert np.array_equal(co, distributed.partition_morton(coarse, 4))
