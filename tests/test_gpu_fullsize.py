@@ -1,27 +1,54 @@
-"""Parity at the BASELINE full sizes (C3: 16.97M DoFs, C5: 6.5M DoFs).
+"""Parity at the BASELINE full sizes (C1 16.6k ... C3/C4 16.97M DoFs) against
+pins the REFERENCE computed at those sizes (tests/golden/full_<C>.npz, written
+by tests/golden/make_fullsize_pins.py in the build container):
 
-The CPU oracle cannot run these sizes whole, so the GPU path is checked on
-sampled rows against the oracle restricted to the touched cells, plus
-size-independent properties: symmetry, exact transpose, bitwise determinism
-of the restriction, V-cycle symmetry, and CG convergence to 1e-8."""
+* index maps bit-exact: SHA-256 of every level's cell_dofs and constraint
+  list, and of every transfer's point_dofs, owning cells and projected flags;
+* the finest apply, diagonal, body-load vector, prolongation and restriction
+  at 1e-11 (strided samples / whole coarse vectors);
+* the outer PCG iteration count within +-1 of the reference's, with the
+  reference's coarse CG (parity mode) and with the direct coarse solve the
+  bench uses; V-cycle of b and lambda_max per level.
+
+Plus size-independent properties: symmetry, exact transpose, bitwise
+determinism of the restriction, V-cycle symmetry, convergence to 1e-8."""
+
+import hashlib
+import os
 
 import numpy as np
 import pytest
 
+from conftest import GOLDEN
+
 pytestmark = pytest.mark.gpu
 
 torch = pytest.importorskip("torch")
+
+CONFIGS = ["C1", "C2", "C3", "C4", "C5"]
 
 
 def rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
-@pytest.fixture(scope="module", params=["C3", "C5"])
+def sha(a, dtype="<i8"):
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(a), dtype=dtype).tobytes()).hexdigest()
+
+
+def pins_of(name):
+    path = os.path.join(GOLDEN, f"full_{name}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing reference pins {path}")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.fixture(scope="module", params=CONFIGS)
 def full(request):
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device")
-    from paper_2412_10910_b200 import configs, mfoperator, multigrid
+    from paper_2412_10910_b200 import configs, multigrid
 
     cfg = configs.get_config(request.param)
     meshes = cfg.make_meshes(scale=1, validate=False)
@@ -29,28 +56,77 @@ def full(request):
                                      lame=cfg.lame,
                                      config=multigrid.HierarchyConfig(chebyshev_degree=cfg.chebyshev_degree))
     b = H.finest.operator.load_vector(cfg.body_force if cfg.body_force else 1.0)
-    yield cfg, H, b
+    yield cfg, H, b, pins_of(request.param)
     del H
     torch.cuda.empty_cache()
 
 
-def test_fullsize_apply_sampled_rows_vs_oracle(full, oracle):
-    cfg, H, _ = full
+def test_fullsize_index_maps_bit_exact(full):
+    cfg, H, _, pin = full
+    for l, lev in enumerate(H.levels):
+        assert lev.operator.n_dofs == int(pin[f"l{l}_n_dofs"])
+        assert sha(lev.space.cell_dofs) == str(pin[f"l{l}_cell_dofs_sha"]), f"cell_dofs level {l}"
+        assert sha(lev.space.constraints.dofs) == str(pin[f"l{l}_cdofs_sha"]), f"constraints level {l}"
+    for i, T in enumerate(H.transfers):
+        assert len(T.cells) == int(pin[f"t{i}_npts"])
+        assert sha(T.point_dofs) == str(pin[f"t{i}_point_dofs_sha"]), f"point_dofs transfer {i}"
+        assert sha(T.cells) == str(pin[f"t{i}_cells_sha"]), f"owning cells transfer {i}"
+        assert sha(T.projected, "u1") == str(pin[f"t{i}_projected_sha"]), f"projected transfer {i}"
+        assert int(T.projected.sum()) == int(pin[f"t{i}_n_projected"])
+        st = int(pin[f"t{i}_xhat_stride"])
+        assert np.abs(T.xhat[::st] - pin[f"t{i}_xhat"]).max() <= 1e-9
+
+
+def test_fullsize_apply_diag_rhs_transfers(full):
+    cfg, H, b, pin = full
     op = H.finest.operator
-    sp = H.finest.space
     n = op.n_dofs
-    rng = np.random.default_rng(0)
-    u = rng.standard_normal(n)
-    v = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
-    rows = np.concatenate([rng.choice(n, 150, replace=False), sp.constraints.dofs[:10]])
-    want = oracle.sampled_apply_rows(sp.mesh.vertices, sp.mesh.cells, np.asarray(sp.cell_dofs), sp.constraints.dofs,
-                                     sp.degree, rows, u, cfg.problem, *(cfg.lame or (1.0, 1.0)),
-                                     ncomp=sp.n_components)
-    assert rel(v[rows], want) <= 1e-11
+    u = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).cuda()
+    v = op.apply(u).cpu().numpy()
+    st = int(pin["apply_stride"])
+    assert rel(v[::st], pin["apply"]) <= 1e-11
+    assert abs(np.linalg.norm(v) / float(pin["apply_norm"]) - 1.0) <= 1e-11
+    assert rel(op.diagonal()[::st], pin["diag"]) <= 1e-12
+    rs = int(pin["rhs_stride"])
+    assert rel(b.cpu().numpy()[::rs], pin["rhs"]) <= 1e-12
+    assert abs(float(b.norm()) / float(pin["rhs_norm"]) - 1.0) <= 1e-12
+    T = H.transfers[-1]
+    rng = np.random.default_rng(1)
+    uc = rng.standard_normal(T.coarse_space.n_dofs)
+    rf = rng.standard_normal(T.fine_space.n_dofs)
+    pu = T.prolongate(torch.from_numpy(uc).cuda()).cpu().numpy()
+    ps = int(pin["prolongate_stride"])
+    assert rel(pu[::ps], pin["prolongate"]) <= 1e-11
+    assert abs(np.linalg.norm(pu) / float(pin["prolongate_norm"]) - 1.0) <= 1e-11
+    rc = T.restrict(torch.from_numpy(rf).cuda()).cpu().numpy()
+    assert rel(rc, pin["restrict"]) <= 1e-11
+
+
+@pytest.mark.parametrize("coarse", ["cg", "direct"])
+def test_fullsize_solve_iterations_match_reference(full, coarse):
+    cfg, H, b, pin = full
+    if "iterations" not in pin:
+        pytest.skip(f"{cfg.name}: the reference's full-size solve does not fit the build container's 62 GB "
+                    "(maps, apply and transfers are pinned)")
+    from paper_2412_10910_b200 import solvers
+
+    if coarse == "direct" and not H.coarse_solver.dense:
+        # the bench's coarse solver: exact, swapped in on the same levels
+        H.coarse_solver = solvers.CoarseSolver(H.levels[0].operator, direct=True)
+        H._vc = None
+    lam = np.array([lev.smoother.lam_max for lev in H.levels])
+    assert np.allclose(lam, pin["lam_max"], rtol=1e-9)
+    z = H.precondition(b).cpu().numpy()
+    st = int(pin["vcycle_stride"])
+    assert rel(z[::st], pin["vcycle"]) <= (1e-8 if coarse == "cg" or H.coarse_solver.dense else 1e-5)
+    res = solvers.cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
+    assert res.converged
+    assert abs(res.iterations - int(pin["iterations"])) <= 1, (res.iterations, int(pin["iterations"]))
+    assert rel(res.x.cpu().numpy()[:: int(pin["x_stride"])], pin["x"]) <= 1e-6
 
 
 def test_fullsize_apply_symmetry(full):
-    _, H, _ = full
+    _, H, _, _ = full
     op = H.finest.operator
     rng = np.random.default_rng(4)
     u = torch.from_numpy(rng.standard_normal(op.n_dofs)).cuda()
@@ -60,22 +136,12 @@ def test_fullsize_apply_symmetry(full):
     assert abs(lhs - rhs) <= 1e-11 * float(au.norm() * w.norm())
 
 
-def test_fullsize_transfer_sampled_and_transpose(full, oracle):
-    cfg, H, _ = full
+def test_fullsize_transfer_transpose_and_determinism(full):
+    _, H, _, _ = full
     T = H.transfers[-1]
-    sc, sf = T.coarse_space, T.fine_space
-    ncomp = sf.n_components
     rng = np.random.default_rng(1)
-    uc = rng.standard_normal(sc.n_dofs)
-    uf = T.prolongate(torch.from_numpy(uc).cuda()).cpu().numpy()
-    pick = rng.choice(len(T.point_dofs), 2000, replace=False)
-    want = oracle.sampled_prolongate(np.asarray(sc.cell_dofs), sc.constraints.dofs, sc.degree, sc.mesh.dim,
-                                     T.cells[pick], T.xhat[pick], uc, ncomp)
-    got = uf.reshape(-1, ncomp)[T.point_dofs[pick]]
-    assert rel(got, want) <= 1e-11
-    # exact transpose: (P u).r == u.(P^T r)
-    r = torch.from_numpy(rng.standard_normal(sf.n_dofs)).cuda()
-    u = torch.from_numpy(uc).cuda()
+    r = torch.from_numpy(rng.standard_normal(T.fine_space.n_dofs)).cuda()
+    u = torch.from_numpy(rng.standard_normal(T.coarse_space.n_dofs)).cuda()
     a = float(torch.dot(T.prolongate(u), r))
     rc = T.restrict(r)
     b = float(torch.dot(u, rc))
@@ -83,23 +149,20 @@ def test_fullsize_transfer_sampled_and_transpose(full, oracle):
     assert torch.equal(rc, T.restrict(r))  # deterministic restriction, bitwise
 
 
-def test_fullsize_vcycle_symmetry_and_solve(full):
-    cfg, H, b = full
+def test_fullsize_vcycle_symmetry_and_residual(full):
+    cfg, H, b, _ = full
     n = H.finest.operator.n_dofs
     rng = np.random.default_rng(2)
     u = torch.from_numpy(rng.standard_normal(n)).cuda()
     w = torch.from_numpy(rng.standard_normal(n)).cuda()
-    # symmetrised inputs: constrained entries zero (the V-cycle acts on residuals)
     cd = torch.from_numpy(H.finest.space.constraints.dofs).cuda()
     u[cd] = 0.0
     w[cd] = 0.0
-    mu, mw = H.precondition(u), H.precondition(w)
+    mu, mw = H.precondition(u).clone(), H.precondition(w).clone()
     lhs, rhs = float(torch.dot(mu, w)), float(torch.dot(u, mw))
     assert abs(lhs - rhs) <= 1e-9 * (float(mu.norm() * w.norm()) + float(u.norm() * mw.norm()))
     from paper_2412_10910_b200 import solvers
 
     res = solvers.cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
-    assert res.converged and res.iterations <= 14
-    x = res.x
-    r = b - H.finest.operator.apply(x)
-    assert float(r.norm()) <= 1.01e-8 * float(b.norm())
+    r = b - H.finest.operator.apply(res.x)
+    assert res.converged and float(r.norm()) <= 1.01e-8 * float(b.norm())
