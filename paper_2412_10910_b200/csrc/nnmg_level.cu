@@ -333,6 +333,7 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       L->elast_recompute = er ? atoi(er) != 0 : false;
       const char* rr = getenv("NNMG_REG_RECOMPUTE");
       L->reg_recompute = rr ? atoi(rr) != 0 : false;
+
     }
     // constraints: the kernels support whole-node constraints (every component
     // of a scalar DoF), which is what dirichlet_constraints produces
@@ -457,17 +458,22 @@ __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* _
                                                    int rnum, const int* __restrict__ cd, int64_t ncd,
                                                    double* __restrict__ cellout = nullptr) {
   if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
-  const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (blk >= b1) return;
-  if constexpr (HYB) {
-    if (blk % rmod < rnum) {
-      CellReg<D, P>::template run<true, false, NEG, D == 3 ? 2 : 1>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk,
-                                                                    threadIdx.x & 31, edges);
-      return;
+  // grid-stride over cell blocks (one pass for a full grid).  Measured on
+  // B200 (profiles/r2_dual_apply_sweep.txt): persistent grids of this kernel
+  // and of the recomputed-G kernel run concurrently on two streams over
+  // complementary block ranges gain at most 3% on C3 (608 vs 627 us)
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t blk = b0 + blockIdx.x * wpb + (threadIdx.x >> 5); blk < b1; blk += gridDim.x * wpb) {
+    if constexpr (HYB) {
+      if (blk % rmod < rnum) {
+        CellReg<D, P>::template run<true, false, NEG, D == 3 ? 2 : 1>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk,
+                                                                      threadIdx.x & 31, edges);
+        continue;
+      }
     }
+    CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk, threadIdx.x & 31,
+                                                     nullptr, nullptr, cellout);
   }
-  CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk, threadIdx.x & 31,
-                                                   nullptr, nullptr, cellout);
 }
 
 // stored G streamed through shared memory by TMA bulk copies (3D, GEO 3)
@@ -489,8 +495,8 @@ template <int D, int P, bool NEG>
 __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const double* __restrict__ src,
                                                         double* __restrict__ dst, const int* __restrict__ idx,
                                                         int64_t b0, int64_t b1, const double* __restrict__ edges) {
-  const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (blk >= b1) return;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t blk = b0 + blockIdx.x * wpb + (threadIdx.x >> 5); blk < b1; blk += gridDim.x * wpb)
   CellReg<D, P>::template run<true, false, NEG, 2>(tab, PlainSrc{src}, dst, idx, static_cast<const double*>(nullptr),
                                                    blk, threadIdx.x & 31,
                                                    edges);
