@@ -28,6 +28,7 @@ struct Level {
   bool apply_recompute = false; // pencil apply: G recomputed from edge vectors (3D Laplace Q3/Q4)
   bool reg_recompute = false;   // register apply: G recomputed from edge vectors (3D Laplace Q1/Q2)
   bool elast_recompute = false; // elasticity register apply (3D Q2): J^-1, |det J| from edge vectors
+  bool elast_xch = true;        // elasticity register apply: node-major gather/scatter via shared memory
   bool reg_tma = false;         // register apply (3D): G streamed through shared memory by TMA bulk copies
   bool fuse_constrained = true;  // register kernels handle the constrained rows in their prologue
   int reg_minb = 1;        // min CTAs/SM launch bound of that kernel (4 caps registers at 128: spills)
