@@ -213,7 +213,37 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle (NumPy port of the reference path) on a sample
 # ---------------------------------------------------------------------------
-def cpu_vcycle_rate(cfg, scale, seconds, steps=None, warmup=1, barrier=None):
+def _cpu_hierarchy(cfg, scale):
+    """(precondition, rhs, n_dofs, kind): the reference's own NumPy hierarchy
+    (oracle/_ref, installed by oracle/build_ref.py: kind "reference") when it
+    travelled with the repo, else the oracle port (kind "port")."""
+    from oracle import build_ref
+
+    h0 = min((hi - lo) / n for (lo, hi), n in zip(cfg.extent, cfg.level_grid(0, scale)))
+    nnmg = build_ref.import_reference()
+    if nnmg is not None:
+        import nnmg.geosearch
+        import nnmg.mfoperator
+        import nnmg.multigrid
+
+        rm = [nnmg.mesh.Mesh(m.dim, m.vertices, m.cells, m.boundary_faces, validate=False)
+              for m in cfg.make_meshes(scale=scale, validate=False)]
+        kw = dict(problem=cfg.problem, dirichlet_ids=cfg.dirichlet_ids, lame=cfg.lame,
+                  config=nnmg.multigrid.HierarchyConfig(chebyshev_degree=cfg.chebyshev_degree))
+        try:
+            H = nnmg.multigrid.build_hp_hierarchy(rm, cfg.degree, **kw)
+        except nnmg.geosearch.GeosearchError:
+            # coarse sample meshes of the curved config miss boundary points: widen
+            # the box padding to 0.1 h_coarse as SURVEY.md §8(c) prescribes
+            H = nnmg.multigrid.build_hp_hierarchy(rm, cfg.degree, search=nnmg.geosearch.SearchConfig(eps_box=0.1 * h0),
+                                                  **kw)
+        sp = H.finest.space
+        if cfg.body_force:
+            f = np.array(cfg.body_force, dtype=float)
+            b = nnmg.mfoperator.assemble_rhs(sp, lambda x: np.broadcast_to(f, (len(x), len(f))))
+        else:
+            b = nnmg.mfoperator.assemble_rhs(sp, 1.0)
+        return H.precondition, b, sp.n_dofs, "reference"
     from oracle import nnmg_oracle as O
 
     meshes = [O.jittered_mesh(cfg.level_grid(l, scale), cfg.extent, cfg.amplitude, 1000 * cfg.index + l + 1,
@@ -222,35 +252,38 @@ def cpu_vcycle_rate(cfg, scale, seconds, steps=None, warmup=1, barrier=None):
     try:
         H, spaces = O.build_hierarchy(*args)
     except O.LocateError:
-        # coarse sample meshes of the curved config miss boundary points: widen
-        # the box padding to 0.1 h_coarse as SURVEY.md §8(c) prescribes
-        h = min((hi - lo) / n for (lo, hi), n in zip(cfg.extent, cfg.level_grid(0, scale)))
-        H, spaces = O.build_hierarchy(*args, search={"eps_box": 0.1 * h})
+        H, spaces = O.build_hierarchy(*args, search={"eps_box": 0.1 * h0})
     b = O.assemble_rhs_const(spaces[-1], cfg.body_force if cfg.body_force else 1.0)
+    return H.precondition, b, spaces[-1].n_dofs, "port"
+
+
+def cpu_vcycle_rate(cfg, scale, seconds, steps=None, warmup=1, barrier=None):
+    precondition, b, n, kind = _cpu_hierarchy(cfg, scale)
     for _ in range(max(1, warmup)):
-        H.precondition(b)  # warm-up
-    n = spaces[-1].n_dofs
+        precondition(b)  # warm-up
     if barrier is not None:
         barrier.wait()  # all worker processes start timing together
     t0 = time.perf_counter()
     k = 0
     while True:
-        H.precondition(b)
+        precondition(b)
         k += 1
         el = time.perf_counter() - t0
         if (steps is not None and k >= steps) or (steps is None and el >= seconds):
             break
-    return n * k / el / 1e9, n, k, el
+    return n * k / el / 1e9, n, k, el, kind
 
 
 _THREAD_VARS = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")
+_KIND_TEXT = {"reference": "the reference's own nnmg.multigrid.MultigridHierarchy (unmodified NumPy package, oracle/_ref)",
+              "port": "NumPy oracle port of nnmg (oracle/_ref absent)"}
 
 
 def _cpu_worker(cfg_name, scale, seconds, steps, warmup, barrier, queue):
     from paper_2412_10910_b200.configs import get_config
 
-    _, n, k, el = cpu_vcycle_rate(get_config(cfg_name), scale, seconds, steps, warmup, barrier)
-    queue.put((n, k, el))
+    _, n, k, el, kind = cpu_vcycle_rate(get_config(cfg_name), scale, seconds, steps, warmup, barrier)
+    queue.put((n, k, el, kind))
 
 
 def cpu_vcycle_rate_all_cores(cfg, scale, seconds, steps=None, warmup=1, procs=None):
@@ -261,8 +294,8 @@ def cpu_vcycle_rate_all_cores(cfg, scale, seconds, steps=None, warmup=1, procs=N
 
     procs = max(1, min(procs or os.cpu_count() or 1, 32))
     if procs == 1:
-        rate, n, k, el = cpu_vcycle_rate(cfg, scale, seconds, steps, warmup)
-        return rate, n, k, el, 1
+        rate, n, k, el, kind = cpu_vcycle_rate(cfg, scale, seconds, steps, warmup)
+        return rate, n, k, el, 1, kind
     ctx = mp.get_context("spawn")
     saved = {v: os.environ.get(v) for v in _THREAD_VARS}
     for v in _THREAD_VARS:
@@ -285,24 +318,24 @@ def cpu_vcycle_rate_all_cores(cfg, scale, seconds, steps=None, warmup=1, procs=N
     n = res[0][0]
     work = sum(r[0] * r[1] for r in res)
     el = max(r[2] for r in res)
-    return work / el / 1e9, n, sum(r[1] for r in res), el, procs
+    return work / el / 1e9, n, sum(r[1] for r in res), el, procs, res[0][3]
 
 
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    rate, n, k, el, procs = cpu_vcycle_rate_all_cores(cfg, args.cpu_scale, args.cpu_seconds,
-                                                      steps=max(1, args.steps), warmup=args.warmup)
+    rate, n, k, el, procs, kind = cpu_vcycle_rate_all_cores(cfg, args.cpu_scale, args.cpu_seconds,
+                                                            steps=max(1, args.steps), warmup=args.warmup)
     sample = (f"{cfg.name} at 1/{args.cpu_scale} cells per axis ({n} fine DoFs), {k} V-cycles over {procs} "
-              f"single-threaded processes ({max(1, args.steps)} each), NumPy oracle port of nnmg")
+              f"single-threaded processes ({max(1, args.steps)} each), {_KIND_TEXT[kind]}")
     line = {
         "impl": "reference", "metric": "fp64 V-cycle GDoF/s", "value": rate, "unit": "GDoF/s", "n_gpus": 0,
         "steps": max(1, args.steps), "warmup": max(1, args.warmup), "ms_per_step": el / max(1, args.steps) * 1e3,
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SURVEY §8(d) meshes)",
         "config": {"workload": CONFIG_TEXT[cfg.name] + f" (CPU sample 1/{args.cpu_scale})", "config": cfg.name},
-        "cpu_baseline": {"value": rate, "unit": "GDoF/s", "cores": procs, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": "GDoF/s", "cores": procs, "kind": kind, "sample": sample},
         "e2e": {"value": rate, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -627,11 +660,11 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, ncpu, k, el, procs = cpu_vcycle_rate_all_cores(cfg, args.cpu_scale, args.cpu_seconds)
-        cpu = {"value": rate, "unit": "GDoF/s", "cores": procs, "kind": "port",
+        rate, ncpu, k, el, procs, kind = cpu_vcycle_rate_all_cores(cfg, args.cpu_scale, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "GDoF/s", "cores": procs, "kind": kind,
                "sample": f"{cfg.name} at 1/{args.cpu_scale} cells per axis ({ncpu} fine DoFs), {k} V-cycles in "
-                         f"{el:.1f} s over {procs} single-threaded processes (one per host core), NumPy oracle "
-                         f"port of nnmg"}
+                         f"{el:.1f} s over {procs} single-threaded processes (one per host core), "
+                         f"{_KIND_TEXT[kind]}"}
 
     if rank == 0:
         clocks = clk.summary()
