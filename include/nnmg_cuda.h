@@ -73,6 +73,18 @@ int nnmg_level_info(nnmg_level_t level, int64_t* n_dofs, int64_t* n_cells, int* 
  * replaces LaplaceOperator.apply (mfoperator.py:108-122) and
  * ElasticityOperator.apply (mfoperator.py:171-202) */
 int nnmg_level_apply(nnmg_level_t level, const double* src_dev, double* dst_dev, void* stream);
+/* the same apply in pieces, for the distributed levels (overlap
+ * interior cells with the ghost exchange).  begin: dst = 0 plus identity-out on
+ * the constrained rows; cells: dst += contributions of the cell blocks
+ * [block0, block1) (blocks of `cells_per_block` consecutive cells, see
+ * nnmg_level_info) to the free rows.  begin + cells(0, n_blocks) == apply.
+ * negate != 0: the residual form dst -= A src of the smoother and the
+ * V-cycle residual (solvers.py:97, 102; multigrid.py:97): begin subtracts src
+ * on the constrained rows and leaves the rest of dst alone, cells subtracts.
+ * Not available in deterministic mode (status 3). */
+int nnmg_level_apply_begin(nnmg_level_t level, const double* src_dev, double* dst_dev, int negate, void* stream);
+int nnmg_level_apply_cells(nnmg_level_t level, const double* src_dev, double* dst_dev, int64_t block0,
+                           int64_t block1, int negate, void* stream);
 /* r_dev = f_dev - A x_dev   (multigrid.py:97) */
 int nnmg_level_residual(nnmg_level_t level, const double* f_dev, const double* x_dev, double* r_dev, void* stream);
 /* compute/cache the exact diagonal and its inverse; copy it out
@@ -98,9 +110,10 @@ int nnmg_smoother_sweep(nnmg_level_t level, double lam_max, double lam_min, int 
                         const double* x0_dev, double* x_dev, double* work_dev, void* stream);
 
 /* fused Chebyshev vector updates for externally applied operators (the
- * distributed smoother): start  r = b - Ax (ax may be NULL: r = b),
- * d = inv_diag*r/theta, x = x0 + d (x0 may be NULL);  step  r -= Ad,
- * d = c1 d + c2 inv_diag r, x += d   (solvers.py:94-107) */
+ * distributed smoother): start  r = b - Ax (ax may be NULL: r = b; b may be
+ * NULL: r already holds the residual), d = inv_diag*r/theta, x = x0 + d (x0
+ * may be NULL);  step  r -= Ad (ad may be NULL: the apply already subtracted
+ * it in place), d = c1 d + c2 inv_diag r, x += d   (solvers.py:94-107) */
 int nnmg_cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag,
                     double theta, double* r, double* d, double* x, void* stream);
 int nnmg_cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
@@ -137,6 +150,14 @@ int nnmg_transfer_prolongate(nnmg_transfer_t transfer, const double* uc_dev, dou
                              void* stream);
 /* rc = P^T rf, deterministic (restrict, transfer.py:46-58, 104-124) */
 int nnmg_transfer_restrict(nnmg_transfer_t transfer, const double* rf_dev, double* rc_dev, void* stream);
+/* per-phase timing rows: replaces timings["evaluate"] / timings["gather_scatter"]
+ * (transfer.py:29, 100-101, 122-123).  While enabled, prolongate / restrict
+ * record CUDA events around the point-evaluation kernel ("evaluate") and around
+ * the zero-fill of point-less DoFs / the fixed-order coarse gather
+ * ("gather_scatter"); last_timing synchronises on the last call and returns
+ * seconds.  Leave it off for calls inside a CUDA-graph capture. */
+int nnmg_transfer_set_timing(nnmg_transfer_t transfer, int enable);
+int nnmg_transfer_last_timing(nnmg_transfer_t transfer, double* evaluate_s, double* gather_scatter_s);
 
 /* ---- point location: replaces locate_points (geosearch.py:163-227) with its
  * tie-break and projection rules.  Outputs are host arrays of n_points.

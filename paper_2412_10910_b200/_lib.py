@@ -46,6 +46,8 @@ _SIGNATURES = {
     "nnmg_level_destroy": [_handle],
     "nnmg_level_info": [_handle, _p_int64, _p_int64, POINTER(c_int), _p_int64, _p_int64],
     "nnmg_level_apply": [_handle, c_void_p, c_void_p, c_void_p],
+    "nnmg_level_apply_begin": [_handle, c_void_p, c_void_p, c_int, c_void_p],
+    "nnmg_level_apply_cells": [_handle, c_void_p, c_void_p, c_int64, c_int64, c_int, c_void_p],
     "nnmg_level_residual": [_handle, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_level_compute_diagonal": [_handle, c_void_p],
     "nnmg_level_diagonal": [_handle, c_void_p, c_void_p],
@@ -64,6 +66,8 @@ _SIGNATURES = {
     "nnmg_transfer_destroy": [_handle],
     "nnmg_transfer_prolongate": [_handle, c_void_p, c_void_p, c_int, c_void_p],
     "nnmg_transfer_restrict": [_handle, c_void_p, c_void_p, c_void_p],
+    "nnmg_transfer_set_timing": [_handle, c_int],
+    "nnmg_transfer_last_timing": [_handle, POINTER(c_double), POINTER(c_double)],
     "nnmg_locate_points": [c_int, c_int, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_double,
                            c_double, c_double, c_void_p, c_void_p, c_void_p, _p_int64, _p_int64],
     "nnmg_coarse_dense_create": [_handle, c_void_p, POINTER(_handle)],

@@ -89,6 +89,21 @@ int nnmg_level_apply(nnmg_level_t level, const double* src, double* dst, void* s
   });
 }
 
+int nnmg_level_apply_begin(nnmg_level_t level, const double* src, double* dst, int negate, void* stream) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    level_apply_begin(*LV(level), src, dst, negate != 0, S(stream));
+  });
+}
+
+int nnmg_level_apply_cells(nnmg_level_t level, const double* src, double* dst, int64_t block0, int64_t block1,
+                           int negate, void* stream) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    level_apply_cells(*LV(level), src, dst, block0, block1, negate != 0, S(stream));
+  });
+}
+
 int nnmg_level_residual(nnmg_level_t level, const double* f, const double* x, double* r, void* stream) {
   return guard([&] {
     REQUIRE_HANDLE(level);
@@ -183,6 +198,20 @@ int nnmg_transfer_prolongate(nnmg_transfer_t transfer, const double* uc, double*
   return guard([&] {
     REQUIRE_HANDLE(transfer);
     transfer_prolongate(*TR(transfer), uc, uf, accumulate != 0, S(stream));
+  });
+}
+
+int nnmg_transfer_set_timing(nnmg_transfer_t transfer, int enable) {
+  return guard([&] {
+    REQUIRE_HANDLE(transfer);
+    transfer_set_timing(*TR(transfer), enable != 0);
+  });
+}
+
+int nnmg_transfer_last_timing(nnmg_transfer_t transfer, double* evaluate_s, double* gather_scatter_s) {
+  return guard([&] {
+    REQUIRE_HANDLE(transfer);
+    transfer_last_timing(*TR(transfer), evaluate_s, gather_scatter_s);
   });
 }
 

@@ -860,6 +860,36 @@ void level_apply(Level& L, const double* src, double* dst, cudaStream_t s) {
   if (!launch_apply_all(L, src, dst, s, false)) launch_copy_constrained(L, src, dst, s);
 }
 
+// Partial applies for the distributed levels: the interior
+// cell blocks run while the ghost import is in flight on another stream, the
+// boundary blocks after it.  begin: dst = 0 and identity-out on the constrained
+// rows; cells: dst += sum over the cell blocks [b0, b1) (free rows only).
+// negate: the residual form dst -= A src (begin subtracts src on the
+// constrained rows and does not zero dst).
+void level_apply_begin(Level& L, const double* src, double* dst, bool negate, cudaStream_t s) {
+  NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
+  if (negate) {
+    // residual form dst -= A src: identity-out rows subtract src
+    const int64_t n = static_cast<int64_t>(L.cdofs.n);
+    if (n) {
+      k_sub_constrained<double><<<grid_for(n, 256), 256, 0, s>>>(L.cdofs.ptr, n, src, dst);
+      NNMG_CHECK_LAUNCH();
+      count_launch();
+    }
+    return;
+  }
+  NNMG_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(double) * L.n_dofs, s));
+  launch_copy_constrained(L, src, dst, s);
+}
+
+void level_apply_cells(Level& L, const double* src, double* dst, int64_t b0, int64_t b1, bool negate,
+                       cudaStream_t s) {
+  NNMG_REQUIRE(src != dst, kInvalidArgument, "apply needs distinct source and destination");
+  NNMG_REQUIRE(0 <= b0 && b0 <= b1 && b1 <= L.nblk, kInvalidArgument, "cell block range out of bounds");
+  NNMG_REQUIRE(!L.deterministic, kUnsupported, "partial applies are not available in deterministic mode");
+  launch_apply_cells(L, src, dst, b0, b1, s, negate);
+}
+
 struct DiagLaunch {
   Level& L;
   cudaStream_t s;

@@ -55,6 +55,10 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
 
 // v = A u with zero-in / identity-out constraint convention (mfoperator.py:108-122)
 void level_apply(Level& L, const double* src, double* dst, cudaStream_t s);
+// partial applies (distributed levels): zero + constrained rows, then cell-block ranges
+void level_apply_begin(Level& L, const double* src, double* dst, bool negate, cudaStream_t s);
+void level_apply_cells(Level& L, const double* src, double* dst, int64_t b0, int64_t b1, bool negate,
+                       cudaStream_t s);
 // exact diagonal, constrained = 1 (mfoperator.py:92-95, 135-150, 219-238)
 void level_compute_diagonal(Level& L, cudaStream_t s);
 

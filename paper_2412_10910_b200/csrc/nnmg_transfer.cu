@@ -46,6 +46,7 @@ struct TransferDispatchT {
       NNMG_CHECK_LAUNCH();
       count_launch();
     } else {
+      if (T.timing) NNMG_CUDA_TRY(cudaEventRecord(T.ev[0], s));
       const int ch = T.chunk;
       const int64_t nwarps = (T.nitems + ch - 1) / ch;
       constexpr int W = StagedRestrict<D, P, NC>::WARPS;
@@ -80,10 +81,15 @@ struct TransferDispatchT {
             C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
       }
       NNMG_CHECK_LAUNCH();
+      if (T.timing) NNMG_CUDA_TRY(cudaEventRecord(T.ev[1], s));
       k_restrict_gather<TV><<<grid_for(C.n_scalar, 256), 256, 0, s>>>(T.t_off.ptr, T.t_ent.ptr, T.cellbuf.ptr,
                                                                        C.n_scalar, NC, out);
       NNMG_CHECK_LAUNCH();
       count_launch(2);
+      if (T.timing) {
+        NNMG_CUDA_TRY(cudaEventRecord(T.ev[2], s));
+        T.ev_eval = 0;
+      }
     }
   }
 };
@@ -210,6 +216,7 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
 
 template <class TV>
 static void prolongate_t(Transfer& T, const TV* uc, TV* uf, bool accumulate, cudaStream_t s) {
+  if (T.timing) NNMG_CUDA_TRY(cudaEventRecord(T.ev[0], s));
   if (!accumulate) {
     // every point DoF is written below; only the point-less ones need zeros
     const int64_t n = int64_t(T.no_point.n) * T.ncomp;
@@ -219,8 +226,37 @@ static void prolongate_t(Transfer& T, const TV* uc, TV* uf, bool accumulate, cud
       count_launch();
     }
   }
+  if (T.timing) NNMG_CUDA_TRY(cudaEventRecord(T.ev[1], s));
   TransferDispatchT<TV> f{T, uc, uf, accumulate ? 1 : 0, s};
   dispatch(T.dim, T.pc, T.ncomp, T.coarse->physics, f);
+  if (T.timing) {
+    NNMG_CUDA_TRY(cudaEventRecord(T.ev[2], s));
+    T.ev_eval = 1;
+  }
+}
+
+Transfer::~Transfer() {
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+}
+
+void transfer_set_timing(Transfer& T, bool on) {
+  if (on && !T.ev[0]) {
+    NNMG_CUDA_TRY(cudaSetDevice(T.coarse->device));
+    for (auto& e : T.ev) NNMG_CUDA_TRY(cudaEventCreate(&e));
+  }
+  T.timing = on;
+}
+
+void transfer_last_timing(Transfer& T, double* evaluate_s, double* gather_scatter_s) {
+  NNMG_REQUIRE(T.ev[0], kInvalidArgument, "transfer timing was never enabled");
+  NNMG_CUDA_TRY(cudaEventSynchronize(T.ev[2]));
+  float a = 0.f, b = 0.f;
+  NNMG_CUDA_TRY(cudaEventElapsedTime(&a, T.ev[0], T.ev[1]));
+  NNMG_CUDA_TRY(cudaEventElapsedTime(&b, T.ev[1], T.ev[2]));
+  const double ev = (T.ev_eval == 0 ? a : b) * 1e-3, gs = (T.ev_eval == 0 ? b : a) * 1e-3;
+  if (evaluate_s) *evaluate_s = ev;
+  if (gather_scatter_s) *gather_scatter_s = gs;
 }
 
 void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s) {

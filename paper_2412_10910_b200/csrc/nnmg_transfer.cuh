@@ -26,6 +26,14 @@ struct Transfer {
   DevBuf<double> cellbuf;   // [nitems][nloc][ncomp] restriction partial local vectors
   DevBuf<int> t_off, t_ent; // coarse DoF -> (cell*nloc + l) entries, fixed order
   DevBuf<int> no_point;     // fine scalar DoFs without a point (zero in P u_c)
+  // per-phase timing rows (the reference's timings["evaluate"] /
+  // ["gather_scatter"], transfer.py:29, 100-101, 122-123): events around the
+  // point-evaluation kernel and around the zero-fill / fixed-order gather;
+  // off on the V-cycle path (events cannot be recorded into a graph capture)
+  bool timing = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  int ev_eval = 0;          // the evaluation kernel ran between ev[ev_eval] and ev[ev_eval + 1]
+  ~Transfer();
 };
 
 Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_t* point_dofs, const int64_t* cells,
@@ -34,6 +42,10 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
 void transfer_prolongate(Transfer& T, const double* uc, double* uf, bool accumulate, cudaStream_t s);
 // r_c = P^T r_f, deterministic two-phase segmented reduction (transfer.py:46-58, 104-124)
 void transfer_restrict(Transfer& T, const double* rf, double* rc, cudaStream_t s);
+// enable / read the per-phase timers of the last prolongate / restrict call
+// (seconds; synchronises on the call's last event)
+void transfer_set_timing(Transfer& T, bool on);
+void transfer_last_timing(Transfer& T, double* evaluate_s, double* gather_scatter_s);
 // mixed-precision V-cycle: fp32 xhat copy, fp32 vectors (fp64 arithmetic)
 void transfer_enable_f32(Transfer& T, cudaStream_t s);
 void transfer_prolongate_f32(Transfer& T, const float* uc, float* uf, bool accumulate, cudaStream_t s);

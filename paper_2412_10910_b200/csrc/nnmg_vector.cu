@@ -10,14 +10,15 @@ static constexpr int kBS = 256;
 static inline unsigned grid_for(int64_t n) { return static_cast<unsigned>((n + kBS - 1) / kBS); }
 
 // r = b - Ax (or b); d = inv_diag*r/theta; x = x0 + d (or d)       (solvers.py:94-100)
-__global__ void k_cheb_start(int64_t n, const double* __restrict__ b, const double* __restrict__ ax,
-                             const double* __restrict__ x0, const double* __restrict__ inv_diag, double theta,
-                             double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
+__global__ void k_cheb_start(int64_t n, const double* b, const double* __restrict__ ax,
+                             const double* x0, const double* __restrict__ inv_diag, double theta,
+                             double* r, double* __restrict__ d, double* x) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double ri = ax ? b[i] - ax[i] : b[i];
+  // b == nullptr: r already holds the residual (the in-place form r -= A x0)
+  const double ri = b ? (ax ? b[i] - ax[i] : b[i]) : r[i];
   const double di = inv_diag[i] * ri / theta;
-  r[i] = ri;
+  if (b) r[i] = ri;
   d[i] = di;
   x[i] = x0 ? x0[i] + di : di;
 }
@@ -28,10 +29,11 @@ __global__ void k_cheb_step(int64_t n, const double* __restrict__ ad, const doub
                             double* __restrict__ x) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double ri = r[i] - ad[i];
+  // ad == nullptr: the apply already subtracted A d from r in place
+  const double ri = ad ? r[i] - ad[i] : r[i];
   const double z = inv_diag[i] * ri;
   const double di = c1 * d[i] + c2 * z;
-  r[i] = ri;
+  if (ad) r[i] = ri;
   d[i] = di;
   x[i] += di;
 }

@@ -12,6 +12,11 @@ One process per GPU with ``torch.distributed`` (NCCL) for the plumbing:
 * **Apply.** Import the ghost values (halo), run the local cell loop (the GPU
   kernels), then export-add the ghost partial sums to their owners.
   Constrained ghosts are never exported; the owner applies identity-out.
+  A rank's cells are ordered interior first (every DoF owned), boundary last:
+  the interior cell blocks run on the compute stream while the ghost import
+  (pack kernel, NCCL point-to-point, unpack kernel) is in flight on a side
+  stream; the boundary blocks wait for it (SURVEY §8(e) "overlap interior
+  cells with the exchange").
 * **Transfers.** Fine points are owned. Prolongation imports the coarse ghosts
   first. Restriction export-adds the coarse ghost partials; on the replicated
   coarsest level it all-reduces them.
@@ -96,6 +101,11 @@ def dof_owner_ranks(cell_dofs, cell_owner, n_scalar):
 # ---------------------------------------------------------------------------
 
 
+# cells per block of the level handles (nnmg_level_info: 32 for every
+# supported element); the interior / boundary split is aligned to it
+CELL_ALIGN = 32
+
+
 class LevelLayout:
     """Local numbering of one level on one rank: owned DoFs, then ghosts."""
 
@@ -105,13 +115,20 @@ class LevelLayout:
         self.replicated = replicated
         self.n_global_scalar = space.n_scalar_dofs
         cell_dofs = np.asarray(space.cell_dofs)
+        self.n_interior_cells = 0
         if replicated:
             self.owned_cells = np.arange(len(cell_dofs))
             self.owned = np.arange(space.n_scalar_dofs)
             self.ghosts = np.zeros(0, dtype=np.int64)
             self.cell_ghosts = self.ghosts
         else:
-            self.owned_cells = np.nonzero(cell_owner == rank)[0]
+            oc = np.nonzero(cell_owner == rank)[0]
+            # interior cells (no ghost DoF) first, boundary cells last, both in
+            # ascending global order; the interior count is cut to whole cell
+            # blocks so the two groups are block ranges of the level handle
+            bnd = (dof_owner[cell_dofs[oc]] != rank).any(axis=1)
+            self.owned_cells = np.concatenate([oc[~bnd], oc[bnd]])
+            self.n_interior_cells = (int((~bnd).sum()) // CELL_ALIGN) * CELL_ALIGN
             self.owned = np.nonzero(dof_owner == rank)[0]
             touched = np.unique(cell_dofs[self.owned_cells])
             self.cell_ghosts = touched[dof_owner[touched] != rank]
@@ -270,7 +287,10 @@ class DistLevel:
         self.exp = export_plan
         self.n = layout.n_local_full
         self.n_owned = layout.n_owned_full
+        self.overlap = True  # interior cells overlap the ghost import (False: import, then all cells)
         self._t = backend.zeros(self.n)
+        self._r = backend.zeros(self.n)  # smoother work vectors (fixed addresses: graph capture)
+        self._d = backend.zeros(self.n)
         d = backend.diagonal_partial(op)
         if self.exp is not None:
             halo_export_add(self.exp, d)
@@ -280,13 +300,51 @@ class DistLevel:
         self.inv_diag = 1.0 / d  # owned entries are exact; ghost entries are never read
         self.lam_max = None
 
+    def _split_cells(self, x, y, negate):
+        """Local cell loop with the ghost import of x overlapped: interior
+        cells never read a ghost entry of x, so they run while the import is
+        in flight; the boundary cells follow it."""
+        n_int = self.layout.n_interior_cells
+        n_cells = len(self.layout.owned_cells)
+        self.bk.apply_begin(self.op, x, y, negate)
+        if self.imp is not None and n_int > 0:
+            self.bk.overlapped(lambda: halo_import(self.imp, x),
+                               lambda: self.bk.apply_cells(self.op, x, y, 0, n_int, negate))
+            self.bk.apply_cells(self.op, x, y, n_int, n_cells, negate)
+        else:
+            if self.imp is not None:
+                halo_import(self.imp, x)
+            self.bk.apply_cells(self.op, x, y, 0, n_cells, negate)
+
+    def _split(self):
+        return self.overlap and self.bk.can_split(self.op)
+
     def apply_into(self, x, y):
-        if self.imp is not None:
-            halo_import(self.imp, x)
-        self.bk.apply_into(self.op, x, y)
+        if self._split():
+            self._split_cells(x, y, False)
+        else:
+            if self.imp is not None:
+                halo_import(self.imp, x)
+            self.bk.apply_into(self.op, x, y)
         if self.exp is not None:
             halo_export_add(self.exp, y)
         return y
+
+    def apply_sub_into(self, x, r):
+        """r -= A x on the owned rows, in place (the residual form of the
+        smoother and of the V-cycle residual: no product vector is written and
+        read back).  The ghost rows of r are scratch: zeroed, they collect this
+        rank's partial sums, which the export adds to the owners."""
+        if not self._split():
+            self.apply_into(x, self._t)
+            self.bk.sub(r, self._t, r)
+            return r
+        if self.n > self.n_owned:
+            r[self.n_owned:].zero_()
+        self._split_cells(x, r, True)
+        if self.exp is not None:
+            halo_export_add(self.exp, r)
+        return r
 
     def dot(self, a, b):
         s = self.bk.dot(a[: self.n_owned], b[: self.n_owned])
@@ -319,17 +377,18 @@ class DistLevel:
         theta = (lam_max + lam_min) / 2.0
         delta = (lam_max - lam_min) / 2.0
         sigma = theta / delta
-        r, d, t = self.bk.zeros(self.n), self.bk.zeros(self.n), self._t
+        r, d = self._r, self._d
         if x0 is None:
             self.bk.cheb_start(b, None, None, self.inv_diag, theta, r, d, x)
         else:
-            self.apply_into(x0, t)
-            self.bk.cheb_start(b, t, x0, self.inv_diag, theta, r, d, x)
+            r.copy_(b)
+            self.apply_sub_into(x0, r)  # r = b - A x0
+            self.bk.cheb_start(None, None, x0, self.inv_diag, theta, r, d, x)
         rho_old = 1.0 / sigma
         for _ in range(degree - 1):
-            self.apply_into(d, t)
+            self.apply_sub_into(d, r)  # r -= A d
             rho = 1.0 / (2.0 * sigma - rho_old)
-            self.bk.cheb_step(t, self.inv_diag, rho * rho_old, 2.0 * rho / delta, r, d, x)
+            self.bk.cheb_step(None, self.inv_diag, rho * rho_old, 2.0 * rho / delta, r, d, x)
             rho_old = rho
         return x
 
@@ -417,15 +476,14 @@ class DistHierarchy:
             self.coarse_solve(f, x)
             return x
         T = self.transfers[l - 2]
-        x = lev.bk.zeros(lev.n)
+        x = lev.bk.empty(lev.n)  # fully written by the first sweep
         cur = None
         for _ in range(self.m1):
             lev.smooth_into(f, cur, x, self.degree, self.window)
             cur = x
-        t = lev.bk.zeros(lev.n)
-        lev.apply_into(x, t)
-        r = lev.bk.zeros(lev.n)
-        lev.bk.sub(f, t, r)
+        r = lev.bk.empty(lev.n)
+        r.copy_(f)
+        lev.apply_sub_into(x, r)  # r = f - A x (multigrid.py:97)
         rc = T.coarse.bk.zeros(T.coarse.n)
         T.restrict_into(r, rc)
         delta = self._v(l - 1, rc)
@@ -617,9 +675,13 @@ class GpuBackend:
         self.comm_device = self.device
         self._D = D
         self._ops = D.vector_ops(self.device)
+        self._side = None
 
     def zeros(self, n):
         return torch.zeros(n, dtype=torch.float64, device=self.device)
+
+    def empty(self, n):
+        return torch.empty(n, dtype=torch.float64, device=self.device)
 
     def make_operator(self, space, problem, lame):
         from .mfoperator import ElasticityOperator, LaplaceOperator
@@ -633,6 +695,30 @@ class GpuBackend:
 
     def apply_into(self, op, x, y):
         op.apply_into(x, y)
+
+    # split apply: y = 0 + constrained rows, then cell ranges (whole blocks)
+    def can_split(self, op):
+        return not op.deterministic
+
+    def apply_begin(self, op, x, y, negate=False):
+        op.apply_begin_into(x, y, negate)
+
+    def apply_cells(self, op, x, y, cell0, cell1, negate=False):
+        if cell1 > cell0:
+            op.apply_cells_into(x, y, cell0 // CELL_ALIGN, -(-cell1 // CELL_ALIGN), negate)
+
+    def overlapped(self, comm_fn, compute_fn):
+        """comm_fn on a side stream forked from the current one, compute_fn on
+        the current stream, then join (inside a graph capture the fork and the
+        join become graph dependencies)."""
+        cur = torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        self._side.wait_stream(cur)
+        with torch.cuda.stream(self._side):
+            comm_fn()
+        compute_fn()
+        cur.wait_stream(self._side)
 
     def make_transfer(self, coarse_space, fine_space, coarse_op, fine_op, records):
         from .transfer import TwoLevelTransferNonNested

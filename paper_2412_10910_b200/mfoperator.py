@@ -99,6 +99,25 @@ class _GpuOperatorBase:
         _lib.call("nnmg_level_apply", self._h, u.data_ptr(), v.data_ptr(), D.stream_ptr(self.device))
         return v
 
+    def apply_begin_into(self, u, v, negate=False):
+        """First piece of a split apply: v = 0 plus identity-out on the
+        constrained rows (the distributed levels' interior / boundary split);
+        negate: the residual form v -= A u (subtracts u on the constrained rows)."""
+        _lib.call("nnmg_level_apply_begin", self._h, u.data_ptr(), v.data_ptr(), 1 if negate else 0,
+                  D.stream_ptr(self.device))
+        return v
+
+    def apply_cells_into(self, u, v, block0, block1, negate=False):
+        """v += (negate: -=) contributions of the cell blocks [block0, block1) to the free rows."""
+        _lib.call("nnmg_level_apply_cells", self._h, u.data_ptr(), v.data_ptr(), int(block0), int(block1),
+                  1 if negate else 0, D.stream_ptr(self.device))
+        return v
+
+    @property
+    def n_cell_blocks(self):
+        i = self.info()
+        return -(-i["n_cells"] // i["cells_per_block"])
+
     def apply(self, u):
         """v = A u; new output, input untouched (mfoperator.py:108-122)."""
         ud, host = D.to_device(u, self._n, self.device)

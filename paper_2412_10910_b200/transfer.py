@@ -107,17 +107,32 @@ class TwoLevelTransferNonNested:
         _lib.call("nnmg_transfer_restrict", self._h, rf.data_ptr(), rc.data_ptr(), D.stream_ptr(self.device))
         return rc
 
+    def _timed(self, call):
+        """Run one public-path call with the library's per-phase events on and
+        add the device times to the reference's rows (transfer.py:100-101,
+        122-123): "evaluate" = the point-evaluation kernel, "gather_scatter" =
+        the zero-fill of point-less DoFs / the fixed-order coarse gather."""
+        _lib.call("nnmg_transfer_set_timing", self._h, 1)
+        try:
+            call()
+            ev, gs = ctypes.c_double(), ctypes.c_double()
+            _lib.call("nnmg_transfer_last_timing", self._h, ctypes.byref(ev), ctypes.byref(gs))
+        finally:
+            _lib.call("nnmg_transfer_set_timing", self._h, 0)
+        self.timings["evaluate"] += ev.value
+        self.timings["gather_scatter"] += gs.value
+
     def prolongate(self, u_c):
         ud, host = D.to_device(u_c, self.coarse_space.n_dofs, self.device, "coarse vector")
         out = D.empty(self.fine_space.n_dofs, self.device)
-        self.prolongate_into(ud, out)
+        self._timed(lambda: self.prolongate_into(ud, out))
         self.timings["calls"] += 1
         return D.from_device(out, host)
 
     def restrict(self, r_f):
         rd, host = D.to_device(r_f, self.fine_space.n_dofs, self.device, "fine vector")
         out = D.empty(self.coarse_space.n_dofs, self.device)
-        self.restrict_into(rd, out)
+        self._timed(lambda: self.restrict_into(rd, out))
         return D.from_device(out, host)
 
 

@@ -23,8 +23,48 @@ class OracleBackend:
     def zeros(self, n):
         return torch.zeros(n, dtype=torch.float64)
 
+    def empty(self, n):
+        return torch.full((n,), float("nan"), dtype=torch.float64)  # catches reads of unwritten entries
+
     def make_operator(self, space, problem, lame):
-        return O.OOperator(_ospace(space), problem, *(lame or (1.0, 1.0)))
+        op = O.OOperator(_ospace(space), problem, *(lame or (1.0, 1.0)))
+        op._meta = (problem, lame or (1.0, 1.0))
+        op._parts = {}
+        return op
+
+    # split apply (interior / boundary cell ranges of a distributed level)
+    def can_split(self, op):
+        return True
+
+    def apply_begin(self, op, x, y, negate=False):
+        cd = torch.from_numpy(op.space.cdofs)
+        if negate:
+            y[cd] -= x[cd]
+            return
+        y.zero_()
+        y[cd] = x[cd]
+
+    def apply_cells(self, op, x, y, cell0, cell1, negate=False):
+        if cell1 <= cell0:
+            return
+        key = (cell0, cell1)
+        if key not in op._parts:
+            sp = op.space
+            om = O.OMesh(sp.mesh.dim, sp.mesh.vertices, sp.mesh.cells[cell0:cell1], np.zeros((0, 3), np.int64))
+            sub = O.OSpace(om, sp.degree, sp.n_components, sp.cell_dofs[cell0:cell1], sp.support_points, sp.cdofs)
+            op._parts[key] = O.OOperator(sub, op._meta[0], *op._meta[1])
+        part = op._parts[key].apply(x.numpy().copy())
+        part[op.space.cdofs] = 0.0  # identity-out belongs to apply_begin
+        if negate:
+            y -= torch.from_numpy(part)
+        else:
+            y += torch.from_numpy(part)
+
+    def overlapped(self, comm_fn, compute_fn):
+        # worst-case order on CPU: the interior cells run BEFORE the ghost
+        # import, so a misclassified interior cell would read stale ghosts
+        compute_fn()
+        comm_fn()
 
     def diagonal_partial(self, op):
         return torch.from_numpy(op.diagonal())
@@ -70,12 +110,14 @@ class OracleBackend:
         y.mul_(beta).add_(alpha * x)
 
     def cheb_start(self, b, ax, x0, inv_diag, theta, r, d, x):
-        r.copy_(b - ax if ax is not None else b)
+        if b is not None:
+            r.copy_(b - ax if ax is not None else b)
         d.copy_(inv_diag * r / theta)
         x.copy_(x0 + d if x0 is not None else d)
 
     def cheb_step(self, ad, inv_diag, c1, c2, r, d, x):
-        r -= ad
+        if ad is not None:
+            r -= ad
         z = inv_diag * r
         d.copy_(c1 * d + c2 * z)
         x += d

@@ -57,6 +57,19 @@ def _worker(rank, world, port, cname, scale, q, policy="matching"):
         xg = fine.gather_global(x)
         lam = [lev.lam_max for lev in DH.levels[1:]]
         owned = [int(lev.layout.n_owned) for lev in DH.levels]
+        # interior / boundary split of this rank's cells (overlap of the ghost import)
+        interior = []
+        for lev in DH.levels[1:]:
+            lay = lev.layout
+            gh = np.zeros(lay.n_global_scalar, bool)
+            gh[lay.ghosts] = True
+            cd = np.asarray(spaces[DH.levels.index(lev)].cell_dofs)[lay.owned_cells]
+            touches = gh[cd].any(axis=1)
+            assert not touches[: lay.n_interior_cells].any()  # interior cells read no ghost
+            assert lay.n_interior_cells % distributed.CELL_ALIGN == 0
+            interior.append(int(lay.n_interior_cells))
+        all_int = [None] * world
+        dist.all_gather_object(all_int, interior)
         if rank == 0:
             # single-process oracle on the same meshes
             om = [O.jittered_mesh(m.grid, cfg.extent, cfg.amplitude, 1000 * cfg.index + l + 1, cfg.warp)
@@ -70,7 +83,8 @@ def _worker(rank, world, port, cname, scale, q, policy="matching"):
             q.put(dict(Au=np.linalg.norm(Au - ref_Au) / np.linalg.norm(ref_Au),
                        z=np.linalg.norm(z - ref_z) / np.linalg.norm(ref_z),
                        x=np.linalg.norm(xg - rx) / np.linalg.norm(rx), its=its, rits=rits, conv=conv,
-                       lam=np.max(np.abs(np.array(lam) - ref_lam) / np.array(ref_lam)), owned=owned))
+                       lam=np.max(np.abs(np.array(lam) - ref_lam) / np.array(ref_lam)), owned=owned,
+                       interior=all_int))
     except Exception as exc:  # surface worker failures
         import traceback
 
@@ -101,6 +115,9 @@ def test_distributed_matches_oracle(cname, scale, world, policy):
     assert res["conv"] and abs(res["its"] - res["rits"]) <= 1, res
     assert res["x"] <= 1e-7, res
     assert min(res["owned"][1:]) > 0  # rank 0 owns part of every partitioned level
+    # the overlapped apply (interior cells before the ghost import) ran on the finest level
+    # (tiny cases: a rank whose every cell touches the interface has no interior block)
+    assert any(r[-1] > 0 for r in res["interior"]), res["interior"]
 
 
 def test_partition_morton_and_dof_owner():

@@ -51,6 +51,19 @@ def test_distributed_gpu_backend_world1(cname, scale):
         zd = fine.gather_global(DH.precondition(fine.from_global(b)))
         zh = H.v_cycle(b, executor=False)
         assert np.linalg.norm(zd - zh) <= 1e-10 * np.linalg.norm(zh)
+        # the cycle ran as a replayed CUDA graph with the split apply (interior
+        # blocks on the compute stream, ghost import forked to a side stream)
+        assert DH.use_graph and DH._graph is not None
+        assert fine.layout.n_interior_cells > 0 and fine.overlap
+        # and equals the unsplit distributed cycle run eagerly
+        for lev in DH.levels:
+            lev.overlap = False
+        DH.use_graph, DH._graph = False, None
+        z0 = fine.gather_global(DH.precondition(fine.from_global(b)))
+        assert np.linalg.norm(zd - z0) <= 1e-12 * np.linalg.norm(z0)
+        for lev in DH.levels:
+            lev.overlap = True
+        DH.use_graph = True
         x, its, conv, _ = distributed.dist_cg_solve(fine, fine.from_global(b), DH.precondition, 1e-8)
         from paper_2412_10910_b200.solvers import cg_solve
 

@@ -189,6 +189,26 @@ def test_prolongate_accumulate_and_linearity(pkg):
     assert np.array_equal(T.restrict(np.zeros(sf.n_dofs)), np.zeros(sc.n_dofs))
 
 
+def test_transfer_timing_rows(pkg):
+    # the reference's per-call rows (transfer.py:29, 43, 100-101, 122-123):
+    # "calls" counts prolongations, both time rows grow on every public call,
+    # and the _into calls of the V-cycle leave them alone (no events in a capture)
+    g = golden("tr_3d_q2")
+    sc, sf, T = _transfer_setup(pkg, g)
+    assert T.timings == {"evaluate": 0.0, "gather_scatter": 0.0, "calls": 0}
+    rng = np.random.default_rng(9)
+    T.prolongate(rng.standard_normal(sc.n_dofs))
+    t1 = dict(T.timings)
+    assert t1["calls"] == 1 and t1["evaluate"] > 0.0 and t1["gather_scatter"] > 0.0
+    T.restrict(rng.standard_normal(sf.n_dofs))
+    t2 = dict(T.timings)
+    assert t2["calls"] == 1 and t2["evaluate"] > t1["evaluate"] and t2["gather_scatter"] > t1["gather_scatter"]
+    assert t2["evaluate"] < 1.0 and t2["gather_scatter"] < 1.0  # device seconds of two small kernels
+    x = torch.zeros(sf.n_dofs, dtype=torch.float64, device="cuda")
+    T.prolongate_into(torch.from_numpy(rng.standard_normal(sc.n_dofs)).cuda(), x)
+    assert T.timings == t2
+
+
 # ---------------------------------------------------------------------------
 # smoother, CG, coarse solver, V-cycle, full solve (solvers.py, multigrid.py)
 # ---------------------------------------------------------------------------
