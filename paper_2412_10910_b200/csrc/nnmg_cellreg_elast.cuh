@@ -24,6 +24,14 @@
 
 namespace nnmg {
 
+// block-local node tables (Level::bln_*), see the BLN variant below
+struct BlnTables {
+  const int* node = nullptr;
+  const int* cnt = nullptr;
+  const unsigned* slot = nullptr;  // [blk][(nloc+1)/2][cb]: staging positions of local points 2i (low half), 2i+1 (high)
+  int kp = 0;
+};
+
 template <int P>
 struct CellRegElast {
   static constexpr int DIM = 3;
@@ -34,9 +42,18 @@ struct CellRegElast {
   static constexpr int SLICE = N1 * N1;     // quadrature points per z-slice
   static constexpr int PER = (SLICE + 2) / 3;  // points per thread in phase B
   static constexpr bool kSupported = NLOC <= 27;
-  static constexpr int SMEM_DOUBLES = 2 * SLICE * 9 * CB;
+  // GSM variant (geometry slices staged by TMA): the flux overwrites the
+  // gradients in place, so the second phase buffer holds the current
+  // z-slice of J^-1 / dv instead: [exchange | geometry slice | mbarrier]
+  static constexpr int KS_BLN = NLOC * CB + NLOC * CB / 8 + 1;  // block-local node staging row (see run)
+  __host__ __device__ static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  static constexpr int XB = (cmax(cmax(NLOC * 3 * (CB + 1), SLICE * 9 * CB), 3 * KS_BLN) + 15) / 16 * 16;
+  static constexpr int GEO_DOUBLES = SLICE * NG * CB;
+  static constexpr int SMEM_GSM = XB + GEO_DOUBLES + 2;
+  static constexpr int SMEM_DOUBLES = 2 * SLICE * 9 * CB > SMEM_GSM ? 2 * SLICE * 9 * CB : SMEM_GSM;
 
   __host__ __device__ static constexpr int at(int i0, int i1, int i2) { return i0 + N1 * (i1 + N1 * i2); }
+  __host__ __device__ __forceinline__ static unsigned bln_phys(unsigned k) { return k + (k >> 3); }
 
   template <int K, bool TRANS>
   __device__ __forceinline__ static void sweep_axis(const double (&M)[kMaxN1][kMaxN1], double (&v)[NLOC]) {
@@ -82,13 +99,39 @@ struct CellRegElast {
   // adjacent in the interleaved vector, so a warp instruction touches ~16
   // sectors instead of 32 (the component-per-warp mapping), halving the L1
   // wavefronts of the two scattered phases (ncu r1: L1 80% busy).
-  static constexpr int XS = CB + 1;  // padded row of the exchange buffer [l][comp][XS]
-  static_assert(NLOC * 3 * XS <= SMEM_DOUBLES, "exchange buffer fits the phase buffers");
+  // padded row of the exchange buffer [l][comp][XS].  Node-major thread t
+  // touches row t % 3, column t / 3: with 3 XS = 1 (mod 16) its 8-byte bank is
+  // XS t (mod 16), a bijection over any 16 consecutive threads, so the
+  // node-major side is conflict-free like the lane-contiguous side (XS = 33
+  // measured 3.5k shared wavefronts per CTA against 2.6k of payload).  The
+  // TMA-staged variant keeps 33: its exchange shares the 48 KB with a
+  // geometry slice.
+  template <bool GSM>
+  __host__ __device__ static constexpr int xs() {
+    return GSM ? CB + 1 : CB + 11;
+  }
+  static_assert(NLOC * 3 * (CB + 11) <= SMEM_DOUBLES && NLOC * 3 * (CB + 1) <= XB, "exchange buffer fits");
 
-  template <bool kNeg, int GEO = 0, class TV, class TG, bool XCH = false>
+  // GSM (GEO 0): the block's stored geometry is streamed through shared
+  // memory one z-slice at a time by TMA bulk copies (cp.async.bulk +
+  // mbarrier): slice 0 is in flight during the gather and the interpolation
+  // sweeps, slice qz+1 during phase C of slice qz and phase A of slice qz+1,
+  // so phase B reads J^-1 / dv from shared memory instead of waiting on 30
+  // global loads per thread (ncu r2: long scoreboard 3.6 warps per issue, the
+  // phase-B DFMAs on top of the sampled stalls).
+  // BLN (block-local nodes): the 32 cells of a block share most of their
+  // nodes (585 distinct of 864 slots on a structured Q2 row), and consecutive
+  // list entries are mostly consecutive in memory.  The CTA gathers the
+  // block's distinct node values once into shared memory (thread i -> entry
+  // i / 3, component i % 3: contiguous runs instead of 27 scattered warp
+  // loads per thread), every thread picks its 27 values by list position, and
+  // after the transposed sweeps thread i sums the slots of entry i / 3 in a
+  // fixed order and issues ONE atomic per node component and block.
+  template <bool kNeg, int GEO = 0, class TV, class TG, bool XCH = false, bool GSM = false, bool BLN = false>
   __device__ __forceinline__ static void run(const Tables& tab, const TV* __restrict__ src, TV* __restrict__ dst,
                                              const int* __restrict__ idx, const TG* __restrict__ geo, int64_t blk,
-                                             double lam, double mu, double* sm, double* __restrict__ cellout = nullptr) {
+                                             double lam, double mu, double* sm, double* __restrict__ cellout = nullptr,
+                                             const BlnTables bln = {}) {
     static_assert(GEO == 0 || sizeof(TG) == sizeof(double), "edge recompute reads fp64 edges");
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     static_assert(GEO == 0 || N1 == 3, "edge recompute relies on qx == component in phase B");
@@ -96,18 +139,85 @@ struct CellRegElast {
     if (w == 0 && lane == 0) {
       if constexpr (GEO == 0) {
         constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(TG);
-        prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
+        if constexpr (!GSM) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
       } else {
         prefetch_l2_bulk(geo + blk * (int64_t)NE * CB, unsigned(NE) * CB * sizeof(double));
       }
     }
+    static_assert(!GSM || GEO == 0, "TMA staging streams the stored geometry");
+    constexpr int XS = xs<GSM>();
     double* gbuf = sm;                     // [SLICE][3 comps][3 dirs][CB]
-    double* fbuf = sm + SLICE * 9 * CB;    // same layout, reference flux
+    double* fbuf = GSM ? sm : sm + SLICE * 9 * CB;  // same layout, reference flux (GSM: in place)
+    const TG* gsm = reinterpret_cast<const TG*>(sm + XB);  // GSM: [SLICE][NG][CB] of the current slice
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + XB + GEO_DOUBLES);
+    constexpr unsigned kSliceBytes = unsigned(SLICE) * NG * CB * sizeof(TG);
+    const TG* gblock = geo + blk * (int64_t)NLOC * NG * CB;
+    if constexpr (GSM) {
+      if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_proxy_async();
+        mbar_expect_tx(bar, kSliceBytes);
+        tma_load_1d(sm + XB, gblock, kSliceBytes, bar);
+      }
+    }
     double v[NLOC];
     const int* ib = idx + blk * NLOC * CB + lane;
     // node-major exchange coordinates of this thread: cell xc, component xw
     const int xc = threadIdx.x / 3, xw = threadIdx.x % 3;
-    if constexpr (XCH) {
+    // BLN staging layout: component-major rows of KS doubles, entry k at
+    // k + k / 8.  At one local index the 32 cells of a structured Q2 block sit
+    // 8 list entries apart for the block's own nodes (conflict-free with the
+    // skew), 4 or 2 for nodes of the previous row / layer / edge (2- to 4-way
+    // conflicts remain: ncu 57k extra shared wavefronts per SM).  A plain
+    // [k][comp] layout measured 16-way conflicts; an xor swizzle
+    // k ^ (k >> 4 & 15) removes the conflicts but its per-entry address
+    // arithmetic spills at the 168-register cap (measured 227 vs 208 us).
+    constexpr int KS = KS_BLN;
+    static_assert(!BLN || 3 * KS <= SMEM_DOUBLES, "node staging fits");
+    static_assert(!(BLN && GSM) || 3 * KS <= XB, "node staging fits beside the geometry slice");
+    // entry xc + CB j sits at xc + xc / 8 + (CB + CB / 8) j: one base register, immediate offsets
+    const int xbase = xw * KS + xc + (xc >> 3);
+    const int bK = BLN ? bln.cnt[blk] : 0;
+    const int* bnode = BLN ? bln.node + blk * (int64_t)bln.kp : nullptr;
+    if constexpr (BLN) {
+      static_assert(XCH, "block-local nodes replace the node-major exchange");
+      // the block's distinct node values: thread t loads entries t/3 + 32 j,
+      // component t % 3 (at most NLOC rounds: 3 CB threads, <= NLOC CB
+      // entries); every load of a round set is in flight together
+      const int n3 = bK * 3;
+      // unconditional ordered loads (clamped addresses), so that the rounds
+      // of a batch are in flight together: first the node ids, then the
+      // values; two batches bound the live addresses (one batch spills)
+      constexpr int NB = (NLOC + 1) / 2;
+#pragma unroll
+      for (int j0 = 0; j0 < NLOC; j0 += NB) {
+        int nd[NB];
+        double val[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          nd[j] = j0 + j < NLOC ? ld_nc_ordered(bnode + min(xc + CB * (j0 + j), bln.kp - 1)) : -1;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          nd[j] = j0 + j < NLOC && threadIdx.x + 96 * (j0 + j) < n3 ? nd[j] : -1;
+          if (j0 + j < NLOC) val[j] = double(ld_nc_ordered(src + (int64_t)max(nd[j], 0) * 3 + xw));
+        }
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (j0 + j < NLOC && nd[j] >= 0) sm[xbase + (CB + CB / 8) * (j0 + j)] = val[j];
+      }
+      __syncthreads();
+      constexpr int NP = (NLOC + 1) / 2;
+      const unsigned* bs = bln.slot + blk * (int64_t)(NP * CB) + lane;
+      unsigned kk[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) kk[i] = ld_nc_ordered(bs + i * CB);
+#pragma unroll
+      for (int l = 0; l < NLOC; ++l) {
+        const unsigned k = (l & 1) ? kk[l / 2] >> 16 : kk[l / 2] & 0xFFFFu;
+        v[l] = k != 0xFFFFu ? sm[w * KS + k] : 0.0;
+      }
+      __syncthreads();  // phase A reuses the buffer
+    } else if constexpr (XCH) {
       const int* xb = idx + blk * NLOC * CB + xc;
 #pragma unroll
       for (int l = 0; l < NLOC; ++l) {
@@ -179,6 +289,7 @@ struct CellRegElast {
         o[2 * CB] = gz;
       }
       __syncthreads();
+      if constexpr (GSM) mbar_wait(bar, qz & 1);
       // B: full stress at points s = w + 3k of the slice
 #pragma unroll
       for (int k = 0; k < PER; ++k) {
@@ -217,6 +328,13 @@ struct CellRegElast {
 #pragma unroll
               for (int b = 0; b < 3; ++b) K[a][b] = C[b][a] * rdet;
             dv = det * (tab.w[w] * tab.w[k] * tab.w[qz]);
+          } else if constexpr (GSM) {
+            const TG* G = gsm + s * NG * CB + lane;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) K[a][b] = double(G[(a * 3 + b) * CB]);
+            dv = double(G[9 * CB]);
           } else {
             const TG* G = gb + (qz * SLICE + s) * NG * CB;
 #pragma unroll
@@ -254,6 +372,13 @@ struct CellRegElast {
         }
       }
       __syncthreads();
+      if constexpr (GSM) {
+        // every thread has read this slice's geometry: refill the buffer
+        if (qz + 1 < N1 && threadIdx.x == 0) {
+          mbar_expect_tx(bar, kSliceBytes);
+          tma_load_1d(sm + XB, gblock + (qz + 1) * SLICE * NG * CB, kSliceBytes, bar);
+        }
+      }
       // C: transposed collocation derivatives of this component's flux
 #pragma unroll
       for (int s = 0; s < SLICE; ++s) {
@@ -270,10 +395,53 @@ struct CellRegElast {
       // the next slice's phase A overwrites gbuf only after every thread
       // passed the phase-B barrier above; fbuf is rewritten after the next
       // phase-A barrier, which every phase-C reader has passed
+      // (GSM: the flux lives in gbuf, so phase C must finish first)
+      if constexpr (GSM) {
+        if (qz + 1 < N1) __syncthreads();
+      }
     }
     sweep_axis<2, true>(tab.S, acc);
     sweep_axis<1, true>(tab.S, acc);
     sweep_axis<0, true>(tab.S, acc);
+    if constexpr (BLN) {
+      if (!cellout) {
+        // block-local sums in shared memory without atomics: warp w owns
+        // component w of every list entry, and within one local index l the
+        // 32 cells of a block hold 32 distinct nodes (checked at setup), so
+        // the read-modify-write of pass l is conflict-free; passes are
+        // ordered by __syncwarp.  Then one atomic per node component and block,
+        // entries in list order (contiguous runs).
+        __syncthreads();  // every thread is done with the phase buffers
+        // re-read rather than kept live across the sweeps (the kernel sits at its register cap)
+        const int n3 = ld_nc_ordered(bln.cnt + blk) * 3;
+#pragma unroll
+        for (int j = 0; j < NLOC; ++j)
+          if (threadIdx.x + 96 * j < n3) sm[xbase + (CB + CB / 8) * j] = 0.0;
+        constexpr int NP = (NLOC + 1) / 2;
+        const unsigned* bs = bln.slot + blk * (int64_t)(NP * CB) + lane;
+        unsigned kk[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) kk[i] = ld_nc_ordered(bs + i * CB);
+        __syncthreads();
+#pragma unroll
+        for (int l = 0; l < NLOC; ++l) {
+          const unsigned k = (l & 1) ? kk[l / 2] >> 16 : kk[l / 2] & 0xFFFFu;
+          if (k != 0xFFFFu) sm[w * KS + k] += acc[l];
+          __syncwarp();
+        }
+        int nd[NLOC];
+#pragma unroll
+        for (int j = 0; j < NLOC; ++j) nd[j] = ld_nc_ordered(bnode + min(xc + CB * j, bln.kp - 1));
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < NLOC; ++j)
+          if (threadIdx.x + 96 * j < n3 && nd[j] >= 0) {
+            const double a = sm[xbase + (CB + CB / 8) * j];
+            atomicAdd(dst + (int64_t)nd[j] * 3 + xw, TV(kNeg ? -a : a));
+          }
+        return;
+      }
+    }
     if constexpr (XCH) {
       if (!cellout) {
         __syncthreads();  // every thread is done with the phase buffers

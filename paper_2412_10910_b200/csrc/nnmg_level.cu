@@ -336,6 +336,10 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       const char* ex = getenv("NNMG_ELAST_XCH");
       // measured on B200 (C5 fine apply): 257 -> 222 us
       L->elast_xch = ex ? atoi(ex) != 0 : true;
+      const char* et = getenv("NNMG_ELAST_TMA");
+      L->elast_tma = et ? atoi(et) != 0 : false;
+      const char* eb = getenv("NNMG_ELAST_BLN");
+      L->elast_bln = eb ? atoi(eb) != 0 : false;
 
     }
     // constraints: the kernels support whole-node constraints (every component
@@ -369,6 +373,55 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       }
     }
     L->idx.upload(idx);
+    if (physics == kElasticity && dim == 3 && nloc <= 27 && L->reg_kernel && L->elast_bln) {
+      // block-local node tables of the elasticity register apply
+      const int nslot = nloc * cb;
+      std::vector<std::vector<int>> nodes(L->nblk);
+      int kmax = 0;
+      for (int64_t b = 0; b < L->nblk; ++b) {
+        auto& nd = nodes[b];
+        nd.reserve(nslot);
+        for (int sidx = 0; sidx < nslot; ++sidx) {
+          const int g = idx[b * nslot + sidx];
+          if (g >= 0) nd.push_back(g);
+        }
+        std::sort(nd.begin(), nd.end());
+        nd.erase(std::unique(nd.begin(), nd.end()), nd.end());
+        kmax = std::max<int>(kmax, static_cast<int>(nd.size()));
+      }
+      const int kp = (kmax + 31) / 32 * 32;
+      L->bln_kp = kp;
+      std::vector<int> bnode(size_t(L->nblk) * kp, -1), bcnt(L->nblk, 0);
+      const int np = (nloc + 1) / 2;
+      std::vector<unsigned> bslot(size_t(L->nblk) * np * cb, 0xFFFFFFFFu);
+      bool distinct = true;  // within one local index, the cells of a block hold distinct nodes
+      std::vector<uint8_t> seen;
+      for (int64_t b = 0; b < L->nblk && distinct; ++b) {
+        const auto& nd = nodes[b];
+        bcnt[b] = static_cast<int>(nd.size());
+        std::copy(nd.begin(), nd.end(), bnode.begin() + b * kp);
+        for (int l = 0; l < nloc && distinct; ++l) {
+          seen.assign(nd.size(), 0);
+          for (int c = 0; c < cb; ++c) {
+            const int g = idx[b * nslot + l * cb + c];
+            if (g < 0) continue;
+            const int k = static_cast<int>(std::lower_bound(nd.begin(), nd.end(), g) - nd.begin());
+            unsigned& word = bslot[(b * np + l / 2) * cb + c];
+            const unsigned ph = static_cast<unsigned>(k + (k >> 3));  // staging position (bln_phys)
+            word = (l & 1) ? (word & 0x0000FFFFu) | (ph << 16) : (word & 0xFFFF0000u) | ph;
+            if (seen[k]) distinct = false;
+            seen[k] = 1;
+          }
+        }
+      }
+      if (distinct) {
+        L->bln_node.upload(bnode);
+        L->bln_cnt.upload(bcnt);
+        L->bln_slot.upload(bslot);
+      } else {
+        L->elast_bln = false;  // e.g. rotated cells sharing a node at one local index: node-major exchange
+      }
+    }
     // geometry on the device from vertex coordinates
     NNMG_REQUIRE(n_vertices < (int64_t(1) << 31), kUnsupported, "more than 2^31 vertices");
     L->verts.upload(vertices, size_t(n_vertices) * dim);
@@ -506,17 +559,19 @@ __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const doubl
 }
 
 // 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
-template <int P, bool NEG, int GEO = 0, class TV = double, class TG = double, bool XCH = false>
+template <int P, bool NEG, int GEO = 0, class TV = double, class TG = double, bool XCH = false, bool GSM = false,
+          bool BLN = false>
 __global__ void __launch_bounds__(96, 4) k_apply_reg_elast(Tables tab, const TV* __restrict__ src,
                                                         TV* __restrict__ dst, const int* __restrict__ idx,
                                                         const TG* __restrict__ geo, int64_t b0, int64_t b1,
                                                         double lam, double mu, const int* __restrict__ cd, int64_t ncd,
-                                                        double* __restrict__ cellout = nullptr) {
-  __shared__ double sm[CellRegElast<P>::SMEM_DOUBLES];
+                                                        double* __restrict__ cellout = nullptr, BlnTables bln = {}) {
+  __shared__ __align__(128) double sm[CellRegElast<P>::SMEM_DOUBLES];
   if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x;
   if (blk >= b1) return;
-  CellRegElast<P>::template run<NEG, GEO, TV, TG, XCH>(tab, src, dst, idx, geo, blk, lam, mu, sm, cellout);
+  CellRegElast<P>::template run<NEG, GEO, TV, TG, XCH, GSM, BLN>(tab, src, dst, idx, geo, blk, lam, mu, sm, cellout,
+                                                                 bln);
 }
 
 // per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
@@ -641,7 +696,7 @@ struct ApplyLaunchT {
           if (L.edges.ptr && L.elast_recompute && !cellout) {
             auto kr = neg ? k_apply_reg_elast<P, true, 2> : k_apply_reg_elast<P, false, 2>;
             kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.edges.ptr, b0, b1, L.lam,
-                                                         L.mu, nullptr, 0, nullptr);
+                                                         L.mu, nullptr, 0, nullptr, BlnTables{});
             NNMG_CHECK_LAUNCH();
             count_launch();
             return;
@@ -651,8 +706,19 @@ struct ApplyLaunchT {
                                      : k_apply_reg_elast<P, true>)
                       : (L.elast_xch ? k_apply_reg_elast<P, false, 0, double, double, true>
                                      : k_apply_reg_elast<P, false>);
+        if (L.elast_tma && L.elast_xch)
+          kr = neg ? k_apply_reg_elast<P, true, 0, double, double, true, true>
+                   : k_apply_reg_elast<P, false, 0, double, double, true, true>;
+        BlnTables bln{};
+        if (L.elast_bln && L.bln_node.ptr && !cellout) {
+          bln = BlnTables{L.bln_node.ptr, L.bln_cnt.ptr, L.bln_slot.ptr, L.bln_kp};
+          kr = L.elast_tma ? (neg ? k_apply_reg_elast<P, true, 0, double, double, true, true, true>
+                                  : k_apply_reg_elast<P, false, 0, double, double, true, true, true>)
+                           : (neg ? k_apply_reg_elast<P, true, 0, double, double, true, false, true>
+                                  : k_apply_reg_elast<P, false, 0, double, double, true, false, true>);
+        }
         kr<<<static_cast<unsigned>(nb), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.lam, L.mu, cd,
-                                                     ncd, cellout);
+                                                     ncd, cellout, bln);
         fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();

@@ -28,6 +28,15 @@ struct Level {
   bool apply_recompute = false; // pencil apply: G recomputed from edge vectors (3D Laplace Q3/Q4)
   bool reg_recompute = false;   // register apply: G recomputed from edge vectors (3D Laplace Q1/Q2)
   bool elast_recompute = false; // elasticity register apply (3D Q2): J^-1, |det J| from edge vectors
+  // elasticity register apply, block-local nodes (BLN): per cell block the
+  // sorted distinct free nodes and each slot's position in that list; the
+  // block's node values are gathered once (contiguous runs) and each node
+  // component gets ONE atomic per block
+  bool elast_bln = false;
+  int bln_kp = 0;                 // padded node-list length per block
+  DevBuf<int> bln_node, bln_cnt;  // [nblk][kp] global scalar node (-1 pad), [nblk] count
+  DevBuf<unsigned> bln_slot;      // [nblk][(nloc+1)/2][cb] staging positions (CellRegElast::bln_phys) of two local points per word, 0xFFFF = constrained / padding
+  bool elast_tma = false;       // elasticity register apply: geometry slices staged in shared memory by TMA
   bool elast_xch = true;        // elasticity register apply: node-major gather/scatter via shared memory
   bool reg_tma = false;         // register apply (3D): G streamed through shared memory by TMA bulk copies
   bool fuse_constrained = true;  // register kernels handle the constrained rows in their prologue

@@ -50,6 +50,8 @@ struct TransferDispatchT {
       const int ch = T.chunk;
       const int64_t nwarps = (T.nitems + ch - 1) / ch;
       constexpr int W = StagedRestrict<D, P, NC>::WARPS;
+      // two planes per lane where the 2 x INNER x NC accumulators fit in registers
+      constexpr bool kPl2 = 2 * (ipow(P + 1, D) / (P + 1)) * NC <= 60 && P >= 1;
       if constexpr (ipow(P + 1, D) * NC <= 32) {
         // default: 3 points per lane and round in 3D (C3 0.176 -> 0.173 ms), 2 in 2D
         // (C2 0.022 vs 0.025 ms with 3); 4 points measured slower in both
@@ -72,8 +74,20 @@ struct TransferDispatchT {
         if (T.restrict_wide) {
           k_restrict_lane<D, P, NC, 1><<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(
               C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
+        } else if (T.restrict_pl == 2 && kPl2) {
+          if constexpr (kPl2) {
+            constexpr int W2 = StagedRestrict<D, P, NC, 2>::WARPS;
+            k_restrict_staged<D, P, NC, TV, TV, 2><<<grid_for(nwarps, W2), W2 * 32, 0, s>>>(
+                C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
+          }
         } else {
           k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
+        }
+      } else if (T.restrict_pl == 2 && kPl2) {
+        if constexpr (kPl2) {
+          constexpr int W2 = StagedRestrict<D, P, NC, 2>::WARPS;
+          k_restrict_staged<D, P, NC, TV, TV, 2><<<grid_for(nwarps, W2), W2 * 32, 0, s>>>(
               C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         }
       } else {
@@ -199,6 +213,9 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
       // 32 < NLOC*NCOMP <= 81: 1 = lane-owned local vector, 0 = staged groups
       const char* w = getenv("NNMG_RESTRICT_WIDE");
       T->restrict_wide = w ? atoi(w) : 0;
+      // staged groups: planes of the outermost axis per lane (1 or 2)
+      const char* pl = getenv("NNMG_RESTRICT_PL");
+      T->restrict_pl = pl ? atoi(pl) : 1;
     }
     // fine scalar DoFs without a transfer point: zeroed by the plain prolongation
     std::vector<uint8_t> has(fine->n_scalar, 0);

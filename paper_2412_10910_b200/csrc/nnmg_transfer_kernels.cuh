@@ -389,12 +389,19 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
 // and lane g accumulates the outermost-axis plane l_last = g of the local
 // vector (all components) in registers.  Slots are combined in shared memory
 // in a fixed order at each cell end.
-template <int DIM, int PC, int NCOMP>
+// PL = planes of the outermost axis per lane: a slot of G = ceil(N1 / PL) lanes
+// shares a staged point, and each 16-byte table read then feeds PL x INNER
+// FMAs per component.  ncu (r2, C4, PL = 1): 6.2 shared-memory wavefronts per
+// point, the L1 data pipe 87% busy and the FP64 pipe 47%: the restriction is
+// bound by its table reads, so PL = 2 (10 points instead of 6 per sub-round
+// for Q4, the same reads) trades idle lanes of the last slot lane for
+// 40% fewer reads per point.
+template <int DIM, int PC, int NCOMP, int PL = 1>
 struct StagedRestrict {
   static constexpr int N1 = PC + 1;
   static constexpr int NLOC = ipow(N1, DIM);
   static constexpr int NOUT = NLOC * NCOMP;
-  static constexpr int G = N1;
+  static constexpr int G = (N1 + PL - 1) / PL;
   static constexpr int SLOTS = 32 / G;
   static constexpr int SUB = 32 / SLOTS;
   static constexpr int P = SLOTS * SUB;  // points per round
@@ -408,18 +415,18 @@ struct StagedRestrict {
   static constexpr int OV = OZ + N1;
   static constexpr int REC0 = OV + NCOMP;
   static constexpr int REC = ((REC0 - 2 + 15) / 16) * 16 + 2;
-  static constexpr int WARP_DOUBLES = (2 * P * REC + SLOTS * G * PLANE + 1) & ~1;  // keeps 16-byte alignment
+  static constexpr int WARP_DOUBLES = (2 * P * REC + SLOTS * N1 * PLANE + 1) & ~1;  // keeps 16-byte alignment
   static constexpr int WARPS = (48 * 1024) / (WARP_DOUBLES * 8) >= kTransferWarps
                                    ? kTransferWarps
                                    : ((48 * 1024) / (WARP_DOUBLES * 8) >= 1 ? (48 * 1024) / (WARP_DOUBLES * 8) : 1);
 };
 
-template <int DIM, int PC, int NCOMP, class TV = double, class TX = double>
-__global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
+template <int DIM, int PC, int NCOMP, class TV = double, class TX = double, int PL = 1>
+__global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL>::WARPS * 32)
     k_restrict_staged(Tables tab, const TV* __restrict__ rf, const int* __restrict__ cell_start,
                       const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t ncc, int chunk,
                       double* __restrict__ cellbuf) {
-  using K = StagedRestrict<DIM, PC, NCOMP>;
+  using K = StagedRestrict<DIM, PC, NCOMP, PL>;
   constexpr int N1 = K::N1, G = K::G, SLOTS = K::SLOTS, SUB = K::SUB, P = K::P, INNER = K::INNER,
                 PLANE = K::PLANE, REC = K::REC, NOUT = K::NOUT;
   __shared__ __align__(16) double smem[K::WARPS][K::WARP_DOUBLES];
@@ -428,16 +435,18 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
   if (c0 >= ncc) return;
   const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
   double* stage = smem[warp];                // [2][P][REC]
-  double* red = smem[warp] + 2 * P * REC;    // [SLOTS*G][PLANE]
+  double* red = smem[warp] + 2 * P * REC;    // [SLOTS][N1][PLANE]
   const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
   zero_empty_cells(R, c0, NOUT, lane, cellbuf);
   const int slot = lane / G, g = lane % G;
   const bool grp = slot < SLOTS;
-  double acc[INNER][NCOMP];
+  double acc[PL][INNER][NCOMP];
 #pragma unroll
-  for (int i = 0; i < INNER; ++i)
+  for (int p = 0; p < PL; ++p)
 #pragma unroll
-    for (int c = 0; c < NCOMP; ++c) acc[i][c] = 0.0;
+    for (int i = 0; i < INNER; ++i)
+#pragma unroll
+      for (int c = 0; c < NCOMP; ++c) acc[p][i][c] = 0.0;
   int buf = 0;
   stream_rounds<DIM, NCOMP, 1>(
       R, pt_dof, xhat, rf, P, lane, lane < P,
@@ -475,20 +484,28 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
                 X1[i + 1] = t.y;
               }
             }
-            const double z = q[K::OZ + g];
+            // this lane's planes g PL .. g PL + PL - 1 (a plane past N1 - 1 adds zeros)
+            double z[PL];
+#pragma unroll
+            for (int p = 0; p < PL; ++p) z[p] = g * PL + p < N1 ? q[K::OZ + g * PL + p] : 0.0;
 #pragma unroll
             for (int c = 0; c < NCOMP; ++c) {
-              const double a = q[K::OV + c] * z;
-              if constexpr (DIM == 3) {
+              const double v = q[K::OV + c];
 #pragma unroll
-                for (int i1 = 0; i1 < N1; ++i1) {
-                  const double b = a * X1[i1];
+              for (int p = 0; p < PL; ++p) {
+                const double a = v * z[p];
+                if constexpr (DIM == 3) {
 #pragma unroll
-                  for (int i0 = 0; i0 < N1; ++i0) acc[i0 + N1 * i1][c] = fma(b, X0[i0], acc[i0 + N1 * i1][c]);
+                  for (int i1 = 0; i1 < N1; ++i1) {
+                    const double b = a * X1[i1];
+#pragma unroll
+                    for (int i0 = 0; i0 < N1; ++i0)
+                      acc[p][i0 + N1 * i1][c] = fma(b, X0[i0], acc[p][i0 + N1 * i1][c]);
+                  }
+                } else {
+#pragma unroll
+                  for (int i0 = 0; i0 < N1; ++i0) acc[p][i0][c] = fma(a, X0[i0], acc[p][i0][c]);
                 }
-              } else {
-#pragma unroll
-                for (int i0 = 0; i0 < N1; ++i0) acc[i0][c] = fma(a, X0[i0], acc[i0][c]);
               }
             }
           }
@@ -498,12 +515,19 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
       [&](int ci) {
         if (grp) {
 #pragma unroll
-          for (int i = 0; i < INNER; ++i)
+          for (int p = 0; p < PL; ++p)
+            if (g * PL + p < N1) {
 #pragma unroll
-            for (int c = 0; c < NCOMP; ++c) {
-              red[lane * PLANE + i * NCOMP + c] = acc[i][c];
-              acc[i][c] = 0.0;
+              for (int i = 0; i < INNER; ++i)
+#pragma unroll
+                for (int c = 0; c < NCOMP; ++c) red[((slot * N1 + g * PL + p) * INNER + i) * NCOMP + c] = acc[p][i][c];
             }
+#pragma unroll
+          for (int p = 0; p < PL; ++p)
+#pragma unroll
+            for (int i = 0; i < INNER; ++i)
+#pragma unroll
+              for (int c = 0; c < NCOMP; ++c) acc[p][i][c] = 0.0;
         }
         __syncwarp();
         // output o = l * NCOMP + c with l = plane * INNER + i: slot sum in fixed order
@@ -511,7 +535,7 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP>::WARPS * 32)
           const int plane = o / PLANE, k = o % PLANE;
           double sum = 0.0;
 #pragma unroll
-          for (int sl = 0; sl < SLOTS; ++sl) sum += red[(sl * G + plane) * PLANE + k];
+          for (int sl = 0; sl < SLOTS; ++sl) sum += red[(sl * N1 + plane) * PLANE + k];
           cellbuf[(c0 + ci) * NOUT + o] = sum * lagrange_norm<DIM, N1>(tab, o / NCOMP);
         }
         __syncwarp();

@@ -49,6 +49,14 @@ APPLY_VARIANTS = [
     ("op_3d_el_q1", {"NNMG_APPLY_KERNEL": "pencil"}),
     ("op_3d_el_q2", {"NNMG_ELAST_RECOMPUTE": "1"}),
     ("op_3d_el_q2", {"NNMG_ELAST_RECOMPUTE": "0"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_TMA": "1"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_TMA": "0"}),
+    ("op_ref_cube3d_el", {"NNMG_ELAST_TMA": "1"}),
+    ("op_3d_el_q1", {"NNMG_ELAST_TMA": "1"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_BLN": "1"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_BLN": "1", "NNMG_ELAST_TMA": "1"}),
+    ("op_3d_el_q1", {"NNMG_ELAST_BLN": "1"}),
+    ("op_ref_cube3d_el", {"NNMG_ELAST_BLN": "1"}),
     ("op_ref_cube3d_el", {"NNMG_ELAST_RECOMPUTE": "1"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_SPLIT": "1"}),
@@ -134,6 +142,27 @@ def test_restriction_wide_lane_matches_reference(pkg, monkeypatch, name, chunk, 
     (NNMG_RESTRICT_WIDE=1) against the staged groups, both against the reference."""
     monkeypatch.setenv("NNMG_RESTRICT_WIDE", wide)
     monkeypatch.setenv("NNMG_RESTRICT_CHUNK", chunk)
+    g = golden(name)
+    sc, sf, T = _transfer(pkg, g)
+    rng = np.random.default_rng(1)
+    rng.standard_normal((3, sc.n_dofs))  # the golden draws the coarse inputs first
+    rf = rng.standard_normal((3, sf.n_dofs))
+    for r, want in zip(rf, g["restrict"]):
+        got = T.restrict(r)
+        assert rel(got, want) <= TOL
+        assert np.array_equal(got, T.restrict(r))
+
+
+@pytest.mark.parametrize("pl", ["1", "2"])
+@pytest.mark.parametrize("name,chunk,maxp", [("tr_3d_el_q2", "1", None), ("tr_3d_el_q2", "4", "64"),
+                                             ("tr_3d_q4_warp", "1", None), ("tr_3d_q4_warp", "3", "64")])
+def test_restriction_planes_per_lane_matches_reference(pkg, monkeypatch, name, chunk, maxp, pl):
+    """Staged restriction with one or two planes of the outermost axis per
+    lane (NNMG_RESTRICT_PL): slots of ceil(N1 / PL) lanes share a staged point."""
+    monkeypatch.setenv("NNMG_RESTRICT_PL", pl)
+    monkeypatch.setenv("NNMG_RESTRICT_CHUNK", chunk)
+    if maxp:
+        monkeypatch.setenv("NNMG_TRANSFER_MAXP", maxp)
     g = golden(name)
     sc, sf, T = _transfer(pkg, g)
     rng = np.random.default_rng(1)

@@ -1,4 +1,5 @@
-"""C5 fine elasticity apply: component-per-warp scatter vs node-major exchange."""
+"""C5 fine elasticity apply variants (env switches read at level creation):
+   python tools/gpu/elast_variants.py NNMG_ELAST_XCH=0 NNMG_ELAST_XCH=1 NNMG_ELAST_XCH=1,NNMG_ELAST_TMA=1"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
@@ -12,8 +13,13 @@ sp.constraints = fespace.dirichlet_constraints(sp, cfg.dirichlet_ids)
 u = torch.from_numpy(np.random.default_rng(0).standard_normal(sp.n_dofs)).cuda()
 s = torch.cuda.Stream()
 ref = None
-for xch in ("0", "1"):
-    os.environ["NNMG_ELAST_XCH"] = xch
+combos = sys.argv[1:] or ["NNMG_ELAST_XCH=0", "NNMG_ELAST_XCH=1", "NNMG_ELAST_XCH=1,NNMG_ELAST_TMA=1"]
+for xch in combos:
+    for k in [k for k in os.environ if k.startswith("NNMG_ELAST")]:
+        del os.environ[k]
+    for kv in xch.split(","):
+        k, v = kv.split("=")
+        os.environ[k] = v
     op = mfoperator.ElasticityOperator(sp, 1.0, 1.0)
     v = torch.empty_like(u)
     with torch.cuda.stream(s):
@@ -27,6 +33,6 @@ for xch in ("0", "1"):
     s.synchronize()
     vv = v.cpu().numpy()
     ref = vv if ref is None else ref
-    print(f"XCH={xch}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us  rel diff {np.linalg.norm(vv - ref) / np.linalg.norm(ref):.1e}",
+    print(f"{xch}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us  rel diff {np.linalg.norm(vv - ref) / np.linalg.norm(ref):.1e}",
           flush=True)
     del op
