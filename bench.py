@@ -8,11 +8,13 @@ smoothing, residual, non-nested restriction/prolongation, device-resident
 coarse CG) on the finest level of the configuration.  ``value`` = fine DoFs x
 steps / device time with the input resident in HBM (replayed CUDA graph);
 ``e2e`` = the same through the public call with pinned-host input, H2D + cycle
-+ D2H of every step inside the timed region (the copies of neighbouring steps
-overlap the current cycle on separate streams).  The roofline object describes the dominant
-kernel (the fine-level matrix-free apply) measured live with CUDA events on
-its stream.  ``--impl reference`` times the CPU port of the reference's path
-(oracle/, NumPy) on a bounded sample of the same configuration.
++ D2H of every step inside the timed region, serialised as a PCG caller's
+dependent chain (the pipelined rate with independent inputs is reported beside
+it as an upper bound).  The roofline object describes the dominant kernel (the
+fine-level matrix-free apply) measured live with CUDA events on its stream.
+``--impl reference`` times the reference's own hierarchy (oracle/_ref, the
+unmodified NumPy package; the oracle port where that is absent) on a bounded
+sample of the same configuration.
 
 Multi-GPU (torchrun): the cell-partitioned hierarchy (strong scaling, same
 global problem as N=1), halo exchange and dots over NCCL; timing is the max
