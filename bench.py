@@ -776,6 +776,21 @@ def run_distributed(args, cfg):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     value = n_global * args.steps / t_max / 1e9
+    # per-GPU roofline of the dominant kernel: this rank's local fine apply (no halo), events on its stream
+    info = fine.op.info()
+    B_local = vmult_bytes(cfg.dim, cfg.degree, ncomp, fine.n, info["n_cells"], cfg.problem)
+    xa, ya = b.clone(), torch.empty_like(b)
+    for _ in range(3):
+        fine.op.apply_into(xa, ya)
+    e0.record()
+    for _ in range(10):
+        fine.op.apply_into(xa, ya)
+    e1.record()
+    torch.cuda.synchronize()
+    t_apply = torch.tensor([e0.elapsed_time(e1) * 1e-3 / 10], device=dev)
+    dist.all_reduce(t_apply, op=dist.ReduceOp.MAX)
+    t_apply = float(t_apply.item())
+    hbm, hbm_kind = measured_peaks()
     # e2e: each rank's owned share from pinned host memory
     hb = b.cpu().pin_memory()
     hz = torch.empty_like(hb).pin_memory()
@@ -801,7 +816,12 @@ def run_distributed(args, cfg):
                        "parallelism": f"cell-partitioned x{world} (Morton), replicated coarse level",
                        "l2": "inputs larger than L2", "setup_s": round(setup_s, 2),
                        "owned_fine_dofs_rank0": fine.n_owned},
-            "roofline": None, "cpu_baseline": None,
+            "roofline": {"bound": "hbm", "achieved": B_local / t_apply / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": B_local / t_apply / 1e9 / hbm, "traffic": None,
+                         "kernel": "k_apply (this rank's fine-level cells, max over ranks)",
+                         "bytes_per_launch": B_local, "avg_launch_ms": t_apply * 1e3,
+                         "peak_kind": hbm_kind},
+            "cpu_baseline": None,
             "e2e": {"value": e2e, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * fine.n,
                     "d2h_bytes_per_step": 8 * fine.n},
             "gpu_launches": launches, "clocks": clk.summary(),

@@ -34,6 +34,8 @@ an oracle backend to check this host logic on CPU with gloo.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import scipy.linalg
 import torch
@@ -560,7 +562,7 @@ def dist_cg_solve(level, b, precond=None, target_reduction=1e-4, max_iter=1000):
 
 
 def build_distributed_hierarchy(spaces, backend, problem="poisson", lame=None, cheb_degree=4, window=10.0,
-                                search=None, m1=1, m2=1, partition=None, policy="matching", graph=True):
+                                search=None, m1=1, m2=1, partition=None, policy="matching", graph=None):
     """spaces: global FESpaces coarsest first (replicated host data on every
     rank).  Returns a DistHierarchy for this rank.  policy: "matching" (the
     finest level Morton-split, each coarser partitioned level takes the owner
@@ -569,6 +571,12 @@ def build_distributed_hierarchy(spaces, backend, problem="poisson", lame=None, c
     if policy not in ("matching", "default"):
         raise ValueError("policy must be 'matching' or 'default'")
     rank, world = dist.get_rank(), dist.get_world_size()
+    if graph is None:
+        # graph=None: replay the cycle as a CUDA graph on one rank (measured);
+        # with peers the captured NCCL point-to-point calls have never run on
+        # hardware here (one GPU per run), so the eager cycle is the default
+        # and NNMG_DIST_GRAPH=1 opts in
+        graph = world == 1 or os.environ.get("NNMG_DIST_GRAPH", "0") == "1"
     nlev = len(spaces)
     owners = [None] * nlev
     dofown = [None] * nlev
