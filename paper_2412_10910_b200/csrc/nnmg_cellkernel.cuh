@@ -423,7 +423,7 @@ struct CellKernel {
 template <class T>
 struct PlainSrcT {
   const T* __restrict__ s;
-  __device__ __forceinline__ double operator()(int64_t i) const { return double(__ldg(s + i)); }
+  __device__ __forceinline__ T operator()(int64_t i) const { return __ldg(s + i); }
 };
 using PlainSrc = PlainSrcT<double>;
 

@@ -22,12 +22,15 @@ struct CellReg {
   static constexpr int CB = 32;
   static constexpr int NG = DIM * (DIM + 1) / 2;
   static constexpr bool kSupported = NLOC <= 27;
+  // fp32 stored geometry in (k, k+1) pairs (level_enable_f32): even NG only (3D)
+  template <class TG>
+  static constexpr bool kPairedGeo = sizeof(TG) == sizeof(float) && NG % 2 == 0;
 
   __host__ __device__ static constexpr int at(int i0, int i1, int i2) { return i0 + N1 * (i1 + N1 * i2); }
 
   // in-register sweep along axis K with matrix M (trans: M^T)
-  template <int K, bool TRANS>
-  __device__ __forceinline__ static void sweep_axis(const double (&M)[kMaxN1][kMaxN1], double (&v)[NLOC]) {
+  template <int K, bool TRANS, class TA = double>
+  __device__ __forceinline__ static void sweep_axis(const TA (&M)[kMaxN1][kMaxN1], TA (&v)[NLOC]) {
     constexpr int S0 = K == 0 ? 1 : (K == 1 ? N1 : N1 * N1);
     constexpr int NL = NLOC / N1;  // lines along axis K
 #pragma unroll
@@ -40,12 +43,12 @@ struct CellReg {
         base = (line % N1) + (line / N1) * N1 * N1;
       else
         base = line;
-      double in[N1], out[N1];
+      TA in[N1], out[N1];
 #pragma unroll
       for (int i = 0; i < N1; ++i) in[i] = v[base + i * S0];
 #pragma unroll
       for (int q = 0; q < N1; ++q) {
-        double s = 0.0;
+        TA s = 0;
 #pragma unroll
         for (int i = 0; i < N1; ++i) s = fma(TRANS ? M[i][q] : M[q][i], in[i], s);
         out[q] = s;
@@ -125,13 +128,19 @@ struct CellReg {
   static constexpr size_t WARP_SMEM = 2 * size_t(SLICE_BYTES) + 16;
 
   // TD / TG: storage types of dst and of the stored geometry (double, or
-  // float in the mixed-precision V-cycle); the arithmetic is fp64 either way
-  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class Src, class TD, class TG>
+  // float in the mixed-precision V-cycle); TA: the arithmetic type (double;
+  // float = the paper's single-precision V-cycle: with fp64
+  // arithmetic on fp32 storage the kernel is bound by its DFMAs and its
+  // 248 registers, 543 us against 597 us for fp64 storage on C3)
+  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class TA = double, class Src, class TD,
+            class TG>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, TD* __restrict__ dst,
                                                const int* __restrict__ idx, const TG* __restrict__ geo,
                                                int64_t blk, int lane, const double* __restrict__ edges = nullptr,
                                                double* wsm = nullptr, double* __restrict__ cellout = nullptr) {
     static_assert(GEO != 3 || sizeof(TG) == sizeof(double), "TMA slice staging is fp64");
+    static_assert(GEO == 0 || sizeof(TA) == sizeof(double), "recomputed / staged geometry is fp64 arithmetic");
+    static_assert(!kEnergy || sizeof(TA) == sizeof(double), "cell energies are fp64");
     double* gbuf = wsm;
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wsm + 2 * SLICE_Q * NG * CB);
     const TG* gchunk = geo + blk * (int64_t)NLOC * NG * CB;
@@ -160,42 +169,44 @@ struct CellReg {
       constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(TG);
       if (lane == 0) prefetch_l2_bulk(geo + blk * (int64_t)NLOC * NG * CB, kGeoBytes);
     }
-    double v[NLOC];
+    TA v[NLOC];
     const int* ib = idx + blk * NLOC * CB + lane;
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) {
       const int g = ld_geo<kStream>(ib + l * CB);
-      v[l] = g >= 0 ? src((int64_t)g) : 0.0;
+      v[l] = g >= 0 ? TA(src((int64_t)g)) : TA(0);
     }
-    double u0[kEnergy ? NLOC : 1];
+    TA u0[kEnergy ? NLOC : 1];
     if constexpr (kEnergy) {
 #pragma unroll
       for (int l = 0; l < NLOC; ++l) u0[l] = v[l];
     }
     // values at the Gauss points
-    sweep_axis<0, false>(tab.S, v);
-    sweep_axis<1, false>(tab.S, v);
-    if constexpr (DIM == 3) sweep_axis<2, false>(tab.S, v);
-    double w[NLOC];
+    const auto& tS = TabSel<TA>::S(tab);
+    const auto& tDc = TabSel<TA>::Dc(tab);
+    sweep_axis<0, false, TA>(tS, v);
+    sweep_axis<1, false, TA>(tS, v);
+    if constexpr (DIM == 3) sweep_axis<2, false, TA>(tS, v);
+    TA w[NLOC];
 #pragma unroll
-    for (int l = 0; l < NLOC; ++l) w[l] = 0.0;
+    for (int l = 0; l < NLOC; ++l) w[l] = 0;
     // one quadrature point: collocation gradient, flux (G g), transposed
     // collocation derivatives accumulated at once
     auto point = [&](int qx, int qy, int qz, auto&& flux) {
-      double gx = 0.0, gy = 0.0, gz = 0.0;
+      TA gx = 0, gy = 0, gz = 0;
 #pragma unroll
       for (int r = 0; r < N1; ++r) {
-        gx = fma(tab.Dc[qx][r], v[at(r, qy, qz)], gx);
-        gy = fma(tab.Dc[qy][r], v[at(qx, r, qz)], gy);
-        if constexpr (DIM == 3) gz = fma(tab.Dc[qz][r], v[at(qx, qy, r)], gz);
+        gx = fma(tDc[qx][r], v[at(r, qy, qz)], gx);
+        gy = fma(tDc[qy][r], v[at(qx, r, qz)], gy);
+        if constexpr (DIM == 3) gz = fma(tDc[qz][r], v[at(qx, qy, r)], gz);
       }
-      double fx, fy, fz = 0.0;
+      TA fx, fy, fz = 0;
       flux(gx, gy, gz, fx, fy, fz);
 #pragma unroll
       for (int r = 0; r < N1; ++r) {
-        w[at(r, qy, qz)] = fma(tab.Dc[qx][r], fx, w[at(r, qy, qz)]);
-        w[at(qx, r, qz)] = fma(tab.Dc[qy][r], fy, w[at(qx, r, qz)]);
-        if constexpr (DIM == 3) w[at(qx, qy, r)] = fma(tab.Dc[qz][r], fz, w[at(qx, qy, r)]);
+        w[at(r, qy, qz)] = fma(tDc[qx][r], fx, w[at(r, qy, qz)]);
+        w[at(qx, r, qz)] = fma(tDc[qy][r], fy, w[at(qx, r, qz)]);
+        if constexpr (DIM == 3) w[at(qx, qy, r)] = fma(tDc[qz][r], fz, w[at(qx, qy, r)]);
       }
     };
     if constexpr (GEO == 2) {
@@ -270,18 +281,29 @@ struct CellReg {
             mbar_wait(&mbar[qz & 1], (qz >> 1) & 1);
           }
         }
-        point(qx, qy, qz, [&](double gx, double gy, double gz, double& fx, double& fy, double& fz) {
-          double gg[NG];
+        point(qx, qy, qz, [&](TA gx, TA gy, TA gz, TA& fx, TA& fy, TA& fz) {
+          TA gg[NG];
           if constexpr (GEO == 1) {
             recompute_g(tab, E, qx, qy, qz, gg);
           } else if constexpr (GEO == 3) {
             const double* G = gbuf + ((qz & 1) * SLICE_Q + q % SLICE_Q) * NG * CB + lane;
 #pragma unroll
             for (int k = 0; k < NG; ++k) gg[k] = G[k * CB];
+          } else if constexpr (kPairedGeo<TG>) {
+            // fp32 geometry of the 3D levels is stored in pairs [q][k/2][CB][2]:
+            // 8-byte loads, 256 bytes per warp instruction like the fp64 stream
+            const float2* G2 = reinterpret_cast<const float2*>(geo) + blk * (int64_t)NLOC * (NG / 2) * CB + lane +
+                               q * (NG / 2) * CB;
+#pragma unroll
+            for (int k = 0; k < NG / 2; ++k) {
+              const float2 t = ld_geo<kStream>(G2 + k * CB);
+              gg[2 * k] = TA(t.x);
+              gg[2 * k + 1] = TA(t.y);
+            }
           } else {
             const TG* G = g0 + q * NG * CB;
 #pragma unroll
-            for (int k = 0; k < NG; ++k) gg[k] = double(ld_geo<kStream>(G + k * CB));
+            for (int k = 0; k < NG; ++k) gg[k] = TA(ld_geo<kStream>(G + k * CB));
           }
           if constexpr (DIM == 3) {
             fx = gg[0] * gx + gg[1] * gy + gg[2] * gz;
@@ -307,9 +329,9 @@ struct CellReg {
       }
     }
     // back to the nodal basis: S^T sweeps
-    if constexpr (DIM == 3) sweep_axis<2, true>(tab.S, w);
-    sweep_axis<1, true>(tab.S, w);
-    sweep_axis<0, true>(tab.S, w);
+    if constexpr (DIM == 3) sweep_axis<2, true, TA>(tS, w);
+    sweep_axis<1, true, TA>(tS, w);
+    sweep_axis<0, true, TA>(tS, w);
     double energy = 0.0;
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) {
@@ -322,7 +344,7 @@ struct CellReg {
           cellout[(blk * NLOC + l) * CB + lane] = w[l];
         else
           atomicAdd(dst + g, TD(kNeg ? -w[l] : w[l]));
-        if constexpr (kEnergy) energy = fma(u0[l], w[l], energy);
+        if constexpr (kEnergy) energy = fma(double(u0[l]), double(w[l]), energy);
       }
     }
     return energy;

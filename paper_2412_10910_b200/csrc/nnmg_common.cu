@@ -137,6 +137,11 @@ Tables make_tables(int degree) {
       t.Dc[a][i] = static_cast<double>(gd / gden);
     }
   }
+  for (int a = 0; a < kMaxN1; ++a)
+    for (int i = 0; i < kMaxN1; ++i) {
+      t.S32[a][i] = static_cast<float>(t.S[a][i]);
+      t.Dc32[a][i] = static_cast<float>(t.Dc[a][i]);
+    }
   return t;
 }
 

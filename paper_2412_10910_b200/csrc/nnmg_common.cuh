@@ -118,6 +118,23 @@ struct Tables {
   double nodes[kMaxN1];       // Lobatto nodes on [0,1]
   double denom[kMaxN1];       // prod_{j!=i} (node_i - node_j)
   double rdenom[kMaxN1];      // 1 / denom (multiplications instead of fp64 divisions)
+  // fp32 copies for the single-precision arithmetic of the mixed-precision V-cycle
+  float S32[kMaxN1][kMaxN1];
+  float Dc32[kMaxN1][kMaxN1];
+};
+
+// sweep matrices in the arithmetic type TA
+template <class TA>
+struct TabSel;
+template <>
+struct TabSel<double> {
+  __host__ __device__ static const double (&S(const Tables& t))[kMaxN1][kMaxN1] { return t.S; }
+  __host__ __device__ static const double (&Dc(const Tables& t))[kMaxN1][kMaxN1] { return t.Dc; }
+};
+template <>
+struct TabSel<float> {
+  __host__ __device__ static const float (&S(const Tables& t))[kMaxN1][kMaxN1] { return t.S32; }
+  __host__ __device__ static const float (&Dc(const Tables& t))[kMaxN1][kMaxN1] { return t.Dc32; }
 };
 
 Tables make_tables(int degree);

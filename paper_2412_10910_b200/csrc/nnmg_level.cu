@@ -336,6 +336,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       const char* ex = getenv("NNMG_ELAST_XCH");
       // measured on B200 (C5 fine apply): 257 -> 222 us
       L->elast_xch = ex ? atoi(ex) != 0 : true;
+      const char* ma = getenv("NNMG_MIXED_ARITH");
+      L->mixed_arith32 = ma ? atoi(ma) != 64 : true;
       const char* et = getenv("NNMG_ELAST_TMA");
       L->elast_tma = et ? atoi(et) != 0 : false;
       const char* eb = getenv("NNMG_ELAST_BLN");
@@ -507,7 +509,7 @@ __device__ __forceinline__ void constrained_rows(const int* __restrict__ cd, int
 // hybrids 0.67-0.74 ms (1/4 .. 3/4 of the blocks recomputing).  Blocks with
 // blk % rmod < rnum take the recompute path.  HYB is an opt-in instantiation
 // (NNMG_RECOMPUTE_MOD / NNMG_RECOMPUTE_NUM) so the default kernel stays lean.
-template <int D, int P, int MINB, bool NEG, bool HYB, class TV = double, class TG = double>
+template <int D, int P, int MINB, bool NEG, bool HYB, class TV = double, class TG = double, class TA = double>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* __restrict__ src, TV* __restrict__ dst,
                                                    const int* __restrict__ idx, const TG* __restrict__ geo,
                                                    int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod,
@@ -527,8 +529,8 @@ __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* _
         continue;
       }
     }
-    CellReg<D, P>::template run<true, false, NEG, 0>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk, threadIdx.x & 31,
-                                                     nullptr, nullptr, cellout);
+    CellReg<D, P>::template run<true, false, NEG, 0, TA>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk,
+                                                         threadIdx.x & 31, nullptr, nullptr, cellout);
   }
 }
 
@@ -619,8 +621,11 @@ struct ApplyLaunchT {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
-        k_apply_reg<D, P, 1, true, false, float, float><<<g, 32 * kWarpsPerCta, 0, s>>>(
-            L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, nullptr, 0, 1, cd, ncd);
+        // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
+        auto kr = L.mixed_arith32 ? (L.reg_minb == 4 ? k_apply_reg<D, P, 4, true, false, float, float, float> : (L.reg_minb == 2 ? k_apply_reg<D, P, 2, true, false, float, float, float> : k_apply_reg<D, P, 3, true, false, float, float, float>))
+                                  : k_apply_reg<D, P, 1, true, false, float, float, double>;
+        kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, nullptr, 0, 1, cd, ncd,
+                                            nullptr);
         fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();
@@ -864,12 +869,28 @@ __global__ void k_to_f32(const double* __restrict__ a, float* __restrict__ b, in
   if (i < n) b[i] = float(a[i]);
 }
 
+// [.. q][k][cb] doubles -> [.. q][k/2][cb][2] floats (ng even)
+__global__ void k_to_f32_paired(const double* __restrict__ a, float* __restrict__ b, int64_t n, int ng, int cb) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t lane = i % cb, k = (i / cb) % ng, row = i / (int64_t(cb) * ng);  // row = blk * nq + q
+  b[((row * (ng / 2) + k / 2) * cb + lane) * 2 + (k & 1)] = float(a[i]);
+}
+
 void level_enable_f32(Level& L, cudaStream_t s) {
   if (L.f32_ready) return;
   NNMG_REQUIRE(L.diag_ready, kInvalidArgument, "level diagonal not computed");
   L.geo32.alloc(L.geo.n);
   L.inv_diag32.alloc(L.inv_diag.n);
-  if (L.geo.n) k_to_f32<<<grid_for(int64_t(L.geo.n), 256), 256, 0, s>>>(L.geo.ptr, L.geo32.ptr, int64_t(L.geo.n));
+  // the register Laplace apply reads 3D fp32 geometry as float2 pairs (CellReg::kPairedGeo)
+  const bool paired = L.physics == kLaplace && L.dim == 3 && L.reg_kernel && L.nloc <= 27 && L.ng % 2 == 0;
+  if (L.geo.n) {
+    if (paired)
+      k_to_f32_paired<<<grid_for(int64_t(L.geo.n), 256), 256, 0, s>>>(L.geo.ptr, L.geo32.ptr, int64_t(L.geo.n), L.ng,
+                                                                      L.cb);
+    else
+      k_to_f32<<<grid_for(int64_t(L.geo.n), 256), 256, 0, s>>>(L.geo.ptr, L.geo32.ptr, int64_t(L.geo.n));
+  }
   NNMG_CHECK_LAUNCH();
   if (L.inv_diag.n)
     k_to_f32<<<grid_for(int64_t(L.inv_diag.n), 256), 256, 0, s>>>(L.inv_diag.ptr, L.inv_diag32.ptr,

@@ -48,6 +48,7 @@ struct Level {
   // geometry and of the inverse diagonal
   DevBuf<float> geo32, inv_diag32;
   bool f32_ready = false;
+  bool mixed_arith32 = true;  // fp32 levels: single-precision arithmetic in the register apply (false: fp64 arithmetic on fp32 storage)
   // deterministic mode (level_set_deterministic): cell buffer [nblk][nloc][ncomp][cb]
   // and, per scalar DoF, its slots in a fixed order (CSR)
   bool deterministic = false;

@@ -45,15 +45,22 @@ def _hierarchy(P, tag, precision):
     return g, H, b
 
 
+@pytest.mark.parametrize("arith", ["32", "64"])
 @pytest.mark.parametrize("tag", ["C1_full", "C2_s8", "C3_s8", "C4_s4", "C5_s8"])
-def test_mixed_precision_iterations_match_reference(pkg, tag):
+def test_mixed_precision_iterations_match_reference(pkg, monkeypatch, tag, arith):
+    # NNMG_MIXED_ARITH: 32 (default) = single-precision arithmetic in the register
+    # Laplace apply of the fp32 levels (the paper's fp32 V-cycle); 64 = fp64
+    # arithmetic on fp32 storage everywhere
+    monkeypatch.setenv("NNMG_MIXED_ARITH", arith)
     g, H, b = _hierarchy(pkg, tag, 32)
     assert H.precision == 32
     z32 = H.v_cycle(b)
     H.set_precision(64)
     z64 = H.v_cycle(b)
     assert rel(z64[:: int(g["stride"])], g["vcycle"]) <= 1e-9  # switching back restores the fp64 cycle
-    assert 0 < rel(z32, z64) <= 2e-5  # fp32 storage: single-precision rounding
+    dev = rel(z32, z64)
+    print(tag, arith, "mixed vs fp64 V-cycle", dev)
+    assert 0 < dev <= (2e-5 if arith == "64" else 2e-4)  # single-precision rounding (storage / + arithmetic)
     H.set_precision(32)
     res = pkg.solvers.cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
     assert res.converged
