@@ -55,8 +55,8 @@ struct CellRegElast {
   __host__ __device__ static constexpr int at(int i0, int i1, int i2) { return i0 + N1 * (i1 + N1 * i2); }
   __host__ __device__ __forceinline__ static unsigned bln_phys(unsigned k) { return k + (k >> 3); }
 
-  template <int K, bool TRANS>
-  __device__ __forceinline__ static void sweep_axis(const double (&M)[kMaxN1][kMaxN1], double (&v)[NLOC]) {
+  template <int K, bool TRANS, class TA = double>
+  __device__ __forceinline__ static void sweep_axis(const TA (&M)[kMaxN1][kMaxN1], TA (&v)[NLOC]) {
     constexpr int S0 = K == 0 ? 1 : (K == 1 ? N1 : N1 * N1);
     constexpr int NL = NLOC / N1;
 #pragma unroll
@@ -68,12 +68,12 @@ struct CellRegElast {
         base = (line % N1) + (line / N1) * N1 * N1;
       else
         base = line;
-      double in[N1], out[N1];
+      TA in[N1], out[N1];
 #pragma unroll
       for (int i = 0; i < N1; ++i) in[i] = v[base + i * S0];
 #pragma unroll
       for (int q = 0; q < N1; ++q) {
-        double s = 0.0;
+        TA s = 0;
 #pragma unroll
         for (int i = 0; i < N1; ++i) s = fma(TRANS ? M[i][q] : M[q][i], in[i], s);
         out[q] = s;
@@ -127,7 +127,11 @@ struct CellRegElast {
   // loads per thread), every thread picks its 27 values by list position, and
   // after the transposed sweeps thread i sums the slots of entry i / 3 in a
   // fixed order and issues ONE atomic per node component and block.
-  template <bool kNeg, int GEO = 0, class TV, class TG, bool XCH = false, bool GSM = false, bool BLN = false>
+  // TA: the arithmetic type (double; float = single-precision arithmetic of
+  // the mixed-precision V-cycle: registers, the exchange buffers and with
+  // them the L1 wavefronts of the three phases halve)
+  template <bool kNeg, int GEO = 0, class TV, class TG, bool XCH = false, bool GSM = false, bool BLN = false,
+            class TA = double>
   __device__ __forceinline__ static void run(const Tables& tab, const TV* __restrict__ src, TV* __restrict__ dst,
                                              const int* __restrict__ idx, const TG* __restrict__ geo, int64_t blk,
                                              double lam, double mu, double* sm, double* __restrict__ cellout = nullptr,
@@ -145,9 +149,15 @@ struct CellRegElast {
       }
     }
     static_assert(!GSM || GEO == 0, "TMA staging streams the stored geometry");
+    static_assert(sizeof(TA) == sizeof(double) || (GEO == 0 && !BLN && !GSM),
+                  "single-precision arithmetic: stored geometry, node-major exchange (the buffers are sized in TA)");
     constexpr int XS = xs<GSM>();
-    double* gbuf = sm;                     // [SLICE][3 comps][3 dirs][CB]
-    double* fbuf = GSM ? sm : sm + SLICE * 9 * CB;  // same layout, reference flux (GSM: in place)
+    TA* gbuf = reinterpret_cast<TA*>(sm);  // [SLICE][3 comps][3 dirs][CB]
+    TA* fbuf = GSM ? gbuf : gbuf + SLICE * 9 * CB;  // same layout, reference flux (GSM: in place)
+    TA* smt = gbuf;                        // node-major exchange buffer [l][comp][XS]
+    const auto& tS = TabSel<TA>::S(tab);
+    const auto& tDc = TabSel<TA>::Dc(tab);
+    const TA lamT = TA(lam), muT = TA(mu);
     const TG* gsm = reinterpret_cast<const TG*>(sm + XB);  // GSM: [SLICE][NG][CB] of the current slice
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + XB + GEO_DOUBLES);
     constexpr unsigned kSliceBytes = unsigned(SLICE) * NG * CB * sizeof(TG);
@@ -160,7 +170,7 @@ struct CellRegElast {
         tma_load_1d(sm + XB, gblock, kSliceBytes, bar);
       }
     }
-    double v[NLOC];
+    TA v[NLOC];
     const int* ib = idx + blk * NLOC * CB + lane;
     // node-major exchange coordinates of this thread: cell xc, component xw
     const int xc = threadIdx.x / 3, xw = threadIdx.x % 3;
@@ -222,25 +232,25 @@ struct CellRegElast {
 #pragma unroll
       for (int l = 0; l < NLOC; ++l) {
         const int g = __ldg(xb + l * CB);
-        sm[(l * 3 + xw) * XS + xc] = g >= 0 ? double(__ldg(src + (int64_t)g * 3 + xw)) : 0.0;
+        smt[(l * 3 + xw) * XS + xc] = g >= 0 ? TA(__ldg(src + (int64_t)g * 3 + xw)) : TA(0);
       }
       __syncthreads();
 #pragma unroll
-      for (int l = 0; l < NLOC; ++l) v[l] = sm[(l * 3 + w) * XS + lane];
+      for (int l = 0; l < NLOC; ++l) v[l] = smt[(l * 3 + w) * XS + lane];
       __syncthreads();  // phase A reuses the buffer
     } else {
 #pragma unroll
       for (int l = 0; l < NLOC; ++l) {
         const int g = __ldcs(ib + l * CB);
-        v[l] = g >= 0 ? double(__ldg(src + (int64_t)g * 3 + w)) : 0.0;
+        v[l] = g >= 0 ? TA(__ldg(src + (int64_t)g * 3 + w)) : TA(0);
       }
     }
-    sweep_axis<0, false>(tab.S, v);
-    sweep_axis<1, false>(tab.S, v);
-    sweep_axis<2, false>(tab.S, v);
-    double acc[NLOC];
+    sweep_axis<0, false, TA>(tS, v);
+    sweep_axis<1, false, TA>(tS, v);
+    sweep_axis<2, false, TA>(tS, v);
+    TA acc[NLOC];
 #pragma unroll
-    for (int l = 0; l < NLOC; ++l) acc[l] = 0.0;
+    for (int l = 0; l < NLOC; ++l) acc[l] = 0;
     const TG* gb = geo + blk * (int64_t)NLOC * NG * CB + lane;
     const TG* eb = geo + blk * (int64_t)NE * CB + lane;
     auto e = [&](int b, int k, int a) { return double(__ldg(eb + ((b * 4 + k) * 3 + a) * CB)); };
@@ -276,14 +286,14 @@ struct CellRegElast {
 #pragma unroll
       for (int s = 0; s < SLICE; ++s) {
         const int qx = s % N1, qy = s / N1;
-        double gx = 0.0, gy = 0.0, gz = 0.0;
+        TA gx = 0, gy = 0, gz = 0;
 #pragma unroll
         for (int r = 0; r < N1; ++r) {
-          gx = fma(tab.Dc[qx][r], v[at(r, qy, qz)], gx);
-          gy = fma(tab.Dc[qy][r], v[at(qx, r, qz)], gy);
-          gz = fma(tab.Dc[qz][r], v[at(qx, qy, r)], gz);
+          gx = fma(tDc[qx][r], v[at(r, qy, qz)], gx);
+          gy = fma(tDc[qy][r], v[at(qx, r, qz)], gy);
+          gz = fma(tDc[qz][r], v[at(qx, qy, r)], gz);
         }
-        double* o = gbuf + ((s * 3 + w) * 3) * CB + lane;
+        TA* o = gbuf + ((s * 3 + w) * 3) * CB + lane;
         o[0] = gx;
         o[CB] = gy;
         o[2 * CB] = gz;
@@ -295,12 +305,12 @@ struct CellRegElast {
       for (int k = 0; k < PER; ++k) {
         const int s = w + 3 * k;
         if (s < SLICE) {
-          double g[3][3];
+          TA g[3][3];
 #pragma unroll
           for (int c = 0; c < 3; ++c)
 #pragma unroll
             for (int j = 0; j < 3; ++j) g[c][j] = gbuf[((s * 3 + c) * 3 + j) * CB + lane];
-          double K[3][3], dv;
+          TA K[3][3], dv;
           if constexpr (GEO == 2) {
             // J at (qx, qy, qz) = (w, k, qz); K = J^-1 = C^T / det, dv = det w_q
             const double y = tab.xq[k];
@@ -333,38 +343,38 @@ struct CellRegElast {
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-              for (int b = 0; b < 3; ++b) K[a][b] = double(G[(a * 3 + b) * CB]);
-            dv = double(G[9 * CB]);
+              for (int b = 0; b < 3; ++b) K[a][b] = TA(G[(a * 3 + b) * CB]);
+            dv = TA(G[9 * CB]);
           } else {
             const TG* G = gb + (qz * SLICE + s) * NG * CB;
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-              for (int b = 0; b < 3; ++b) K[a][b] = double(__ldcs(G + (a * 3 + b) * CB));
-            dv = double(__ldcs(G + 9 * CB));
+              for (int b = 0; b < 3; ++b) K[a][b] = TA(__ldcs(G + (a * 3 + b) * CB));
+            dv = TA(__ldcs(G + 9 * CB));
           }
           // pg = ghat J^-1, eps = sym(pg), sigma = 2 mu eps + lam tr(eps) I, flux = sigma J^-T dv
-          double pg[3][3];
+          TA pg[3][3];
 #pragma unroll
           for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int b = 0; b < 3; ++b) {
-              double t = 0.0;
+              TA t = 0;
 #pragma unroll
               for (int j = 0; j < 3; ++j) t = fma(g[a][j], K[j][b], t);
               pg[a][b] = t;
             }
-          const double tr = pg[0][0] + pg[1][1] + pg[2][2];
-          double sig[3][3];
+          const TA tr = pg[0][0] + pg[1][1] + pg[2][2];
+          TA sig[3][3];
 #pragma unroll
           for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int b = 0; b < 3; ++b) sig[a][b] = mu * (pg[a][b] + pg[b][a]) + (a == b ? lam * tr : 0.0);
+            for (int b = 0; b < 3; ++b) sig[a][b] = muT * (pg[a][b] + pg[b][a]) + (a == b ? lamT * tr : TA(0));
 #pragma unroll
           for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-              double t = 0.0;
+              TA t = 0;
 #pragma unroll
               for (int b = 0; b < 3; ++b) t = fma(sig[a][b], K[j][b], t);
               fbuf[((s * 3 + a) * 3 + j) * CB + lane] = t * dv;
@@ -383,13 +393,13 @@ struct CellRegElast {
 #pragma unroll
       for (int s = 0; s < SLICE; ++s) {
         const int qx = s % N1, qy = s / N1;
-        const double* f = fbuf + ((s * 3 + w) * 3) * CB + lane;
-        const double fx = f[0], fy = f[CB], fz = f[2 * CB];
+        const TA* f = fbuf + ((s * 3 + w) * 3) * CB + lane;
+        const TA fx = f[0], fy = f[CB], fz = f[2 * CB];
 #pragma unroll
         for (int r = 0; r < N1; ++r) {
-          acc[at(r, qy, qz)] = fma(tab.Dc[qx][r], fx, acc[at(r, qy, qz)]);
-          acc[at(qx, r, qz)] = fma(tab.Dc[qy][r], fy, acc[at(qx, r, qz)]);
-          acc[at(qx, qy, r)] = fma(tab.Dc[qz][r], fz, acc[at(qx, qy, r)]);
+          acc[at(r, qy, qz)] = fma(tDc[qx][r], fx, acc[at(r, qy, qz)]);
+          acc[at(qx, r, qz)] = fma(tDc[qy][r], fy, acc[at(qx, r, qz)]);
+          acc[at(qx, qy, r)] = fma(tDc[qz][r], fz, acc[at(qx, qy, r)]);
         }
       }
       // the next slice's phase A overwrites gbuf only after every thread
@@ -400,9 +410,9 @@ struct CellRegElast {
         if (qz + 1 < N1) __syncthreads();
       }
     }
-    sweep_axis<2, true>(tab.S, acc);
-    sweep_axis<1, true>(tab.S, acc);
-    sweep_axis<0, true>(tab.S, acc);
+    sweep_axis<2, true, TA>(tS, acc);
+    sweep_axis<1, true, TA>(tS, acc);
+    sweep_axis<0, true, TA>(tS, acc);
     if constexpr (BLN) {
       if (!cellout) {
         // block-local sums in shared memory without atomics: warp w owns
@@ -446,13 +456,13 @@ struct CellRegElast {
       if (!cellout) {
         __syncthreads();  // every thread is done with the phase buffers
 #pragma unroll
-        for (int l = 0; l < NLOC; ++l) sm[(l * 3 + w) * XS + lane] = acc[l];
+        for (int l = 0; l < NLOC; ++l) smt[(l * 3 + w) * XS + lane] = acc[l];
         __syncthreads();
         const int* xb = idx + blk * NLOC * CB + xc;
 #pragma unroll
         for (int l = 0; l < NLOC; ++l) {
           const int g = __ldg(xb + l * CB);
-          const double a = sm[(l * 3 + xw) * XS + xc];
+          const TA a = smt[(l * 3 + xw) * XS + xc];
           if (g >= 0) atomicAdd(dst + (int64_t)g * 3 + xw, TV(kNeg ? -a : a));
         }
         return;

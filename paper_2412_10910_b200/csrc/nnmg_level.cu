@@ -562,18 +562,20 @@ __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const doubl
 
 // 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
 template <int P, bool NEG, int GEO = 0, class TV = double, class TG = double, bool XCH = false, bool GSM = false,
-          bool BLN = false>
-__global__ void __launch_bounds__(96, 4) k_apply_reg_elast(Tables tab, const TV* __restrict__ src,
+          bool BLN = false, class TA = double>
+__global__ void __launch_bounds__(96, sizeof(TA) == sizeof(float) ? 5 : 4) k_apply_reg_elast(Tables tab, const TV* __restrict__ src,
                                                         TV* __restrict__ dst, const int* __restrict__ idx,
                                                         const TG* __restrict__ geo, int64_t b0, int64_t b1,
                                                         double lam, double mu, const int* __restrict__ cd, int64_t ncd,
                                                         double* __restrict__ cellout = nullptr, BlnTables bln = {}) {
-  __shared__ __align__(128) double sm[CellRegElast<P>::SMEM_DOUBLES];
+  // sized in elements of the arithmetic type: the fp32 exchange buffers take half the bytes
+  __shared__ __align__(128) TA smt[CellRegElast<P>::SMEM_DOUBLES];
+  double* sm = reinterpret_cast<double*>(smt);
   if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x;
   if (blk >= b1) return;
-  CellRegElast<P>::template run<NEG, GEO, TV, TG, XCH, GSM, BLN>(tab, src, dst, idx, geo, blk, lam, mu, sm, cellout,
-                                                                 bln);
+  CellRegElast<P>::template run<NEG, GEO, TV, TG, XCH, GSM, BLN, TA>(tab, src, dst, idx, geo, blk, lam, mu, sm,
+                                                                     cellout, bln);
 }
 
 // per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
@@ -686,8 +688,11 @@ struct ApplyLaunchT {
     }
     if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported && !kF64) {
       if (L.reg_kernel) {
-        k_apply_reg_elast<P, true, 0, float, float, true><<<static_cast<unsigned>(b1 - b0), 96, 0, s>>>(
-            L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, L.lam, L.mu, cd, ncd);
+        // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
+        auto kr = L.mixed_arith32 ? k_apply_reg_elast<P, true, 0, float, float, true, false, false, float>
+                                  : k_apply_reg_elast<P, true, 0, float, float, true, false, false, double>;
+        kr<<<static_cast<unsigned>(b1 - b0), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, L.lam, L.mu,
+                                                          cd, ncd, nullptr, BlnTables{});
         fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();

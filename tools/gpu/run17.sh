@@ -1,11 +1,11 @@
 #!/bin/bash
-# mixed-precision cycle with single-precision arithmetic in the register apply
+# mixed-precision cycle with single-precision arithmetic: tests + bench of the given configs
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_mixed.py -q -x -s > gpurun_out/r2_g17_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/r2_g17_tests.log
-grep "mixed vs\|passed\|failed\|rc=" gpurun_out/r2_g17_tests.log | tail -14
-for a in 32 64; do for c in C3 C2; do
+grep "mixed vs\|passed\|failed\|rc=\|Error\|assert" gpurun_out/r2_g17_tests.log | tail -16
+for a in 32 64; do for c in "$@"; do
   NNMG_MIXED_ARITH=$a timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_g17_${c}_a$a.json 2> gpurun_out/r2_g17_${c}_a$a.err
   python - <<PY
 import json
