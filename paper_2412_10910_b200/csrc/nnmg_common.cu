@@ -142,6 +142,10 @@ Tables make_tables(int degree) {
       t.S32[a][i] = static_cast<float>(t.S[a][i]);
       t.Dc32[a][i] = static_cast<float>(t.Dc[a][i]);
     }
+  for (int i = 0; i < kMaxN1; ++i) {
+    t.nodes32[i] = static_cast<float>(t.nodes[i]);
+    t.rdenom32[i] = static_cast<float>(t.rdenom[i]);
+  }
   return t;
 }
 

@@ -121,6 +121,8 @@ struct Tables {
   // fp32 copies for the single-precision arithmetic of the mixed-precision V-cycle
   float S32[kMaxN1][kMaxN1];
   float Dc32[kMaxN1][kMaxN1];
+  float nodes32[kMaxN1];
+  float rdenom32[kMaxN1];
 };
 
 // sweep matrices in the arithmetic type TA
@@ -130,11 +132,15 @@ template <>
 struct TabSel<double> {
   __host__ __device__ static const double (&S(const Tables& t))[kMaxN1][kMaxN1] { return t.S; }
   __host__ __device__ static const double (&Dc(const Tables& t))[kMaxN1][kMaxN1] { return t.Dc; }
+  __host__ __device__ static const double (&nodes(const Tables& t))[kMaxN1] { return t.nodes; }
+  __host__ __device__ static const double (&rdenom(const Tables& t))[kMaxN1] { return t.rdenom; }
 };
 template <>
 struct TabSel<float> {
   __host__ __device__ static const float (&S(const Tables& t))[kMaxN1][kMaxN1] { return t.S32; }
   __host__ __device__ static const float (&Dc(const Tables& t))[kMaxN1][kMaxN1] { return t.Dc32; }
+  __host__ __device__ static const float (&nodes(const Tables& t))[kMaxN1] { return t.nodes32; }
+  __host__ __device__ static const float (&rdenom(const Tables& t))[kMaxN1] { return t.rdenom32; }
 };
 
 Tables make_tables(int degree);

@@ -41,6 +41,9 @@ struct TransferDispatchT {
       auto kp = k_prolongate<D, P, NC, CBC, PPL, TV, TV>;
       if constexpr (kF64 && PPL == 1)
         if (T.prolong_ppl == 2) kp = k_prolongate<D, P, NC, CBC, 2>;
+      // fp32 levels: single-precision arithmetic unless NNMG_MIXED_ARITH=64
+      if constexpr (!kF64)
+        if (T.mixed_arith32) kp = k_prolongate<D, P, NC, CBC, PPL, TV, TV, float>;
       kp<<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.nitems == T.ncc ? nullptr : T.item_cell.ptr,
                                    T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems);
       NNMG_CHECK_LAUNCH();
@@ -57,9 +60,11 @@ struct TransferDispatchT {
         // (C2 0.022 vs 0.025 ms with 3); 4 points measured slower in both
         const int rk = T.restrict_kernel >= 0 ? T.restrict_kernel : (D == 3 ? 3 : 1);
         if constexpr (!kF64) {
-          (D == 3 ? k_restrict_lane<D, P, NC, 3, TV, TV> : k_restrict_lane<D, P, NC, 1, TV, TV>)
-              <<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems,
-                                                                 ch, T.cellbuf.ptr);
+          auto kl = D == 3 ? k_restrict_lane<D, P, NC, 3, TV, TV> : k_restrict_lane<D, P, NC, 1, TV, TV>;
+          if (T.mixed_arith32)
+            kl = D == 3 ? k_restrict_lane<D, P, NC, 3, TV, TV, float> : k_restrict_lane<D, P, NC, 1, TV, TV, float>;
+          kl<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch,
+                                                             T.cellbuf.ptr);
         } else if (rk != 2) {
           auto k = rk == 0 ? k_restrict_lane<D, P, NC, 1>
                    : rk == 3 ? k_restrict_lane<D, P, NC, 3>
@@ -91,8 +96,18 @@ struct TransferDispatchT {
               C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         }
       } else {
-        k_restrict_staged<D, P, NC, TV, TV><<<grid_for(nwarps, W), W * 32, 0, s>>>(
-            C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
+        bool done = false;
+        if constexpr (!kF64) {
+          if (T.mixed_arith32) {
+            constexpr int WF = StagedRestrict<D, P, NC, 1, float>::WARPS;
+            k_restrict_staged<D, P, NC, TV, TV, 1, float><<<grid_for(nwarps, WF), WF * 32, 0, s>>>(
+                C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
+            done = true;
+          }
+        }
+        if (!done)
+          k_restrict_staged<D, P, NC, TV, TV><<<grid_for(nwarps, W), W * 32, 0, s>>>(
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
       }
       NNMG_CHECK_LAUNCH();
       if (T.timing) NNMG_CUDA_TRY(cudaEventRecord(T.ev[1], s));
@@ -216,6 +231,8 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
       // staged groups: planes of the outermost axis per lane (1 or 2)
       const char* pl = getenv("NNMG_RESTRICT_PL");
       T->restrict_pl = pl ? atoi(pl) : 1;
+      const char* ma = getenv("NNMG_MIXED_ARITH");
+      T->mixed_arith32 = ma ? atoi(ma) != 64 : true;
     }
     // fine scalar DoFs without a transfer point: zeroed by the plain prolongation
     std::vector<uint8_t> has(fine->n_scalar, 0);

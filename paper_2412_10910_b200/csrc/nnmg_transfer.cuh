@@ -15,6 +15,7 @@ struct Transfer {
   int chunk = 1;            // coarse cells per warp in the restriction
   int restrict_kernel = -1;  // variant for NLOC*NCOMP <= 32 (see transfer_create; -1: by dimension)
   int restrict_wide = 0;    // 32 < NLOC*NCOMP <= 81: lane-owned local vector instead of staged groups
+  bool mixed_arith32 = true;  // fp32 vectors: single-precision arithmetic in the transfer kernels
   int restrict_pl = 1;      // staged restriction: planes of the outermost axis per lane (1, 2)
   int prolong_ppl = 1;      // 2: two points per lane also where one is the default
   DevBuf<int> cell_start;   // [ncc+1] CSR of points by owning coarse cell

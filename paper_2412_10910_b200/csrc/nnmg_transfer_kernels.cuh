@@ -24,22 +24,22 @@ static constexpr int kTransferWarps = 4;  // coarse cells (one per warp) per thr
 // end nodes are exactly 0 and 1, nnmg_common.cu).  The 1/denom factors are
 // per local DoF, so the kernels apply their tensor product once per cell
 // (staged coarse values, cell-end sums) instead of once per point.
-template <int N1>
-__device__ __forceinline__ void lagrange_un(const Tables& tab, double t, double (&out)[N1]) {
+template <int N1, class TA = double>
+__device__ __forceinline__ void lagrange_un(const Tables& tab, TA t, TA (&out)[N1]) {
   if constexpr (N1 == 1) {
-    out[0] = 1.0;
+    out[0] = TA(1);
   } else {
-    double d[N1];
+    TA d[N1];
     d[0] = t;
 #pragma unroll
-    for (int j = 1; j < N1 - 1; ++j) d[j] = t - tab.nodes[j];
-    d[N1 - 1] = t - 1.0;
-    double suf[N1];
+    for (int j = 1; j < N1 - 1; ++j) d[j] = t - TabSel<TA>::nodes(tab)[j];
+    d[N1 - 1] = t - TA(1);
+    TA suf[N1];
     suf[N1 - 1] = d[N1 - 1];
 #pragma unroll
     for (int j = N1 - 2; j >= 1; --j) suf[j] = d[j] * suf[j + 1];
     out[0] = suf[1];
-    double pre = d[0];
+    TA pre = d[0];
 #pragma unroll
     for (int i = 1; i < N1 - 1; ++i) {
       out[i] = pre * suf[i + 1];
@@ -50,13 +50,13 @@ __device__ __forceinline__ void lagrange_un(const Tables& tab, double t, double 
 }
 
 // prod_j 1/denom[l_j] of local point l (x fastest)
-template <int DIM, int N1>
-__device__ __forceinline__ double lagrange_norm(const Tables& tab, int l) {
-  double r = tab.rdenom[l % N1];
+template <int DIM, int N1, class TA = double>
+__device__ __forceinline__ TA lagrange_norm(const Tables& tab, int l) {
+  TA r = TabSel<TA>::rdenom(tab)[l % N1];
 #pragma unroll
   for (int j = 1; j < DIM; ++j) {
     l /= N1;
-    r *= tab.rdenom[l % N1];
+    r *= TabSel<TA>::rdenom(tab)[l % N1];
   }
   return r;
 }
@@ -68,26 +68,26 @@ __device__ __forceinline__ double lagrange_norm(const Tables& tab, int l) {
 // records of the next round are loaded before the current round's arithmetic.
 // Contraction order x, y, z as transfer.py:93-95.
 // ---------------------------------------------------------------------------
-template <int DIM, int N1>
-__device__ __forceinline__ double contract(const double* __restrict__ U, const double (&X)[DIM][N1]) {
+template <int DIM, int N1, class TA = double>
+__device__ __forceinline__ TA contract(const TA* __restrict__ U, const TA (&X)[DIM][N1]) {
   if constexpr (DIM == 2) {
-    double val = 0.0;
+    TA val = 0;
 #pragma unroll
     for (int i1 = 0; i1 < N1; ++i1) {
-      double s = 0.0;
+      TA s = 0;
 #pragma unroll
       for (int i0 = 0; i0 < N1; ++i0) s = fma(U[i0 + N1 * i1], X[0][i0], s);
       val = fma(s, X[1][i1], val);
     }
     return val;
   } else {
-    double val = 0.0;
+    TA val = 0;
 #pragma unroll
     for (int i2 = 0; i2 < N1; ++i2) {
-      double s2 = 0.0;
+      TA s2 = 0;
 #pragma unroll
       for (int i1 = 0; i1 < N1; ++i1) {
-        double s = 0.0;
+        TA s = 0;
 #pragma unroll
         for (int i0 = 0; i0 < N1; ++i0) s = fma(U[i0 + N1 * i1 + N1 * N1 * i2], X[0][i0], s);
         s2 = fma(s, X[1][i1], s2);
@@ -107,15 +107,18 @@ __host__ __device__ constexpr int prolongate_ppl() {
 }
 
 // TV / TX: storage types of the vectors and of xhat (double, or float in the
-// mixed-precision V-cycle); the arithmetic is fp64
-template <int DIM, int PC, int NCOMP, int CBC, int PPL, class TV = double, class TX = double>
+// mixed-precision V-cycle); TA: the arithmetic type (float = the paper's
+// single-precision V-cycle; fp64 arithmetic on fp32 storage pays F2F
+// conversions on every record: the fp32 restriction measured 206 us against
+// 159 us in fp64 on C3)
+template <int DIM, int PC, int NCOMP, int CBC, int PPL, class TV = double, class TX = double, class TA = double>
 __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NCOMP > 1) ? 4 : 6)
     k_prolongate(Tables tab, const TV* __restrict__ uc, TV* __restrict__ uf, int accumulate,
                  const int* __restrict__ cidx, const int* __restrict__ item_cell, const int* __restrict__ item_pt,
                  const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t nitems) {
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
-  __shared__ double su[kTransferWarps][NCOMP * NLOC];
+  __shared__ TA su[kTransferWarps][NCOMP * NLOC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t item = blockIdx.x * (int64_t)kTransferWarps + warp;
   if (item >= nitems) return;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
   constexpr int STEP = 32 * PPL;
   // first round's records are in flight while the coarse values are staged
   int dd[PPL];
-  double xt[PPL][DIM];
+  TA xt[PPL][DIM];
   auto load = [&](int base) {
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
       const bool ok = p < p1;
       dd[k] = ok ? __ldcs(pt_dof + p) : -1;
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) xt[k][j] = ok ? double(__ldcs(xhat + (int64_t)p * DIM + j)) : 0.5;
+      for (int j = 0; j < DIM; ++j) xt[k][j] = ok ? TA(__ldcs(xhat + (int64_t)p * DIM + j)) : TA(0.5);
     }
   };
   load(p0);
@@ -142,28 +145,28 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
     const int g = cidx[(blk * NLOC + l) * CBC + cl];
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c)
-      su[warp][c * NLOC + l] = g >= 0 ? double(uc[(int64_t)g * NCOMP + c]) * lagrange_norm<DIM, N1>(tab, l) : 0.0;
+      su[warp][c * NLOC + l] = g >= 0 ? TA(uc[(int64_t)g * NCOMP + c]) * lagrange_norm<DIM, N1, TA>(tab, l) : TA(0);
   }
   __syncwarp();
   for (int base = p0; base < p1; base += STEP) {
     int cd[PPL];
-    double X[PPL][DIM][N1];
+    TA X[PPL][DIM][N1];
 #pragma unroll
     for (int k = 0; k < PPL; ++k) {
       cd[k] = dd[k];
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) lagrange_un<N1>(tab, xt[k][j], X[k][j]);
+      for (int j = 0; j < DIM; ++j) lagrange_un<N1, TA>(tab, xt[k][j], X[k][j]);
     }
     if (base + STEP < p1) load(base + STEP);
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c) {
-      const double* U = su[warp] + c * NLOC;
+      const TA* U = su[warp] + c * NLOC;
 #pragma unroll
       for (int k = 0; k < PPL; ++k) {
-        const double a = contract<DIM, N1>(U, X[k]);
+        const TA a = contract<DIM, N1, TA>(U, X[k]);
         if (cd[k] >= 0) {
           TV* o = uf + (int64_t)cd[k] * NCOMP + c;
-          *o = TV(accumulate ? double(*o) + a : a);
+          *o = TV(accumulate ? TA(*o) + a : a);
         }
       }
     }
@@ -227,10 +230,10 @@ __device__ __forceinline__ void zero_empty_cells(const CellRounds& R, int64_t c0
 }
 
 // per-lane point records of one round: point p = base + k*stride + off
-template <int DIM, int NCOMP, int PPR>
+template <int DIM, int NCOMP, int PPR, class TA = double>
 struct PointRec {
   int d[PPR];
-  double x[PPR][DIM];
+  TA x[PPR][DIM];
   template <class TX>
   __device__ __forceinline__ void load(const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int base,
                                        int end, int stride, int off, bool live) {
@@ -240,22 +243,22 @@ struct PointRec {
       const bool ok = live && p < end;
       d[k] = ok ? __ldcs(pt_dof + p) : -1;
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) x[k][j] = ok ? double(__ldcs(xhat + (int64_t)p * DIM + j)) : 0.5;
+      for (int j = 0; j < DIM; ++j) x[k][j] = ok ? TA(__ldcs(xhat + (int64_t)p * DIM + j)) : TA(0.5);
     }
   }
   template <class TV>
-  __device__ __forceinline__ void values(const TV* __restrict__ rf, double (&v)[PPR][NCOMP]) const {
+  __device__ __forceinline__ void values(const TV* __restrict__ rf, TA (&v)[PPR][NCOMP]) const {
 #pragma unroll
     for (int k = 0; k < PPR; ++k)
 #pragma unroll
-      for (int c = 0; c < NCOMP; ++c) v[k][c] = d[k] >= 0 ? double(rf[(int64_t)d[k] * NCOMP + c]) : 0.0;
+      for (int c = 0; c < NCOMP; ++c) v[k][c] = d[k] >= 0 ? TA(rf[(int64_t)d[k] * NCOMP + c]) : TA(0);
   }
 };
 
 // The pipelined round loop shared by the restriction kernels.  body(rec_x, v)
 // evaluates the current round; flush(ci) is called after the last round of
 // chunk cell ci.
-template <int DIM, int NCOMP, int PPR, class TX, class TV, class Body, class Flush>
+template <int DIM, int NCOMP, int PPR, class TA = double, class TX, class TV, class Body, class Flush>
 __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __restrict__ pt_dof,
                                               const TX* __restrict__ xhat, const TV* __restrict__ rf,
                                               int stride, int off, bool live, Body&& body, Flush&& flush) {
@@ -267,10 +270,10 @@ __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __
   R.next(ciB, bB, rs);
   int ciC = ciB, bC = bB;
   R.next(ciC, bC, rs);
-  PointRec<DIM, NCOMP, PPR> rA, rB, rC;
+  PointRec<DIM, NCOMP, PPR, TA> rA, rB, rC;
   rA.load(pt_dof, xhat, bA, R.end(ciA), stride, off, live && ciA < R.nch);
   rB.load(pt_dof, xhat, bB, R.end(ciB), stride, off, live && ciB < R.nch);
-  double vA[PPR][NCOMP], vB[PPR][NCOMP];
+  TA vA[PPR][NCOMP], vB[PPR][NCOMP];
   rA.values(rf, vA);
   while (ciA < R.nch) {
     rB.values(rf, vB);
@@ -294,7 +297,7 @@ __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __
 // 32: Q1/Q2 scalar, 2D vector; up to 81 with NNMG_RESTRICT_WIDE: 3D Q2
 // elasticity, Q3 scalar); a cell's lanes are combined through shared memory
 // at the cell end, 32 outputs at a time, lane l ending with output l of a tile.
-template <int DIM, int PC, int NCOMP, int PPR, class TV = double, class TX = double>
+template <int DIM, int PC, int NCOMP, int PPR, class TV = double, class TX = double, class TA = double>
 __global__ void __launch_bounds__(kTransferWarps * 32)
     k_restrict_lane(Tables tab, const TV* __restrict__ rf, const int* __restrict__ cell_start,
                     const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t ncc, int chunk,
@@ -317,28 +320,28 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
   // flush is conditional).
   constexpr int TW = NOUT < 32 ? NOUT : 32;
   constexpr int RS = TW | 1;
-  __shared__ double red[kTransferWarps][32 * RS];
-  double* rw = red[warp];
-  double acc[NOUT];
+  __shared__ TA red[kTransferWarps][32 * RS];
+  TA* rw = red[warp];
+  TA acc[NOUT];
 #pragma unroll
-  for (int o = 0; o < NOUT; ++o) acc[o] = 0.0;
-  stream_rounds<DIM, NCOMP, PPR>(
+  for (int o = 0; o < NOUT; ++o) acc[o] = 0;
+  stream_rounds<DIM, NCOMP, PPR, TA>(
       R, pt_dof, xhat, rf, 32, lane, true,
-      [&](const double (&xs)[PPR][DIM], const double (&vs)[PPR][NCOMP]) {
+      [&](const TA (&xs)[PPR][DIM], const TA (&vs)[PPR][NCOMP]) {
 #pragma unroll
         for (int k = 0; k < PPR; ++k) {
-          double X[DIM][N1];
+          TA X[DIM][N1];
 #pragma unroll
-          for (int j = 0; j < DIM; ++j) lagrange_un<N1>(tab, xs[k][j], X[j]);
+          for (int j = 0; j < DIM; ++j) lagrange_un<N1, TA>(tab, xs[k][j], X[j]);
 #pragma unroll
           for (int c = 0; c < NCOMP; ++c) {
             if constexpr (DIM == 3) {
 #pragma unroll
               for (int i2 = 0; i2 < N1; ++i2) {
-                const double a = vs[k][c] * X[2][i2];
+                const TA a = vs[k][c] * X[2][i2];
 #pragma unroll
                 for (int i1 = 0; i1 < N1; ++i1) {
-                  const double b = a * X[1][i1];
+                  const TA b = a * X[1][i1];
 #pragma unroll
                   for (int i0 = 0; i0 < N1; ++i0) {
                     const int o = (i0 + N1 * (i1 + N1 * i2)) * NCOMP + c;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
             } else {
 #pragma unroll
               for (int i1 = 0; i1 < N1; ++i1) {
-                const double b = vs[k][c] * X[1][i1];
+                const TA b = vs[k][c] * X[1][i1];
 #pragma unroll
                 for (int i0 = 0; i0 < N1; ++i0) {
                   const int o = (i0 + N1 * i1) * NCOMP + c;
@@ -367,15 +370,15 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
           for (int j = 0; j < TW; ++j)
             if (t0 + j < NOUT) {
               rw[lane * RS + j] = acc[t0 + j];
-              acc[t0 + j] = 0.0;
+              acc[t0 + j] = 0;
             }
           __syncwarp();
           const int o = t0 + lane;
           if (lane < TW && o < NOUT) {
-            double r = 0.0;
+            TA r = 0;
 #pragma unroll
             for (int sl = 0; sl < 32; ++sl) r += rw[sl * RS + lane];
-            cellbuf[(c0 + ci) * NOUT + o] = r * lagrange_norm<DIM, N1>(tab, o / NCOMP);
+            cellbuf[(c0 + ci) * NOUT + o] = double(r * lagrange_norm<DIM, N1, TA>(tab, o / NCOMP));
           }
           __syncwarp();
         }
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
 // bound by its table reads, so PL = 2 (10 points instead of 6 per sub-round
 // for Q4, the same reads) trades idle lanes of the last slot lane for
 // 40% fewer reads per point.
-template <int DIM, int PC, int NCOMP, int PL = 1>
+template <int DIM, int PC, int NCOMP, int PL = 1, class TA = double>
 struct StagedRestrict {
   static constexpr int N1 = PC + 1;
   static constexpr int NLOC = ipow(N1, DIM);
@@ -415,49 +418,64 @@ struct StagedRestrict {
   static constexpr int OV = OZ + N1;
   static constexpr int REC0 = OV + NCOMP;
   static constexpr int REC = ((REC0 - 2 + 15) / 16) * 16 + 2;
-  static constexpr int WARP_DOUBLES = (2 * P * REC + SLOTS * N1 * PLANE + 1) & ~1;  // keeps 16-byte alignment
-  static constexpr int WARPS = (48 * 1024) / (WARP_DOUBLES * 8) >= kTransferWarps
+  // per-warp buffer in elements of the arithmetic type (even: keeps the 2-element alignment)
+  static constexpr int WARP_DOUBLES = (2 * P * REC + SLOTS * N1 * PLANE + 1) & ~1;
+  static constexpr int WARP_BYTES = WARP_DOUBLES * int(sizeof(TA));
+  static constexpr int WARPS = (48 * 1024) / WARP_BYTES >= kTransferWarps
                                    ? kTransferWarps
-                                   : ((48 * 1024) / (WARP_DOUBLES * 8) >= 1 ? (48 * 1024) / (WARP_DOUBLES * 8) : 1);
+                                   : ((48 * 1024) / WARP_BYTES >= 1 ? (48 * 1024) / WARP_BYTES : 1);
 };
 
-template <int DIM, int PC, int NCOMP, class TV = double, class TX = double, int PL = 1>
-__global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL>::WARPS * 32)
+// two consecutive staged table entries in one load (16 bytes in fp64, 8 in fp32)
+template <class TA>
+struct Pair2;
+template <>
+struct Pair2<double> {
+  using type = double2;
+};
+template <>
+struct Pair2<float> {
+  using type = float2;
+};
+
+template <int DIM, int PC, int NCOMP, class TV = double, class TX = double, int PL = 1, class TA = double>
+__global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL, TA>::WARPS * 32)
     k_restrict_staged(Tables tab, const TV* __restrict__ rf, const int* __restrict__ cell_start,
                       const int* __restrict__ pt_dof, const TX* __restrict__ xhat, int64_t ncc, int chunk,
                       double* __restrict__ cellbuf) {
-  using K = StagedRestrict<DIM, PC, NCOMP, PL>;
+  using K = StagedRestrict<DIM, PC, NCOMP, PL, TA>;
+  using V2 = typename Pair2<TA>::type;
   constexpr int N1 = K::N1, G = K::G, SLOTS = K::SLOTS, SUB = K::SUB, P = K::P, INNER = K::INNER,
                 PLANE = K::PLANE, REC = K::REC, NOUT = K::NOUT;
-  __shared__ __align__(16) double smem[K::WARPS][K::WARP_DOUBLES];
+  __shared__ __align__(16) TA smem[K::WARPS][K::WARP_DOUBLES];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = (blockIdx.x * (int64_t)K::WARPS + warp) * chunk;
   if (c0 >= ncc) return;
   const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
-  double* stage = smem[warp];                // [2][P][REC]
-  double* red = smem[warp] + 2 * P * REC;    // [SLOTS][N1][PLANE]
+  TA* stage = smem[warp];                // [2][P][REC]
+  TA* red = smem[warp] + 2 * P * REC;    // [SLOTS][N1][PLANE]
   const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
   zero_empty_cells(R, c0, NOUT, lane, cellbuf);
   const int slot = lane / G, g = lane % G;
   const bool grp = slot < SLOTS;
-  double acc[PL][INNER][NCOMP];
+  TA acc[PL][INNER][NCOMP];
 #pragma unroll
   for (int p = 0; p < PL; ++p)
 #pragma unroll
     for (int i = 0; i < INNER; ++i)
 #pragma unroll
-      for (int c = 0; c < NCOMP; ++c) acc[p][i][c] = 0.0;
+      for (int c = 0; c < NCOMP; ++c) acc[p][i][c] = 0;
   int buf = 0;
-  stream_rounds<DIM, NCOMP, 1>(
+  stream_rounds<DIM, NCOMP, 1, TA>(
       R, pt_dof, xhat, rf, P, lane, lane < P,
-      [&](const double (&xs)[1][DIM], const double (&vs)[1][NCOMP]) {
+      [&](const TA (&xs)[1][DIM], const TA (&vs)[1][NCOMP]) {
         // stage this lane's point: 1D tables and values
-        double* st = stage + buf * P * REC;
+        TA* st = stage + buf * P * REC;
         if (lane < P) {
-          double X[N1];
+          TA X[N1];
 #pragma unroll
           for (int j = 0; j < DIM; ++j) {
-            lagrange_un<N1>(tab, xs[0][j], X);
+            lagrange_un<N1, TA>(tab, xs[0][j], X);
 #pragma unroll
             for (int i = 0; i < N1; ++i) st[lane * REC + (j == 0 ? 0 : (j == DIM - 1 ? K::OZ : K::A)) + i] = X[i];
           }
@@ -468,36 +486,36 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL>::WARPS * 32
         if (grp) {
 #pragma unroll 1
           for (int s = 0; s < SUB; ++s) {
-            const double* q = st + (s * SLOTS + slot) * REC;
-            double X0[K::A], X1[DIM == 3 ? K::A : 1];
+            const TA* q = st + (s * SLOTS + slot) * REC;
+            TA X0[K::A], X1[DIM == 3 ? K::A : 1];
 #pragma unroll
             for (int i = 0; i < K::A; i += 2) {
-              const double2 t = *reinterpret_cast<const double2*>(q + i);
+              const V2 t = *reinterpret_cast<const V2*>(q + i);
               X0[i] = t.x;
               X0[i + 1] = t.y;
             }
             if constexpr (DIM == 3) {
 #pragma unroll
               for (int i = 0; i < K::A; i += 2) {
-                const double2 t = *reinterpret_cast<const double2*>(q + K::A + i);
+                const V2 t = *reinterpret_cast<const V2*>(q + K::A + i);
                 X1[i] = t.x;
                 X1[i + 1] = t.y;
               }
             }
             // this lane's planes g PL .. g PL + PL - 1 (a plane past N1 - 1 adds zeros)
-            double z[PL];
+            TA z[PL];
 #pragma unroll
-            for (int p = 0; p < PL; ++p) z[p] = g * PL + p < N1 ? q[K::OZ + g * PL + p] : 0.0;
+            for (int p = 0; p < PL; ++p) z[p] = g * PL + p < N1 ? q[K::OZ + g * PL + p] : TA(0);
 #pragma unroll
             for (int c = 0; c < NCOMP; ++c) {
-              const double v = q[K::OV + c];
+              const TA v = q[K::OV + c];
 #pragma unroll
               for (int p = 0; p < PL; ++p) {
-                const double a = v * z[p];
+                const TA a = v * z[p];
                 if constexpr (DIM == 3) {
 #pragma unroll
                   for (int i1 = 0; i1 < N1; ++i1) {
-                    const double b = a * X1[i1];
+                    const TA b = a * X1[i1];
 #pragma unroll
                     for (int i0 = 0; i0 < N1; ++i0)
                       acc[p][i0 + N1 * i1][c] = fma(b, X0[i0], acc[p][i0 + N1 * i1][c]);
@@ -527,16 +545,16 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL>::WARPS * 32
 #pragma unroll
             for (int i = 0; i < INNER; ++i)
 #pragma unroll
-              for (int c = 0; c < NCOMP; ++c) acc[p][i][c] = 0.0;
+              for (int c = 0; c < NCOMP; ++c) acc[p][i][c] = 0;
         }
         __syncwarp();
         // output o = l * NCOMP + c with l = plane * INNER + i: slot sum in fixed order
         for (int o = lane; o < NOUT; o += 32) {
           const int plane = o / PLANE, k = o % PLANE;
-          double sum = 0.0;
+          TA sum = 0;
 #pragma unroll
           for (int sl = 0; sl < SLOTS; ++sl) sum += red[(sl * N1 + plane) * PLANE + k];
-          cellbuf[(c0 + ci) * NOUT + o] = sum * lagrange_norm<DIM, N1>(tab, o / NCOMP);
+          cellbuf[(c0 + ci) * NOUT + o] = double(sum * lagrange_norm<DIM, N1, TA>(tab, o / NCOMP));
         }
         __syncwarp();
       });
