@@ -185,6 +185,10 @@ int nnmg_coarse_cg_create(nnmg_level_t level, double reduction, int max_iter, nn
  * read.  The library packs it into symmetric 64x64 tiles (nf^2/2 doubles
  * streamed per solve, no atomics: bitwise reproducible). */
 int nnmg_coarse_direct_create(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out);
+/* the same with the tiles stored in fp32 (half the streamed bytes;
+ * single-precision products within a tile, fp64 partial sums): the coarse
+ * solver of the mixed-precision cycle, see nnmg_vcycle_set_mixed_coarse */
+int nnmg_coarse_direct_create_f32(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out);
 int nnmg_coarse_destroy(nnmg_coarse_t coarse);
 int nnmg_coarse_solve(nnmg_coarse_t coarse, const double* b_dev, double* x_dev, void* stream);
 /* iterations / converged / indefinite flag of the last CG solve (synchronises) */
@@ -208,6 +212,9 @@ int nnmg_vcycle_run(nnmg_vcycle_t vcycle, const double* f_dev, double* x_dev, vo
  * registers, the coarse solve in fp64; f_dev / x_dev stay fp64.  Parity is by
  * outer CG iteration count. */
 int nnmg_vcycle_set_precision(nnmg_vcycle_t vcycle, int bits);
+/* coarse solver the mixed-precision cycle uses instead of the fp64 cycle's
+ * (NULL: the same one); the caller keeps it alive while it is attached */
+int nnmg_vcycle_set_mixed_coarse(nnmg_vcycle_t vcycle, nnmg_coarse_t coarse);
 /* capture the cycle for (f_dev, x_dev) into a CUDA graph and replay it on run */
 int nnmg_vcycle_use_graph(nnmg_vcycle_t vcycle, int enable);
 /* number of kernels one cycle launches (for graph replays) */

@@ -73,6 +73,7 @@ _SIGNATURES = {
     "nnmg_coarse_dense_create": [_handle, c_void_p, POINTER(_handle)],
     "nnmg_coarse_cg_create": [_handle, c_double, c_int, POINTER(_handle)],
     "nnmg_coarse_direct_create": [_handle, c_void_p, c_int64, POINTER(_handle)],
+    "nnmg_coarse_direct_create_f32": [_handle, c_void_p, c_int64, POINTER(_handle)],
     "nnmg_coarse_destroy": [_handle],
     "nnmg_coarse_solve": [_handle, c_void_p, c_void_p, c_void_p],
     "nnmg_coarse_status": [_handle, POINTER(c_int), POINTER(c_int), POINTER(c_int)],
@@ -83,6 +84,7 @@ _SIGNATURES = {
     "nnmg_vcycle_run": [_handle, c_void_p, c_void_p, c_void_p],
     "nnmg_vcycle_use_graph": [_handle, c_int],
     "nnmg_vcycle_set_precision": [_handle, c_int],
+    "nnmg_vcycle_set_mixed_coarse": [_handle, _handle],
     "nnmg_level_set_deterministic": [_handle, c_int],
     "nnmg_halo_pack": [c_int64, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_halo_unpack": [c_int64, c_void_p, c_void_p, c_void_p, c_int, c_void_p],

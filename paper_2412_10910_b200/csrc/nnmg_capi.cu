@@ -263,6 +263,14 @@ int nnmg_coarse_direct_create(nnmg_level_t level, const double* inverse_dev, int
   });
 }
 
+int nnmg_coarse_direct_create_f32(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    NNMG_REQUIRE(out && inverse_dev, kInvalidArgument, "null argument");
+    *out = reinterpret_cast<nnmg_coarse_t>(coarse_direct_create(LV(level), inverse_dev, ld, true));
+  });
+}
+
 int nnmg_coarse_destroy(nnmg_coarse_t coarse) {
   return guard([&] { delete CO(coarse); });
 }
@@ -345,6 +353,13 @@ int nnmg_vcycle_set_precision(nnmg_vcycle_t vcycle, int bits) {
   return guard([&] {
     REQUIRE_HANDLE(vcycle);
     vcycle_set_precision(*VC(vcycle), bits);
+  });
+}
+
+int nnmg_vcycle_set_mixed_coarse(nnmg_vcycle_t vcycle, nnmg_coarse_t coarse) {
+  return guard([&] {
+    REQUIRE_HANDLE(vcycle);
+    vcycle_set_mixed_coarse(*VC(vcycle), CO(coarse));
   });
 }
 

@@ -30,6 +30,8 @@ struct Coarse {
   DevBuf<int> dfree, dcons;      // free DoFs (ascending), constrained DoFs
   int nb = 0;                    // 64-row blocks of free DoFs
   DevBuf<double> tiles;          // [nb(nb+1)/2][64][64], tile (I, J <= I) at I(I+1)/2 + J
+  bool tiles_f32 = false;        // fp32 tiles (the mixed-precision cycle's coarse solve)
+  DevBuf<float> tiles32;
   DevBuf<double> prow, pcol;     // per-tile partial products (rows of I / columns of J)
 };
 
@@ -39,7 +41,7 @@ Coarse* coarse_cg_create(Level* L, double reduction, int max_iter);
 // memory): the inverse of the free-DoF block (free DoFs ascending, the
 // complement of the level's constrained list), read in its lower triangle
 // only and packed into symmetric tiles
-Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld);
+Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bool f32 = false);
 void coarse_direct_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
 void coarse_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
 void coarse_status(Coarse& C, int* iterations, int* converged, int* error);

@@ -36,11 +36,12 @@ __device__ inline void tri_decode(int64_t t, int& I, int& J) {
 
 // full (lower triangle read) -> tiles; the diagonal tiles are symmetrised
 // from the lower triangle, padding is zero
-__global__ void k_pack(const double* __restrict__ full, int64_t n, int64_t ld, double* __restrict__ tiles) {
+template <class TT>
+__global__ void k_pack(const double* __restrict__ full, int64_t n, int64_t ld, TT* __restrict__ tiles) {
   // full: the free-block inverse (n = number of free DoFs)
   int I, J;
   tri_decode(blockIdx.x, I, J);
-  double* dst = tiles + int64_t(blockIdx.x) * kT * kT;
+  TT* dst = tiles + int64_t(blockIdx.x) * kT * kT;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int r = e / kT, c = e % kT;
     int64_t gr = int64_t(I) * kT + r, gc = int64_t(J) * kT + c;
@@ -49,16 +50,33 @@ __global__ void k_pack(const double* __restrict__ full, int64_t n, int64_t ld, d
       gr = gc;
       gc = t;
     }
-    dst[e] = (gr < n && gc < n) ? full[gr * ld + gc] : 0.0;
+    dst[e] = (gr < n && gc < n) ? TT(full[gr * ld + gc]) : TT(0);
   }
 }
 
 // phase 1: thread t holds elements 2(t + 256k), k < 8, of its tile, i.e. rows
 // w + 8k (w = warp) and columns 2 lane, 2 lane + 1
-__global__ void __launch_bounds__(256) k_symv_tiles(const double* __restrict__ tiles, const double* __restrict__ x,
+// TT: tile storage and product type (double; float = the mixed-precision
+// cycle's coarse solve: half the streamed bytes, single-precision products
+// within a tile, per-tile partials and their sums in fp64)
+template <class TT>
+struct Tile2;
+template <>
+struct Tile2<double> {
+  using type = double2;
+};
+template <>
+struct Tile2<float> {
+  using type = float2;
+};
+
+template <class TT>
+__global__ void __launch_bounds__(256) k_symv_tiles(const TT* __restrict__ tiles, const double* __restrict__ x,
                                                     const int* __restrict__ freedofs, int64_t n,
                                                     double* __restrict__ prow, double* __restrict__ pcol) {
-  __shared__ double xs[2][kT];
+  using double2 = typename Tile2<TT>::type;  // element pairs of the tile type
+  using double_t = TT;
+  __shared__ double_t xs[2][kT];
   __shared__ double2 cs[8][kT / 2];
   const int64_t t = blockIdx.x;
   int I, J;
@@ -71,53 +89,53 @@ __global__ void __launch_bounds__(256) k_symv_tiles(const double* __restrict__ t
   if (tid < 2 * kT) {
     const int which = tid / kT, r = tid % kT;
     const int64_t g = int64_t(which ? I : J) * kT + r;
-    xs[which][r] = g < n ? __ldcg(x + freedofs[g]) : 0.0;
+    xs[which][r] = g < n ? double_t(__ldcg(x + freedofs[g])) : double_t(0);
   }
   __syncthreads();
   // row part: y_I[w + 8k] += sum_c A[w + 8k][c] x_J[c]
-  const double xj0 = xs[0][2 * lane], xj1 = xs[0][2 * lane + 1];
-  double rp[8];
+  const double_t xj0 = xs[0][2 * lane], xj1 = xs[0][2 * lane + 1];
+  double_t rp[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) rp[k] = fma(a[k].x, xj0, a[k].y * xj1);
   // transposing butterfly: after it lane L holds row w + 8 k(L),
   // k(L) = 4 b4(L) + 2 b3(L) + b2(L), summed over all 64 columns
   const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-  double r4[4], r2[2];
+  double_t r4[4], r2[2];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const double send = b16 ? rp[j] : rp[4 + j];
-    const double keep = b16 ? rp[4 + j] : rp[j];
+    const double_t send = b16 ? rp[j] : rp[4 + j];
+    const double_t keep = b16 ? rp[4 + j] : rp[j];
     r4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
-    const double send = b8 ? r4[j] : r4[2 + j];
-    const double keep = b8 ? r4[2 + j] : r4[j];
+    const double_t send = b8 ? r4[j] : r4[2 + j];
+    const double_t keep = b8 ? r4[2 + j] : r4[j];
     r2[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
   }
-  double r1 = (b4 ? r2[1] : r2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? r2[0] : r2[1], 4);
+  double_t r1 = (b4 ? r2[1] : r2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? r2[0] : r2[1], 4);
   r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
   r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
   if ((lane & 3) == 0) {
     const int k = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
-    prow[t * kT + w + 8 * k] = r1;
+    prow[t * kT + w + 8 * k] = double(r1);
   }
   if (I == J) return;  // diagonal tiles are stored whole: no column part
   // column part: y_J[c] += sum_r A[r][c] x_I[r]
-  double c0 = 0.0, c1 = 0.0;
+  double_t c0 = 0, c1 = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const double xi = xs[1][w + 8 * k];
+    const double_t xi = xs[1][w + 8 * k];
     c0 = fma(a[k].x, xi, c0);
     c1 = fma(a[k].y, xi, c1);
   }
-  cs[w][lane] = make_double2(c0, c1);
+  cs[w][lane] = double2{c0, c1};
   __syncthreads();
   if (tid < kT) {
-    const double* csd = reinterpret_cast<const double*>(&cs[0][0]);
+    const double_t* csd = reinterpret_cast<const double_t*>(&cs[0][0]);
     double s = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) s += csd[q * kT + tid];
+    for (int q = 0; q < 8; ++q) s += double(csd[q * kT + tid]);
     pcol[t * kT + tid] = s;
   }
 }
@@ -153,7 +171,7 @@ __global__ void __launch_bounds__(256) k_symv_reduce(const double* __restrict__ 
 
 }  // namespace
 
-Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld) {
+Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bool f32) {
   NNMG_REQUIRE(L != nullptr && inverse_dev != nullptr, kInvalidArgument, "null argument");
   NNMG_CUDA_TRY(cudaSetDevice(L->device));
   // free DoFs: the complement of the level's sorted constrained list
@@ -180,12 +198,21 @@ Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld) {
     C->nb = static_cast<int>((nf + kT - 1) / kT);
     const int64_t nt = tri_id(C->nb, 0);
     NNMG_REQUIRE(nt < (int64_t(1) << 31), kInvalidArgument, "coarse level too large for the direct solve");
-    C->tiles.alloc(size_t(nt) * kT * kT);
+    C->tiles_f32 = f32;
+    if (f32)
+      C->tiles32.alloc(size_t(nt) * kT * kT);
+    else
+      C->tiles.alloc(size_t(nt) * kT * kT);
     C->prow.alloc(size_t(nt) * kT);
     C->pcol.alloc(size_t(nt) * kT);
     C->status.alloc(3);
     C->status.zero();
-    if (nt) k_pack<<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles.ptr);
+    if (nt) {
+      if (f32)
+        k_pack<float><<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles32.ptr);
+      else
+        k_pack<double><<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles.ptr);
+    }
     NNMG_CHECK_LAUNCH();
     NNMG_CUDA_TRY(cudaDeviceSynchronize());
   } catch (...) {
@@ -199,7 +226,10 @@ void coarse_direct_solve(Coarse& C, const double* b, double* x, cudaStream_t s) 
   const int64_t nt = tri_id(C.nb, 0);
   const int64_t ncons = static_cast<int64_t>(C.dcons.n);
   if (nt) {
-    k_symv_tiles<<<unsigned(nt), 256, 0, s>>>(C.tiles.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr);
+    if (C.tiles_f32)
+      k_symv_tiles<float><<<unsigned(nt), 256, 0, s>>>(C.tiles32.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr);
+    else
+      k_symv_tiles<double><<<unsigned(nt), 256, 0, s>>>(C.tiles.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr);
     NNMG_CHECK_LAUNCH();
   }
   const unsigned extra = static_cast<unsigned>(std::min<int64_t>((ncons + 255) / 256, 64));

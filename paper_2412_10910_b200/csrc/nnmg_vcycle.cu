@@ -167,7 +167,7 @@ static void cycle32(VCycle& V, int l, const float* f, float* x, cudaStream_t s) 
   if (l == 0) {
     const int64_t n0 = V.levels[0]->n_dofs;
     convert(n0, f, V.cf.ptr, s);
-    coarse_solve(*V.coarse, V.cf.ptr, V.cx.ptr, s);
+    coarse_solve(V.coarse32 ? *V.coarse32 : *V.coarse, V.cf.ptr, V.cx.ptr, s);
     convert(n0, V.cx.ptr, x, s);
     return;
   }
@@ -206,6 +206,15 @@ static void run_cycle(VCycle& V, const double* f, double* x, cudaStream_t s) {
   convert(n, f, V.f32[top].ptr, s);
   cycle32(V, top, V.f32[top].ptr, V.x32[top].ptr, s);
   convert(n, V.x32[top].ptr, x, s);
+}
+
+void vcycle_set_mixed_coarse(VCycle& V, Coarse* coarse) {
+  NNMG_REQUIRE(coarse == nullptr || coarse->level == V.levels[0], kInvalidArgument,
+               "coarse solver belongs to another level");
+  if (coarse == V.coarse32) return;
+  for (auto& g : V.graphs) cudaGraphExecDestroy(g.exec);
+  V.graphs.clear();
+  V.coarse32 = coarse;
 }
 
 void vcycle_set_precision(VCycle& V, int bits) {

@@ -20,6 +20,7 @@ struct VCycle {
   std::vector<Level*> levels;        // coarsest first
   std::vector<Transfer*> transfers;  // transfers[l-1] connects l-1 -> l
   Coarse* coarse = nullptr;
+  Coarse* coarse32 = nullptr;  // optional coarse solver of the mixed-precision cycle (fp32 inverse tiles)
   std::vector<double> lam_max, lam_min;
   std::vector<int> degree;
   int m1 = 1, m2 = 1;
@@ -53,6 +54,8 @@ void vcycle_run(VCycle& V, const double* f, double* x, cudaStream_t s);
 // of vectors / geometry / transfer records on levels >= 1, fp64 arithmetic,
 // fp64 coarse solve); input and output stay fp64
 void vcycle_set_precision(VCycle& V, int bits);
+// coarse solver used by the mixed-precision cycle instead of V.coarse (nullptr: the same); drops captured graphs
+void vcycle_set_mixed_coarse(VCycle& V, Coarse* coarse);
 int64_t vcycle_kernels(VCycle& V);
 
 }  // namespace nnmg

@@ -157,19 +157,33 @@ class MultigridHierarchy:
             self._vc = h
             self._vc_keep = (lv, tr, lmax, lmin, deg)
             if self.precision != 64:
+                self._attach_mixed_coarse()
                 _lib.call("nnmg_vcycle_set_precision", h, int(self.precision))
         return self._vc
+
+    def _attach_mixed_coarse(self):
+        """The mixed-precision cycle's coarse solve: the packed inverse in fp32
+        tiles where the coarse solver offers it (half the bytes of the fp64
+        direct solve; on C3 faster than the coarse CG the fp64 cycle keeps)."""
+        make = getattr(self.coarse_solver, "mixed_handle", None)
+        h32 = make() if make is not None else None
+        if h32 is not None and self._vc is not None:
+            _lib.call("nnmg_vcycle_set_mixed_coarse", self._vc, h32)
 
     def set_precision(self, bits):
         """64: the fp64 V-cycle (default).  32: the paper's mixed-precision
         cycle: fp32 storage of level vectors, geometry,
         inverse diagonals and transfer coordinates above the coarsest level,
-        fp64 arithmetic and coarse solve; the cycle's input and output (and
-        the outer CG) stay fp64.  Native executor only."""
+        single-precision arithmetic in the register applies and the transfers
+        (NNMG_MIXED_ARITH=64: fp64 arithmetic on the fp32 storage), fp64
+        coarse vectors; the cycle's input and output (and the outer CG) stay
+        fp64.  Native executor only."""
         if bits not in (32, 64):
             raise ValueError("precision must be 32 or 64")
         self.precision = int(bits)
         if self._vc is not None:
+            if bits == 32:
+                self._attach_mixed_coarse()
             _lib.call("nnmg_vcycle_set_precision", self._vc, int(bits))
 
     def use_graph(self, enable=True):

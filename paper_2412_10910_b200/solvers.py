@@ -271,6 +271,10 @@ class CoarseSolver:
         self.cg_max_iter = cg_max_iter
         self.dense = op.n_dofs <= dense_limit
         self.direct = False
+        self._direct_mode = direct   # False: the reference's CG only (parity mode)
+        self._h32 = None             # fp32-tile direct solve of the mixed-precision cycle (mixed_handle)
+        self._h32_tried = False
+        self.timing = None
         self.choice = "dense" if self.dense else "cg"
         h = ctypes.c_void_p()
         if self.dense:
@@ -331,7 +335,30 @@ class CoarseSolver:
         e1.synchronize()
         return e0.elapsed_time(e1) * 1e-3
 
-    def _make_direct(self):
+    def mixed_handle(self):
+        """Coarse solver handle for the mixed-precision cycle, or None to share
+        the fp64 one: the exact inverse packed in fp32 tiles
+        (nnmg_coarse_direct_create_f32), half the bytes of the fp64 direct
+        solve.  Built on first use where the direct path is allowed
+        (direct=True / "auto") and predicted faster than the active solver."""
+        if self.dense or not self._direct_mode:
+            return None
+        if self._h32 is None and not self._h32_tried:
+            self._h32_tried = True
+            nf = self.op.n_dofs - len(self.op.constraints.dofs)
+            t32 = 0.5 * direct_solve_bytes(nf) / DIRECT_STREAM_BYTES_PER_S
+            if self.direct:
+                t_now = direct_solve_bytes(nf) / DIRECT_STREAM_BYTES_PER_S
+            else:
+                t_now = (self.timing or {}).get("cg_s") or self._time_cg()
+            mem = torch.cuda.mem_get_info(self.device)[0]
+            fits = 3 * 8 * nf ** 2 + direct_solve_bytes(nf) // 2 < 0.8 * mem
+            if self._direct_mode is True or (fits and t32 < 0.9 * t_now):
+                self._h32 = self._make_direct(f32=True)
+                self.timing = dict(self.timing or {}, mixed_direct_predicted_s=t32)
+        return self._h32
+
+    def _make_direct(self, f32=False):
         n = self.op.n_dofs
         cons = np.asarray(self.op.constraints.dofs, dtype=np.int64)
         if len(cons) == 0:
@@ -360,19 +387,23 @@ class CoarseSolver:
         inv = torch.cholesky_inverse(Lc)
         del Lc
         h = ctypes.c_void_p()
-        _lib.call("nnmg_coarse_direct_create", self.op.handle, inv.data_ptr(), len(free), ctypes.byref(h))
+        _lib.call("nnmg_coarse_direct_create_f32" if f32 else "nnmg_coarse_direct_create", self.op.handle,
+                  inv.data_ptr(), len(free), ctypes.byref(h))
         torch.cuda.synchronize(self.device)
         del inv
+        if f32:
+            return h
         _lib.load().nnmg_coarse_destroy(self._h)
         self._h = h
         self.direct = True
         self.choice = "direct"
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None and _lib._lib is not None:  # not at interpreter exit
-            _lib.load().nnmg_coarse_destroy(h)
-            self._h = None
+        for name in ("_h", "_h32"):
+            h = getattr(self, name, None)
+            if h is not None and h.value and _lib is not None and _lib._lib is not None:  # not at interpreter exit
+                _lib.load().nnmg_coarse_destroy(h)
+                setattr(self, name, None)
 
     @property
     def handle(self):

@@ -105,3 +105,32 @@ def test_hierarchy_with_direct_coarse_converges_like_cg(pkg):
         z2 = H.v_cycle(b, executor=False)
         assert rel(z1.cpu().numpy(), z2.cpu().numpy()) <= 1e-12
     assert abs(its[True] - its[False]) <= 1
+
+
+def test_mixed_cycle_uses_fp32_tile_coarse_solve(pkg):
+    """The mixed-precision cycle attaches the packed inverse in fp32 tiles
+    (nnmg_coarse_direct_create_f32) where the direct path is allowed: same
+    outer iterations as the fp64 cycle, cycle within single-precision rounding
+    of the fp64 one; the parity mode (coarse_direct=False) keeps one solver."""
+    from paper_2412_10910_b200 import configs, multigrid, solvers
+
+    cfg = configs.get_config("C2")
+    meshes = cfg.make_meshes(scale=2, validate=False)
+    H = multigrid.build_hp_hierarchy(meshes, cfg.degree, config=multigrid.HierarchyConfig(
+        chebyshev_degree=4, coarse_direct=True))
+    b = H.finest.operator.load_vector(1.0)
+    z64 = H.v_cycle(b).cpu().numpy()
+    r64 = solvers.cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
+    H.set_precision(32)
+    assert H.coarse_solver._h32 is not None
+    assert H.coarse_solver.info().get("mixed_direct_predicted_s", 0) > 0
+    z32 = H.v_cycle(b).cpu().numpy()
+    assert 0 < rel(z32, z64) <= 2e-4
+    r32 = solvers.cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
+    assert r32.converged and abs(r32.iterations - r64.iterations) <= 1
+    H.set_precision(64)
+    assert rel(H.v_cycle(b).cpu().numpy(), z64) <= 1e-14  # the fp64 cycle keeps its own solver
+    Hp = multigrid.build_hp_hierarchy(meshes, cfg.degree, config=multigrid.HierarchyConfig(
+        chebyshev_degree=4, coarse_direct=False, vcycle_precision=32))
+    Hp.v_cycle(b)
+    assert Hp.coarse_solver._h32 is None and not Hp.coarse_solver.direct
