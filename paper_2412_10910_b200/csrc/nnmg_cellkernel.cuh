@@ -51,7 +51,21 @@ __device__ unsigned long long nnmg_cell_trace[16];
 // SCB_ > 0: one thread group handles a sub-block of SCB_ of the CB cells of a
 // block (lanes lane_off .. lane_off+SCB_-1), so a block can be spread over
 // several CTAs (latency-bound coarse levels); the HBM layout keeps CB.
-template <int DIM, int P, int NCOMP, int PHYS, int SCB_ = 0>
+// reciprocal in the arithmetic type
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+
+// stored-geometry physics exists in fp64 only; the single-precision cell
+// kernel recomputes its geometry (GEO 2) and never reaches this call
+template <int DIM, int NCOMP, int PHYS, int CB, bool kStream, class TA>
+__device__ __forceinline__ void qp_flux_any(const double* __restrict__ geo, const TA (&g)[NCOMP][DIM],
+                                            TA (&f)[NCOMP][DIM], double lam, double mu) {
+  if constexpr (sizeof(TA) == sizeof(double)) qp_flux<DIM, NCOMP, PHYS, CB, kStream>(geo, g, f, lam, mu);
+}
+
+// TA: the arithmetic and shared-memory type (double; float = the single-
+// precision arithmetic of the mixed-precision V-cycle, GEO 2 only)
+template <int DIM, int P, int NCOMP, int PHYS, int SCB_ = 0, class TA = double>
 struct CellKernel {
   static constexpr int N1 = P + 1;
   static constexpr int NLOC = ipow(N1, DIM);
@@ -61,7 +75,7 @@ struct CellKernel {
   static constexpr int NG = GeoCount<DIM, PHYS>::value;
   static constexpr int NTHREADS = NPEN * SCB;
   static constexpr int NBUF = 3;
-  static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * SCB * sizeof(double);
+  static constexpr size_t SMEM = size_t(NBUF) * NCOMP * NLOC * SCB * sizeof(TA);
   // geometry modes (template GEO of run / run_values):
   //   0  stored G / J^-1 streamed from HBM (L2 bulk prefetch)
   //   1  stored, the sub-block's rows staged in shared memory (LDGSTS) behind SMEM
@@ -73,12 +87,12 @@ struct CellKernel {
   static constexpr size_t EDGE_SMEM = size_t(NE) * SCB * sizeof(double);
   using PL = Pencil<DIM, N1>;
 
-  __device__ __forceinline__ static double& S(double* sm, int b, int c, int pos, int lane) {
+  __device__ __forceinline__ static TA& S(TA* sm, int b, int c, int pos, int lane) {
     return sm[((b * NCOMP + c) * NLOC + pos) * SCB + lane];
   }
 
   template <int K>
-  __device__ __forceinline__ static void load(double* sm, int b, int pen, int lane, double (&v)[NCOMP][N1]) {
+  __device__ __forceinline__ static void load(TA* sm, int b, int pen, int lane, TA (&v)[NCOMP][N1]) {
     const int base = PL::base(K, pen);
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c)
@@ -86,17 +100,17 @@ struct CellKernel {
       for (int i = 0; i < N1; ++i) v[c][i] = S(sm, b, c, base + i * PL::stride(K), lane);
   }
   template <int K>
-  __device__ __forceinline__ static void store(double* sm, int b, int pen, int lane, const double (&v)[NCOMP][N1]) {
+  __device__ __forceinline__ static void store(TA* sm, int b, int pen, int lane, const TA (&v)[NCOMP][N1]) {
     const int base = PL::base(K, pen);
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
       for (int i = 0; i < N1; ++i) S(sm, b, c, base + i * PL::stride(K), lane) = v[c][i];
   }
-  __device__ __forceinline__ static void op(const double (&M)[kMaxN1][kMaxN1], double (&v)[NCOMP][N1], bool trans) {
+  __device__ __forceinline__ static void op(const TA (&M)[kMaxN1][kMaxN1], TA (&v)[NCOMP][N1], bool trans) {
 #pragma unroll
     for (int c = 0; c < NCOMP; ++c) {
-      double t[N1];
+      TA t[N1];
       if (trans)
         sweep_t<N1>(M, v[c], t);
       else
@@ -135,15 +149,16 @@ struct CellKernel {
   template <bool kRes = false, bool kNeg = false, int GEO = 0, class Src, class Sync, class TD>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, TD* __restrict__ dst,
                                                const int* __restrict__ idx, const double* __restrict__ geo,
-                                               int64_t blk, double lam, double mu, double* sm, int tid,
+                                               int64_t blk, double lam, double mu, TA* sm, int tid,
                                                Sync&& sync, int lane_off = 0, double* __restrict__ cellout = nullptr) {
+    static_assert(sizeof(TA) == sizeof(double) || GEO == 2, "single-precision arithmetic: recomputed geometry only");
     // the block's geometry chunk (85% of the bytes) is consumed only in phase
     // 5: start streaming it into L2 now so it overlaps gathers and sweeps
     constexpr unsigned kGeoBytes = unsigned(NLOC) * NG * CB * sizeof(double);
     if constexpr (GEO == 2) {
       static_assert(!kRes && DIM == 3 && PHYS == kLaplace, "edge recompute: 3D Laplace apply");
       // asynchronous (LDGSTS) so the gathers below are issued right behind it
-      double* es = sm + SMEM / sizeof(double);
+      double* es = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + SMEM);
       const double* esrc = edges_of(geo) + blk * (int64_t)NE * CB + lane_off;
       if constexpr ((SCB * sizeof(double)) % 16 == 0) {
         constexpr int CH = SCB * sizeof(double) / 16;
@@ -158,7 +173,7 @@ struct CellKernel {
       // [q][k] row) into shared memory asynchronously (LDGSTS, L2 only); it
       // lands while the gathers and sweeps run and is waited for before P5
       static_assert(!kRes && (SCB * sizeof(double)) % 16 == 0, "16-byte chunks");
-      double* gs = sm + SMEM / sizeof(double);
+      double* gs = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + SMEM);
       constexpr int CH = SCB * sizeof(double) / 16;
       constexpr int TOT = NLOC * NG * CH;
       const double* gsrc = geo + blk * (int64_t)NLOC * NG * CB + lane_off;
@@ -172,11 +187,11 @@ struct CellKernel {
     }
     int gi[N1];
     pencil_dofs<kRes>(idx, blk, tid, lane_off, gi);
-    double v[NCOMP][N1];
+    TA v[NCOMP][N1];
 #pragma unroll
     for (int i = 0; i < N1; ++i)
 #pragma unroll
-      for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? src((int64_t)gi[i] * NCOMP + c) : 0.0;
+      for (int c = 0; c < NCOMP; ++c) v[c][i] = gi[i] >= 0 ? TA(src((int64_t)gi[i] * NCOMP + c)) : TA(0);
     return run_values<kRes, kNeg, GEO>(tab, gi, v, dst, geo, blk, lam, mu, sm, tid, sync, lane_off, cellout);
   }
 
@@ -184,10 +199,12 @@ struct CellKernel {
   // callers that can issue the gather early (the coarse CG) enter here
   template <bool kRes = false, bool kNeg = false, int GEO = 0, class Sync, class TD>
   __device__ __forceinline__ static double run_values(const Tables& tab, const int (&gi)[N1],
-                                                      double (&v)[NCOMP][N1], TD* __restrict__ dst,
+                                                      TA (&v)[NCOMP][N1], TD* __restrict__ dst,
                                                       const double* __restrict__ geo, int64_t blk, double lam,
-                                                      double mu, double* sm, int tid, Sync&& sync, int lane_off = 0,
+                                                      double mu, TA* sm, int tid, Sync&& sync, int lane_off = 0,
                                                       double* __restrict__ cellout = nullptr) {
+    const auto& tS = TabSel<TA>::S(tab);
+    const auto& tDc = TabSel<TA>::Dc(tab);
     // lsub indexes shared memory (stride SCB); glane indexes the tables:
     // HBM layout (stride CB) or a resident shared copy of the sub-block (SCB)
     NNMG_CT_BEGIN;
@@ -196,14 +213,14 @@ struct CellKernel {
     constexpr int GS = kRes ? SCB : CB;
     const int glane = kRes ? lsub : lane_off + lsub;
     constexpr int A = 0, GX = 1, GY = 2;
-    double u0[NCOMP][N1];
+    TA u0[NCOMP][N1];
     // P1: interpolate the x-pencil along x
     {
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
         for (int i = 0; i < N1; ++i) u0[c][i] = v[c][i];
-      op(tab.S, v, false);
+      op(tS, v, false);
       store<0>(sm, A, pen, lsub, v);
     }
     sync();
@@ -211,30 +228,30 @@ struct CellKernel {
     if constexpr (DIM == 3) {
       // P2: interpolate along y
       load<1>(sm, A, pen, lsub, v);
-      op(tab.S, v, false);
+      op(tS, v, false);
       store<1>(sm, A, pen, lsub, v);
       sync();
       NNMG_CT(2);
     }
     // P3: interpolate along the last axis -> values at quadrature points
     constexpr int KL = DIM - 1;
-    double gl[NCOMP][N1];
+    TA gl[NCOMP][N1];
     load<KL>(sm, A, pen, lsub, v);
-    op(tab.S, v, false);
+    op(tS, v, false);
 #pragma unroll
-    for (int c = 0; c < NCOMP; ++c) sweep<N1>(tab.Dc, v[c], gl[c]);
+    for (int c = 0; c < NCOMP; ++c) sweep<N1>(tDc, v[c], gl[c]);
     store<KL>(sm, A, pen, lsub, v);
     sync();
     NNMG_CT(3);
     // P4: collocation derivatives along x (and y in 3D)
     {
-      double w[NCOMP][N1];
+      TA w[NCOMP][N1];
       load<0>(sm, A, pen, lsub, w);
-      op(tab.Dc, w, false);
+      op(tDc, w, false);
       store<0>(sm, GX, pen, lsub, w);
       if constexpr (DIM == 3) {
         load<1>(sm, A, pen, lsub, w);
-        op(tab.Dc, w, false);
+        op(tDc, w, false);
         store<1>(sm, GY, pen, lsub, w);
       }
     }
@@ -244,21 +261,21 @@ struct CellKernel {
     // P5: quadrature-point physics on the last-axis pencil
     {
       const int base = PL::base(KL, pen);
-      double fl[NCOMP][N1];
-      double fx[NCOMP][N1], fy[NCOMP][N1];
+      TA fl[NCOMP][N1];
+      TA fx[NCOMP][N1], fy[NCOMP][N1];
       // GEO 2: the z-pencil (qx, qy) = (pen % N1, pen / N1) of the trilinear
       // map: dx/dz is constant along it, dx/dx and dx/dy are affine in z
-      double A0[3], B0[3], A1[3], B1[3], J2[3], wxy = 0.0;
+      TA A0[3], B0[3], A1[3], B1[3], J2[3], wxy = 0;
       if constexpr (GEO == 2) {
-        const double* E = sm + SMEM / sizeof(double) + lsub;
-        auto e = [&](int b, int k, int a) { return E[((b * 4 + k) * 3 + a) * SCB]; };
+        const double* E = reinterpret_cast<const double*>(reinterpret_cast<const char*>(sm) + SMEM) + lsub;
+        auto e = [&](int b, int k, int a) { return TA(E[((b * 4 + k) * 3 + a) * SCB]); };
         const int qx = pen % N1, qy = pen / N1;
-        const double x = tab.xq[qx], y = tab.xq[qy];
-        wxy = tab.w[qx] * tab.w[qy];
+        const TA x = TA(tab.xq[qx]), y = TA(tab.xq[qy]);
+        wxy = TA(tab.w[qx] * tab.w[qy]);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           // edges along b, k = (lower other axis) + 2 (higher other axis)
-          J2[a] = (1.0 - y) * fma(x, e(2, 1, a) - e(2, 0, a), e(2, 0, a)) + y * fma(x, e(2, 3, a) - e(2, 2, a), e(2, 2, a));
+          J2[a] = (TA(1) - y) * fma(x, e(2, 1, a) - e(2, 0, a), e(2, 0, a)) + y * fma(x, e(2, 3, a) - e(2, 2, a), e(2, 2, a));
           A0[a] = fma(y, e(0, 1, a) - e(0, 0, a), e(0, 0, a));
           B0[a] = fma(y, e(0, 3, a) - e(0, 2, a), e(0, 2, a)) - A0[a];
           A1[a] = fma(x, e(1, 1, a) - e(1, 0, a), e(1, 0, a));
@@ -268,7 +285,7 @@ struct CellKernel {
 #pragma unroll
       for (int q = 0; q < N1; ++q) {
         const int pos = base + q * PL::stride(KL);
-        double g[NCOMP][DIM], f[NCOMP][DIM];
+        TA g[NCOMP][DIM], f[NCOMP][DIM];
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           g[c][0] = S(sm, GX, c, pos, lsub);
@@ -277,15 +294,15 @@ struct CellKernel {
         }
         if constexpr (GEO == 2) {
           // J = [A0 + z B0 | A1 + z B1 | J2]; G g = (w / det) C^T (C g), C = cofactors
-          const double z = tab.xq[q];
-          double J[3][3];
+          const TA z = TA(tab.xq[q]);
+          TA J[3][3];
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             J[a][0] = fma(z, B0[a], A0[a]);
             J[a][1] = fma(z, B1[a], A1[a]);
             J[a][2] = J2[a];
           }
-          double C[3][3];
+          TA C[3][3];
           C[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
           C[0][1] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
           C[0][2] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
@@ -295,17 +312,17 @@ struct CellKernel {
           C[2][0] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
           C[2][1] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
           C[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-          const double det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
-          const double sc = wxy * tab.w[q] * __drcp_rn(det);
-          double h[3];
+          const TA det = J[0][0] * C[0][0] + J[0][1] * C[0][1] + J[0][2] * C[0][2];
+          const TA sc = wxy * TA(tab.w[q]) * rcp_rn(det);
+          TA h[3];
 #pragma unroll
           for (int i = 0; i < 3; ++i) h[i] = sc * (C[i][0] * g[0][0] + C[i][1] * g[0][1] + C[i][2] * g[0][2]);
 #pragma unroll
           for (int a = 0; a < 3; ++a) f[0][a] = C[0][a] * h[0] + C[1][a] * h[1] + C[2][a] * h[2];
         } else if constexpr (GEO == 1)
-          qp_flux<DIM, NCOMP, PHYS, SCB, false>(sm + SMEM / sizeof(double) + pos * NG * SCB + lsub, g, f, lam, mu);
+          qp_flux_any<DIM, NCOMP, PHYS, SCB, false>(reinterpret_cast<const double*>(reinterpret_cast<const char*>(sm) + SMEM) + pos * NG * SCB + lsub, g, f, lam, mu);
         else
-          qp_flux<DIM, NCOMP, PHYS, GS, !kRes>(geo + ((blk * (int64_t)NLOC + pos) * NG) * GS + glane, g, f, lam, mu);
+          qp_flux_any<DIM, NCOMP, PHYS, GS, !kRes>(geo + ((blk * (int64_t)NLOC + pos) * NG) * GS + glane, g, f, lam, mu);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c) {
           fx[c][q] = f[c][0];
@@ -316,8 +333,8 @@ struct CellKernel {
       // last-axis derivative transpose stays in registers
 #pragma unroll
       for (int c = 0; c < NCOMP; ++c) {
-        double t[N1];
-        sweep_t<N1>(tab.Dc, fl[c], t);
+        TA t[N1];
+        sweep_t<N1>(tDc, fl[c], t);
 #pragma unroll
         for (int i = 0; i < N1; ++i) fl[c][i] = t[i];
       }
@@ -338,9 +355,9 @@ struct CellKernel {
     if constexpr (DIM == 3) {
       // P6: A += Dc^T fx along x
       {
-        double w[NCOMP][N1], a[NCOMP][N1];
+        TA w[NCOMP][N1], a[NCOMP][N1];
         load<0>(sm, GX, pen, lsub, w);
-        op(tab.Dc, w, true);
+        op(tDc, w, true);
         load<0>(sm, A, pen, lsub, a);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c)
@@ -352,44 +369,44 @@ struct CellKernel {
       NNMG_CT(6);
       // P7: w = A + Dc^T fy along y, then S^T along y
       {
-        double w[NCOMP][N1], a[NCOMP][N1];
+        TA w[NCOMP][N1], a[NCOMP][N1];
         load<1>(sm, GY, pen, lsub, w);
-        op(tab.Dc, w, true);
+        op(tDc, w, true);
         load<1>(sm, A, pen, lsub, a);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
           for (int i = 0; i < N1; ++i) a[c][i] += w[c][i];
-        op(tab.S, a, true);
+        op(tS, a, true);
         store<1>(sm, A, pen, lsub, a);
       }
       sync();
       NNMG_CT(7);
       // P8: S^T along z
       load<2>(sm, A, pen, lsub, v);
-      op(tab.S, v, true);
+      op(tS, v, true);
       store<2>(sm, A, pen, lsub, v);
       sync();
       NNMG_CT(8);
     } else {
       // 2D P6: A = Dc^T fx along x
       {
-        double w[NCOMP][N1];
+        TA w[NCOMP][N1];
         load<0>(sm, GX, pen, lsub, w);
-        op(tab.Dc, w, true);
+        op(tDc, w, true);
         store<0>(sm, A, pen, lsub, w);
       }
       sync();
       NNMG_CT(9);
       // 2D P7: w = A + (y part in registers), S^T along y
       {
-        double a[NCOMP][N1];
+        TA a[NCOMP][N1];
         load<1>(sm, A, pen, lsub, a);
 #pragma unroll
         for (int c = 0; c < NCOMP; ++c)
 #pragma unroll
           for (int i = 0; i < N1; ++i) a[c][i] += v[c][i];
-        op(tab.S, a, true);
+        op(tS, a, true);
         store<1>(sm, A, pen, lsub, a);
       }
       sync();
@@ -397,7 +414,7 @@ struct CellKernel {
     }
     // final: S^T along x and scatter-add the x-pencil
     load<0>(sm, A, pen, lsub, v);
-    op(tab.S, v, true);
+    op(tS, v, true);
     double energy = 0.0;
 #pragma unroll
     for (int i = 0; i < N1; ++i) {
@@ -408,7 +425,7 @@ struct CellKernel {
             cellout[((blk * NLOC + PL::base(0, pen) + i) * NCOMP + c) * CB + glane] = v[c][i];
           else
             atomicAdd(dst + (int64_t)gi[i] * NCOMP + c, TD(kNeg ? -v[c][i] : v[c][i]));
-          energy = fma(u0[c][i], v[c][i], energy);
+          energy = fma(double(u0[c][i]), double(v[c][i]), energy);
         }
       }
     }

@@ -114,11 +114,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // out[q] = sum_i M[q][i] in[i]
-template <int N1>
-__device__ __forceinline__ void sweep(const double (&M)[kMaxN1][kMaxN1], const double* in, double* out) {
+template <int N1, class TA>
+__device__ __forceinline__ void sweep(const TA (&M)[kMaxN1][kMaxN1], const TA* in, TA* out) {
 #pragma unroll
   for (int q = 0; q < N1; ++q) {
-    double s = 0.0;
+    TA s = 0;
 #pragma unroll
     for (int i = 0; i < N1; ++i) s = fma(M[q][i], in[i], s);
     out[q] = s;
@@ -126,11 +126,11 @@ __device__ __forceinline__ void sweep(const double (&M)[kMaxN1][kMaxN1], const d
 }
 
 // out[i] = sum_q M[q][i] in[q]
-template <int N1>
-__device__ __forceinline__ void sweep_t(const double (&M)[kMaxN1][kMaxN1], const double* in, double* out) {
+template <int N1, class TA>
+__device__ __forceinline__ void sweep_t(const TA (&M)[kMaxN1][kMaxN1], const TA* in, TA* out) {
 #pragma unroll
   for (int i = 0; i < N1; ++i) {
-    double s = 0.0;
+    TA s = 0;
 #pragma unroll
     for (int q = 0; q < N1; ++q) s = fma(M[q][i], in[q], s);
     out[i] = s;

@@ -98,8 +98,8 @@ __global__ void k_edges(const double* __restrict__ verts, const int* __restrict_
 
 // SPLIT CTAs per cell block (SCB = CB / SPLIT cells each): smaller CTAs get
 // a larger register budget per thread (the Q4 kernel spills at CB = 32)
-template <int DIM, int P, int NCOMP, int PHYS, int SPLIT>
-using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PHYS>::CB / SPLIT>;
+template <int DIM, int P, int NCOMP, int PHYS, int SPLIT, class TA = double>
+using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PHYS>::CB / SPLIT, TA>;
 
 // min resident CTAs per SM for the split variants (measured on B200: 5 gives
 // C5 0.310 -> 0.279 ms, C4 0.643 -> 0.639 ms)
@@ -110,14 +110,16 @@ using ApplyKernel = CellKernel<DIM, P, NCOMP, PHYS, CellKernel<DIM, P, NCOMP, PH
 #ifndef NNMG_APPLY_MINB_GEOS
 #define NNMG_APPLY_MINB_GEOS 3
 #endif
-template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, int GEO = 0, int MINB = 0, class TV = double>
+template <int DIM, int P, int NCOMP, int PHYS, bool NEG, int SPLIT, int GEO = 0, int MINB = 0, class TV = double,
+          class TA = double>
 __global__ void __launch_bounds__(ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>::NTHREADS,
                                   MINB > 0 ? MINB
                                            : (SPLIT == 1 ? 1 : (GEO == 1 ? NNMG_APPLY_MINB_GEOS : NNMG_APPLY_MINB)))
     k_apply(Tables tab, const TV* __restrict__ src, TV* __restrict__ dst, const int* __restrict__ idx,
             const double* __restrict__ geo, int64_t b0, double lam, double mu, double* __restrict__ cellout) {
-  extern __shared__ double sm[];
-  using CK = ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT>;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  TA* sm = reinterpret_cast<TA*>(sm_raw);
+  using CK = ApplyKernel<DIM, P, NCOMP, PHYS, SPLIT, TA>;
   CK::template run<false, NEG, GEO>(tab, PlainSrcT<TV>{src}, dst, idx, geo, b0 + blockIdx.x / SPLIT, lam, mu, sm,
                                      threadIdx.x, [] __device__() { __syncthreads(); },
                                      int(blockIdx.x % SPLIT) * CK::SCB, cellout);
@@ -739,7 +741,11 @@ struct ApplyLaunchT {
       // fp32 vectors: one compile-time variant per element type, the default
       // split (recomputed G for 3D Laplace Q3/Q4)
       if constexpr (D == 3 && P >= 3 && PH == kLaplace) {
-        if (L.edges.ptr && L.apply_recompute) return launch<D, P, NC, PH, 8, 2>();
+        if (L.edges.ptr && L.apply_recompute) {
+          // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
+          if (L.mixed_arith32) return launch<D, P, NC, PH, 8, 2, 0, float>();
+          return launch<D, P, NC, PH, 8, 2>();
+        }
       }
       constexpr int SP = (D == 3 && P >= 4) ? 4 : (NC > 1 ? 2 : 1);
       launch<D, P, NC, PH, SP>();
@@ -763,14 +769,14 @@ struct ApplyLaunchT {
     launch<D, P, NC, PH, 1>();
     }
   }
-  template <int D, int P, int NC, int PH, int SPLIT, int GEO = 0, int MINB = 0>
+  template <int D, int P, int NC, int PH, int SPLIT, int GEO = 0, int MINB = 0, class TA = double>
   void launch() {
-    using CK = ApplyKernel<D, P, NC, PH, SPLIT>;
+    using CK = ApplyKernel<D, P, NC, PH, SPLIT, TA>;
     constexpr size_t kSmem = CK::SMEM + (GEO == 1 ? CK::GEO_SMEM : (GEO == 2 ? CK::EDGE_SMEM : 0));
     // fp32 vectors: residual form only (no NEG=false instantiation)
-    auto kneg = k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB, TV>;
+    auto kneg = k_apply<D, P, NC, PH, true, SPLIT, GEO, MINB, TV, TA>;
     auto kpos = kneg;
-    if constexpr (kF64) kpos = k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB, TV>;
+    if constexpr (kF64) kpos = k_apply<D, P, NC, PH, false, SPLIT, GEO, MINB, TV, TA>;
     auto kern = neg ? kneg : kpos;
     const double* gsrc = GEO == 2 ? L.edges.ptr : L.geo.ptr;
     static bool attr = false;

@@ -2,7 +2,7 @@
 # mixed-precision cycle with the fp32-tile coarse solve: tests + bench
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_mixed.py tests/test_gpu_coarse_direct.py -q -x > gpurun_out/r2_g20_tests.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_mixed.py tests/test_gpu_coarse_direct.py tests/test_gpu_variants.py tests/test_gpu_parity.py -q -x > gpurun_out/r2_g20_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/r2_g20_tests.log
 tail -4 gpurun_out/r2_g20_tests.log
 for c in "$@"; do
