@@ -656,8 +656,11 @@ def run_ours(args, cfg):
         mixed = {"value": world * n * args.steps / t32 / 1e9, "unit": "GDoF/s",
                  "ms_per_step": t32 / args.steps * 1e3, "solve_iterations": res32.iterations,
                  "solve_converged": res32.converged, "reference_iterations": reference_pin(cfg.name, "iterations"),
-                 "storage": "fp32 level vectors, geometry, inverse diagonals, transfer xhat (levels >= 2); "
-                            "fp64 arithmetic, coarse solve and outer CG"}
+                 "storage": "fp32 level vectors, geometry, inverse diagonals, transfer xhat (levels >= 2), "
+                            "single-precision arithmetic in the applies and transfers (NNMG_MIXED_ARITH=64: fp64), "
+                            "coarse solve from the packed inverse in fp32 tiles where faster, fp64 coarse vectors "
+                            "and outer CG",
+                 "coarse_solver": H.coarse_solver.info()}
         H.set_precision(64)
 
     cpu = None
