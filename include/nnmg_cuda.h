@@ -208,9 +208,10 @@ int nnmg_vcycle_run(nnmg_vcycle_t vcycle, const double* f_dev, double* x_dev, vo
 /* 64 (default): the fp64 cycle.  32: the mixed-precision cycle of the paper
  * (the V-cycle in single precision inside double-precision CG):
  * level vectors, stored geometry, inverse diagonals and transfer reference
- * coordinates in fp32 on every level above the coarsest, fp64 arithmetic in
- * registers, the coarse solve in fp64; f_dev / x_dev stay fp64.  Parity is by
- * outer CG iteration count. */
+ * coordinates in fp32 on every level above the coarsest, single-precision
+ * arithmetic in the cell applies and the transfers (environment
+ * NNMG_MIXED_ARITH=64: fp64 arithmetic on the fp32 storage), fp64 coarse
+ * vectors; f_dev / x_dev stay fp64.  Parity is by outer CG iteration count. */
 int nnmg_vcycle_set_precision(nnmg_vcycle_t vcycle, int bits);
 /* coarse solver the mixed-precision cycle uses instead of the fp64 cycle's
  * (NULL: the same one); the caller keeps it alive while it is attached */
