@@ -338,6 +338,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       const char* ex = getenv("NNMG_ELAST_XCH");
       // measured on B200 (C5 fine apply): 257 -> 222 us
       L->elast_xch = ex ? atoi(ex) != 0 : true;
+      const char* mb = getenv("NNMG_APPLY_MINB");
+      L->apply_minb = mb ? atoi(mb) : 0;
       const char* ma = getenv("NNMG_MIXED_ARITH");
       L->mixed_arith32 = ma ? atoi(ma) != 64 : true;
       const char* et = getenv("NNMG_ELAST_TMA");
@@ -752,6 +754,11 @@ struct ApplyLaunchT {
     } else {
     if constexpr (D == 3 && P >= 3 && PH == kLaplace) {
       if (L.edges.ptr && L.apply_recompute) {
+        // NNMG_APPLY_MINB: min CTAs per SM of the launch bound (register cap) for the split variants
+        if (L.apply_split == 8 && L.apply_minb == 6) return launch<D, P, NC, PH, 8, 2, 6>();
+        if (L.apply_split == 8 && L.apply_minb == 4) return launch<D, P, NC, PH, 8, 2, 4>();
+        if (L.apply_split == 4 && L.apply_minb == 3) return launch<D, P, NC, PH, 4, 2, 3>();
+        if (L.apply_split == 4 && L.apply_minb == 2) return launch<D, P, NC, PH, 4, 2, 2>();
         if (L.apply_split == 8) return launch<D, P, NC, PH, 8, 2>();
         if (L.apply_split == 4) return launch<D, P, NC, PH, 4, 2>();
         if (L.apply_split == 2) return launch<D, P, NC, PH, 2, 2>();

@@ -23,6 +23,7 @@ struct Level {
   DevBuf<double> inv_diag;
   bool diag_ready = false;
   bool reg_kernel = true;  // register-resident thread-per-cell apply where supported
+  int apply_minb = 0;      // launch bound (min CTAs/SM) of the recomputed-G pencil apply (0: default 5)
   int apply_split = 1;     // CTAs per cell block of the pencil apply kernel (1, 2, 4, 8)
   bool apply_geos = false; // pencil apply: geometry staged in shared memory (Q3/Q4)
   bool apply_recompute = false; // pencil apply: G recomputed from edge vectors (3D Laplace Q3/Q4)
