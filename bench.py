@@ -77,6 +77,7 @@ def relaunch_under_torchrun(args):
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries the one JSON line
     raise SystemExit(subprocess.call(cmd, env=env))
 
 
@@ -739,6 +740,7 @@ def run_distributed(args, cfg):
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL's version / debug lines stay off stdout
     dist.init_process_group("nccl", device_id=dev)
     from paper_2412_10910_b200 import _lib, distributed, fespace
 

@@ -116,6 +116,10 @@ int nnmg_smoother_sweep(nnmg_level_t level, double lam_max, double lam_min, int 
  * it in place), d = c1 d + c2 inv_diag r, x += d   (solvers.py:94-107) */
 int nnmg_cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag,
                     double theta, double* r, double* d, double* x, void* stream);
+/* first post-smoothing sweep right after the prolongation (multigrid.py:107-111):
+ * r already holds b - A (x0 + t); d = inv_diag*r/theta, x = (x0 + t) + d */
+int nnmg_cheb_start_t(int64_t n, const double* t, const double* x0, const double* inv_diag, double theta,
+                      const double* r, double* d, double* x, void* stream);
 int nnmg_cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
                    double* x, void* stream);
 

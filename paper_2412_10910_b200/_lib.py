@@ -55,6 +55,7 @@ _SIGNATURES = {
     "nnmg_smoother_sweep": [_handle, c_double, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_cheb_start": [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p, c_void_p,
                         c_void_p],
+    "nnmg_cheb_start_t": [c_int64, c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_cheb_step": [c_int64, c_void_p, c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p, c_void_p],
     "nnmg_dot_workspace": [],
     "nnmg_dot2": [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],

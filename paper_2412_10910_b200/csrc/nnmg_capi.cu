@@ -152,6 +152,14 @@ int nnmg_cheb_start(int64_t n, const double* b, const double* ax, const double* 
   return guard([&] { cheb_start(n, b, ax, x0, inv_diag, theta, r, d, x, S(stream)); });
 }
 
+int nnmg_cheb_start_t(int64_t n, const double* t, const double* x0, const double* inv_diag, double theta,
+                      const double* r, double* d, double* x, void* stream) {
+  return guard([&] {
+    NNMG_REQUIRE(n >= 0 && (n == 0 || (t && x0 && inv_diag && r && d && x)), kInvalidArgument, "null vector");
+    cheb_start_t(n, t, x0, inv_diag, theta, r, d, x, S(stream));
+  });
+}
+
 int nnmg_cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
                    double* x, void* stream) {
   return guard([&] { cheb_step(n, ad, inv_diag, c1, c2, r, d, x, S(stream)); });

@@ -23,6 +23,18 @@ __global__ void k_cheb_start(int64_t n, const double* b, const double* __restric
   x[i] = x0 ? x0[i] + di : di;
 }
 
+// r already holds b - A (x0 + t): d = inv_diag*r/theta; x = (x0 + t) + d (the first
+// post-smoothing sweep right after the prolongation, multigrid.py:107-111)
+__global__ void k_cheb_start_t(int64_t n, const double* __restrict__ t, const double* x0,
+                               const double* __restrict__ inv_diag, double theta, const double* __restrict__ r,
+                               double* __restrict__ d, double* x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = inv_diag[i] * r[i] / theta;
+  d[i] = di;
+  x[i] = (x0[i] + t[i]) + di;
+}
+
 // r -= Ad; z = inv_diag r; d = c1 d + c2 z; x += d                 (solvers.py:101-107)
 __global__ void k_cheb_step(int64_t n, const double* __restrict__ ad, const double* __restrict__ inv_diag,
                             double c1, double c2, double* __restrict__ r, double* __restrict__ d,
@@ -280,6 +292,14 @@ void cheb_start(int64_t n, const double* b, const double* ax, const double* x0, 
                 double* r, double* d, double* x, cudaStream_t s) {
   if (!n) return;
   k_cheb_start<<<grid_for(n), kBS, 0, s>>>(n, b, ax, x0, inv_diag, theta, r, d, x);
+  NNMG_CHECK_LAUNCH();
+  count_launch();
+}
+
+void cheb_start_t(int64_t n, const double* t, const double* x0, const double* inv_diag, double theta,
+                  const double* r, double* d, double* x, cudaStream_t s) {
+  if (!n) return;
+  k_cheb_start_t<<<grid_for(n), kBS, 0, s>>>(n, t, x0, inv_diag, theta, r, d, x);
   NNMG_CHECK_LAUNCH();
   count_launch();
 }

@@ -10,6 +10,8 @@ void dot2(int64_t n, const double* a, const double* b, const double* c, const do
           cudaStream_t s);
 void cheb_start(int64_t n, const double* b, const double* ax, const double* x0, const double* inv_diag, double theta,
                 double* r, double* d, double* x, cudaStream_t s);
+void cheb_start_t(int64_t n, const double* t, const double* x0, const double* inv_diag, double theta,
+                  const double* r, double* d, double* x, cudaStream_t s);
 void cheb_step(int64_t n, const double* ad, const double* inv_diag, double c1, double c2, double* r, double* d,
                double* x, cudaStream_t s);
 void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double theta, const double* r, double* d,

@@ -290,7 +290,8 @@ class DistLevel:
         self.n = layout.n_local_full
         self.n_owned = layout.n_owned_full
         self.overlap = True  # interior cells overlap the ghost import (False: import, then all cells)
-        self._t = backend.zeros(self.n)
+        self._t = backend.zeros(self.n)   # product scratch of the unsplit residual form
+        self._tc = backend.zeros(self.n)  # prolongated correction of the V-cycle
         self._r = backend.zeros(self.n)  # smoother work vectors (fixed addresses: graph capture)
         self._d = backend.zeros(self.n)
         d = backend.diagonal_partial(op)
@@ -373,14 +374,23 @@ class DistLevel:
         return out
 
     # -- Chebyshev-Jacobi sweep (solvers.py:88-108) on local vectors --------
-    def smooth_into(self, b, x0, x, degree, window):
+    def smooth_into(self, b, x0, x, degree, window, residual_out=False, t=None):
+        """One degree-k sweep.  residual_out: one more residual-form apply
+        leaves b - A x in self._r (the recurrence keeps r = b - A (x - d), so
+        the V-cycle needs no copy of b and no extra vector for its residual).
+        t: self._r already holds b - A x0 (left by residual_out) and the sweep
+        starts from x0 + t, the prolongated correction: r -= A t, then
+        x = (x0 + t) + d in the first vector kernel (no copy of b either)."""
         lam_max = self.lam_max
         lam_min = lam_max / window
         theta = (lam_max + lam_min) / 2.0
         delta = (lam_max - lam_min) / 2.0
         sigma = theta / delta
         r, d = self._r, self._d
-        if x0 is None:
+        if t is not None:
+            self.apply_sub_into(t, r)  # r = b - A (x0 + t)
+            self.bk.cheb_start_t(t, x0, self.inv_diag, theta, r, d, x)
+        elif x0 is None:
             self.bk.cheb_start(b, None, None, self.inv_diag, theta, r, d, x)
         else:
             r.copy_(b)
@@ -392,6 +402,8 @@ class DistLevel:
             rho = 1.0 / (2.0 * sigma - rho_old)
             self.bk.cheb_step(None, self.inv_diag, rho * rho_old, 2.0 * rho / delta, r, d, x)
             rho_old = rho
+        if residual_out:
+            self.apply_sub_into(d, r)  # r = b - A x
         return x
 
     def estimate_lam_max(self, n_iter=12, seed=0, safety=1.1):
@@ -466,6 +478,8 @@ class DistHierarchy:
         # point-to-point and the coarse all-reduce) captured as one CUDA graph
         self.use_graph = bool(graph)
         self._graph = None
+        # residuals from the smoother recurrence (False: the explicit form of multigrid.py:97, 101)
+        self.recurrence = True
 
     @property
     def finest(self):
@@ -479,14 +493,32 @@ class DistHierarchy:
             return x
         T = self.transfers[l - 2]
         x = lev.bk.empty(lev.n)  # fully written by the first sweep
+        rc = T.coarse.bk.zeros(T.coarse.n)
+        if self.recurrence and self.m1 >= 1 and self.m2 >= 1:
+            # residual after pre-smoothing from the smoother's recurrence and
+            # the first post-smoothing sweep from that residual (as the native
+            # executor): no copy of f, no read-modify-write of x by
+            # the prolongation; the same applies as multigrid.py:93-111
+            cur = None
+            for k in range(self.m1):
+                lev.smooth_into(f, cur, x, self.degree, self.window, residual_out=(k == self.m1 - 1))
+                cur = x
+            T.restrict_into(lev._r, rc)
+            delta = self._v(l - 1, rc)
+            T.prolongate_into(delta, lev._tc, accumulate=False)
+            lev.smooth_into(f, x, x, self.degree, self.window, t=lev._tc)
+            for _ in range(self.m2 - 1):
+                lev.smooth_into(f, x, x, self.degree, self.window)
+            return x
         cur = None
         for _ in range(self.m1):
             lev.smooth_into(f, cur, x, self.degree, self.window)
             cur = x
+        if cur is None:
+            x.zero_()
         r = lev.bk.empty(lev.n)
         r.copy_(f)
         lev.apply_sub_into(x, r)  # r = f - A x (multigrid.py:97)
-        rc = T.coarse.bk.zeros(T.coarse.n)
         T.restrict_into(r, rc)
         delta = self._v(l - 1, rc)
         T.prolongate_into(delta, x, accumulate=True)
@@ -771,6 +803,13 @@ class GpuBackend:
         D = self._D
         _lib.call("nnmg_cheb_start", r.numel(), D.ptr(b), D.ptr(ax), D.ptr(x0), D.ptr(inv_diag), float(theta),
                   D.ptr(r), D.ptr(d), D.ptr(x), D.stream_ptr(self.device))
+
+    def cheb_start_t(self, t, x0, inv_diag, theta, r, d, x):
+        from . import _lib
+
+        D = self._D
+        _lib.call("nnmg_cheb_start_t", r.numel(), D.ptr(t), D.ptr(x0), D.ptr(inv_diag), float(theta), D.ptr(r),
+                  D.ptr(d), D.ptr(x), D.stream_ptr(self.device))
 
     def cheb_step(self, ad, inv_diag, c1, c2, r, d, x):
         from . import _lib

@@ -115,6 +115,10 @@ class OracleBackend:
         d.copy_(inv_diag * r / theta)
         x.copy_(x0 + d if x0 is not None else d)
 
+    def cheb_start_t(self, t, x0, inv_diag, theta, r, d, x):
+        d.copy_(inv_diag * r / theta)
+        x.copy_((x0 + t) + d)
+
     def cheb_step(self, ad, inv_diag, c1, c2, r, d, x):
         if ad is not None:
             r -= ad

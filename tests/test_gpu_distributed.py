@@ -61,6 +61,11 @@ def test_distributed_gpu_backend_world1(cname, scale):
         DH.use_graph, DH._graph = False, None
         z0 = fine.gather_global(DH.precondition(fine.from_global(b)))
         assert np.linalg.norm(zd - z0) <= 1e-12 * np.linalg.norm(z0)
+        # ... and to the explicit-residual form of multigrid.py:97, 101 (rounding-level difference)
+        DH.recurrence = False
+        z1 = fine.gather_global(DH.precondition(fine.from_global(b)))
+        assert np.linalg.norm(z1 - z0) <= 1e-11 * np.linalg.norm(z0)
+        DH.recurrence = True
         for lev in DH.levels:
             lev.overlap = True
         DH.use_graph = True
