@@ -189,6 +189,12 @@ int nnmg_coarse_cg_create(nnmg_level_t level, double reduction, int max_iter, nn
  * read.  The library packs it into symmetric 64x64 tiles (nf^2/2 doubles
  * streamed per solve, no atomics: bitwise reproducible). */
 int nnmg_coarse_direct_create(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out);
+/* one share of the same solve for cell-partitioned runs: this
+ * handle packs and streams the tiles [nt share / n_shares, nt (share+1) / n_shares)
+ * only; the outputs of all shares add up to the solution (share 0 also
+ * writes the identity rows, the others zeros), so the ranks all-reduce x. */
+int nnmg_coarse_direct_create_share(nnmg_level_t level, const double* inverse_dev, int64_t ld, int share,
+                                    int n_shares, nnmg_coarse_t* out);
 /* the same with the tiles stored in fp32 (half the streamed bytes;
  * single-precision products within a tile, fp64 partial sums): the coarse
  * solver of the mixed-precision cycle, see nnmg_vcycle_set_mixed_coarse */

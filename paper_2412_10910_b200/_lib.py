@@ -75,6 +75,7 @@ _SIGNATURES = {
     "nnmg_coarse_cg_create": [_handle, c_double, c_int, POINTER(_handle)],
     "nnmg_coarse_direct_create": [_handle, c_void_p, c_int64, POINTER(_handle)],
     "nnmg_coarse_direct_create_f32": [_handle, c_void_p, c_int64, POINTER(_handle)],
+    "nnmg_coarse_direct_create_share": [_handle, c_void_p, c_int64, c_int, c_int, POINTER(_handle)],
     "nnmg_coarse_destroy": [_handle],
     "nnmg_coarse_solve": [_handle, c_void_p, c_void_p, c_void_p],
     "nnmg_coarse_status": [_handle, POINTER(c_int), POINTER(c_int), POINTER(c_int)],

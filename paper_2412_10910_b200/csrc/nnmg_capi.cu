@@ -271,6 +271,15 @@ int nnmg_coarse_direct_create(nnmg_level_t level, const double* inverse_dev, int
   });
 }
 
+int nnmg_coarse_direct_create_share(nnmg_level_t level, const double* inverse_dev, int64_t ld, int share, int n_shares,
+                                    nnmg_coarse_t* out) {
+  return guard([&] {
+    REQUIRE_HANDLE(level);
+    NNMG_REQUIRE(out && inverse_dev, kInvalidArgument, "null argument");
+    *out = reinterpret_cast<nnmg_coarse_t>(coarse_direct_create(LV(level), inverse_dev, ld, false, share, n_shares));
+  });
+}
+
 int nnmg_coarse_direct_create_f32(nnmg_level_t level, const double* inverse_dev, int64_t ld, nnmg_coarse_t* out) {
   return guard([&] {
     REQUIRE_HANDLE(level);

@@ -33,6 +33,8 @@ struct Coarse {
   bool tiles_f32 = false;        // fp32 tiles (the mixed-precision cycle's coarse solve)
   DevBuf<float> tiles32;
   DevBuf<double> prow, pcol;     // per-tile partial products (rows of I / columns of J)
+  int64_t t0 = 0, t1 = 0;        // this handle's tile range (a share of the tiles when split across ranks)
+  bool identity = true;          // this share writes the identity (constrained) rows
 };
 
 Coarse* coarse_dense_create(Level* L, const double* inverse);
@@ -41,7 +43,10 @@ Coarse* coarse_cg_create(Level* L, double reduction, int max_iter);
 // memory): the inverse of the free-DoF block (free DoFs ascending, the
 // complement of the level's constrained list), read in its lower triangle
 // only and packed into symmetric tiles
-Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bool f32 = false);
+// share / n_shares: this handle streams an equal contiguous share of the tiles
+// (cell-partitioned runs: the shares' outputs are summed by an all-reduce)
+Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bool f32 = false, int share = 0,
+                             int n_shares = 1);
 void coarse_direct_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
 void coarse_solve(Coarse& C, const double* b, double* x, cudaStream_t s);
 void coarse_status(Coarse& C, int* iterations, int* converged, int* error);

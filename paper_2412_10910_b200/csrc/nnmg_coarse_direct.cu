@@ -37,10 +37,10 @@ __device__ inline void tri_decode(int64_t t, int& I, int& J) {
 // full (lower triangle read) -> tiles; the diagonal tiles are symmetrised
 // from the lower triangle, padding is zero
 template <class TT>
-__global__ void k_pack(const double* __restrict__ full, int64_t n, int64_t ld, TT* __restrict__ tiles) {
-  // full: the free-block inverse (n = number of free DoFs)
+__global__ void k_pack(const double* __restrict__ full, int64_t n, int64_t ld, TT* __restrict__ tiles, int64_t t0) {
+  // full: the free-block inverse (n = number of free DoFs); this handle's tiles start at t0
   int I, J;
-  tri_decode(blockIdx.x, I, J);
+  tri_decode(t0 + blockIdx.x, I, J);
   TT* dst = tiles + int64_t(blockIdx.x) * kT * kT;
   for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
     const int r = e / kT, c = e % kT;
@@ -73,14 +73,15 @@ struct Tile2<float> {
 template <class TT>
 __global__ void __launch_bounds__(256) k_symv_tiles(const TT* __restrict__ tiles, const double* __restrict__ x,
                                                     const int* __restrict__ freedofs, int64_t n,
-                                                    double* __restrict__ prow, double* __restrict__ pcol) {
+                                                    double* __restrict__ prow, double* __restrict__ pcol, int64_t t0) {
   using double2 = typename Tile2<TT>::type;  // element pairs of the tile type
   using double_t = TT;
   __shared__ double_t xs[2][kT];
   __shared__ double2 cs[8][kT / 2];
+  // tiles, prow and pcol hold this handle's tile range [t0, t0 + gridDim.x) only
   const int64_t t = blockIdx.x;
   int I, J;
-  tri_decode(t, I, J);
+  tri_decode(t0 + t, I, J);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const double2* tp = reinterpret_cast<const double2*>(tiles + t * (kT * kT));
   double2 a[8];
@@ -147,18 +148,23 @@ __global__ void __launch_bounds__(256) k_symv_reduce(const double* __restrict__ 
                                                      const double* __restrict__ pcol, int nb, int64_t n,
                                                      const int* __restrict__ freedofs, const int* __restrict__ cons,
                                                      int64_t ncons, const double* __restrict__ b,
-                                                     double* __restrict__ y) {
+                                                     double* __restrict__ y, int64_t t0, int64_t t1, int identity) {
+  // [t0, t1): the tile range of this handle (a share of the tiles when the
+  // solve is split across ranks: the shares' outputs add up to the solution,
+  // and exactly one share writes the identity rows, the others zeros)
   __shared__ double part[4][kT];
   if (int(blockIdx.x) >= nb) {
     for (int64_t i = int64_t(blockIdx.x - nb) * blockDim.x + threadIdx.x; i < ncons;
          i += int64_t(gridDim.x - nb) * blockDim.x)
-      y[cons[i]] = b[cons[i]];
+      y[cons[i]] = identity ? b[cons[i]] : 0.0;
     return;
   }
   const int I = blockIdx.x, r = threadIdx.x & (kT - 1), q = threadIdx.x >> 6;
   double s = 0.0;
   for (int j = q; j < nb; j += 4) {
-    const double v = j <= I ? __ldcg(prow + tri_id(I, j) * kT + r) : __ldcg(pcol + tri_id(j, I) * kT + r);
+    const int64_t t = j <= I ? tri_id(I, j) : tri_id(j, I);
+    if (t < t0 || t >= t1) continue;
+    const double v = j <= I ? __ldcg(prow + (t - t0) * kT + r) : __ldcg(pcol + (t - t0) * kT + r);
     s += v;
   }
   part[q][r] = s;
@@ -171,7 +177,8 @@ __global__ void __launch_bounds__(256) k_symv_reduce(const double* __restrict__ 
 
 }  // namespace
 
-Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bool f32) {
+Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bool f32, int share, int n_shares) {
+  NNMG_REQUIRE(n_shares >= 1 && share >= 0 && share < n_shares, kInvalidArgument, "tile share out of range");
   NNMG_REQUIRE(L != nullptr && inverse_dev != nullptr, kInvalidArgument, "null argument");
   NNMG_CUDA_TRY(cudaSetDevice(L->device));
   // free DoFs: the complement of the level's sorted constrained list
@@ -196,8 +203,13 @@ Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bo
     C->dfree.upload(freed);
     C->dcons.upload(cons);
     C->nb = static_cast<int>((nf + kT - 1) / kT);
-    const int64_t nt = tri_id(C->nb, 0);
-    NNMG_REQUIRE(nt < (int64_t(1) << 31), kInvalidArgument, "coarse level too large for the direct solve");
+    const int64_t nt_all = tri_id(C->nb, 0);
+    NNMG_REQUIRE(nt_all < (int64_t(1) << 31), kInvalidArgument, "coarse level too large for the direct solve");
+    // this handle's share of the tiles (equal contiguous ranges; one share = all)
+    C->t0 = nt_all * share / n_shares;
+    C->t1 = nt_all * (share + 1) / n_shares;
+    C->identity = share == 0;
+    const int64_t nt = C->t1 - C->t0;
     C->tiles_f32 = f32;
     if (f32)
       C->tiles32.alloc(size_t(nt) * kT * kT);
@@ -209,9 +221,9 @@ Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bo
     C->status.zero();
     if (nt) {
       if (f32)
-        k_pack<float><<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles32.ptr);
+        k_pack<float><<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles32.ptr, C->t0);
       else
-        k_pack<double><<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles.ptr);
+        k_pack<double><<<unsigned(nt), 256>>>(inverse_dev, nf, ld, C->tiles.ptr, C->t0);
     }
     NNMG_CHECK_LAUNCH();
     NNMG_CUDA_TRY(cudaDeviceSynchronize());
@@ -223,19 +235,21 @@ Coarse* coarse_direct_create(Level* L, const double* inverse_dev, int64_t ld, bo
 }
 
 void coarse_direct_solve(Coarse& C, const double* b, double* x, cudaStream_t s) {
-  const int64_t nt = tri_id(C.nb, 0);
+  const int64_t nt = C.t1 - C.t0;
   const int64_t ncons = static_cast<int64_t>(C.dcons.n);
   if (nt) {
     if (C.tiles_f32)
-      k_symv_tiles<float><<<unsigned(nt), 256, 0, s>>>(C.tiles32.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr);
+      k_symv_tiles<float><<<unsigned(nt), 256, 0, s>>>(C.tiles32.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr,
+                                                        C.t0);
     else
-      k_symv_tiles<double><<<unsigned(nt), 256, 0, s>>>(C.tiles.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr);
+      k_symv_tiles<double><<<unsigned(nt), 256, 0, s>>>(C.tiles.ptr, b, C.dfree.ptr, C.nfree, C.prow.ptr, C.pcol.ptr,
+                                                         C.t0);
     NNMG_CHECK_LAUNCH();
   }
   const unsigned extra = static_cast<unsigned>(std::min<int64_t>((ncons + 255) / 256, 64));
   if (C.nb + extra) {
     k_symv_reduce<<<unsigned(C.nb) + extra, 256, 0, s>>>(C.prow.ptr, C.pcol.ptr, C.nb, C.nfree, C.dfree.ptr,
-                                                          C.dcons.ptr, ncons, b, x);
+                                                          C.dcons.ptr, ncons, b, x, C.t0, C.t1, C.identity ? 1 : 0);
     NNMG_CHECK_LAUNCH();
   }
   count_launch(nt ? 2 : 1);

@@ -781,8 +781,38 @@ class GpuBackend:
     def make_coarse(self, op):
         from .solvers import CoarseSolver
 
-        cs = CoarseSolver(op, direct="auto")
+        world = dist.get_world_size() if dist.is_initialized() else 1
+        if world == 1:
+            cs = CoarseSolver(op, direct="auto")
+        else:
+            # with peers the direct path streams 1/world of the inverse tiles
+            # per rank and the shares are summed by one all-reduce of the
+            # coarse vector (the replicated CG otherwise): the coarse solve
+            # then scales with the ranks instead of bounding the parallel
+            # efficiency.  The choice is made collectively (slowest
+            # CG time, smallest free memory) so every rank takes the same path.
+            from .solvers import DIRECT_STREAM_BYTES_PER_S, direct_solve_bytes
+
+            cs = CoarseSolver(op, direct=False)
+            if not cs.dense:
+                nf = op.n_dofs - len(op.constraints.dofs)
+                mem = torch.cuda.mem_get_info(self.device)[0]
+                v = torch.tensor([cs._time_cg(), -float(mem)], dtype=torch.float64, device=self.device)
+                dist.all_reduce(v, op=dist.ReduceOp.MAX)
+                t_cg, mem = float(v[0]), -float(v[1])
+                t_direct = direct_solve_bytes(nf) / DIRECT_STREAM_BYTES_PER_S / world
+                fits = 3 * 8 * nf ** 2 + direct_solve_bytes(nf) // world < 0.8 * mem
+                if fits and t_direct < 0.9 * t_cg:
+                    cs = CoarseSolver(op, direct=True, share=(dist.get_rank(), world))
+                cs.timing = dict(cs.timing or {}, cg_s=t_cg, direct_predicted_s=t_direct)
         self.coarse_solver = cs
+        if cs.partial:
+            def solve(b, x):
+                cs.solve_into(b, x)
+                dist.all_reduce(x)
+                return x
+
+            return solve
         return lambda b, x: cs.solve_into(b, x)
 
     def dot(self, a, b):

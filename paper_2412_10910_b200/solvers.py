@@ -262,9 +262,15 @@ class CoarseSolver:
     then differs from the reference's at the level of the coarse CG tolerance
     (1e-8); outer CG iteration counts are the parity gate."""
 
-    def __init__(self, op, dense_limit=2000, cg_reduction=1e-8, cg_max_iter=10_000, direct=False):
+    def __init__(self, op, dense_limit=2000, cg_reduction=1e-8, cg_max_iter=10_000, direct=False, share=None):
         if direct not in (False, True, "auto"):
             raise ValueError("direct must be False, True or 'auto'")
+        # share = (i, n): cell-partitioned runs with the direct path stream an
+        # equal share of the inverse tiles per rank; solve_into then yields a
+        # PARTIAL result and the caller sums the shares (all-reduce)
+        if share is not None and not (len(share) == 2 and 0 <= share[0] < share[1]):
+            raise ValueError("share must be (index, count) with 0 <= index < count")
+        self.share = tuple(int(v) for v in share) if share is not None and share[1] > 1 else None
         self.op = op
         self.device = op.device
         self.cg_reduction = cg_reduction
@@ -313,10 +319,13 @@ class CoarseSolver:
             t_cg = self._time_cg() if direct == "auto" else None
             t_direct = direct_solve_bytes(nf) / DIRECT_STREAM_BYTES_PER_S
             mem = torch.cuda.mem_get_info(self.device)[0]
+            if self.share is not None:
+                t_direct /= self.share[1]
             fits = 3 * 8 * nf ** 2 + direct_solve_bytes(nf) < 0.8 * mem
             self.timing = {"cg_s": t_cg, "direct_predicted_s": t_direct}
             if direct is True or (fits and t_direct < 0.9 * t_cg):
                 self._make_direct()
+        self.partial = self.direct and self.share is not None  # solve_into returns this rank's share of x
 
     def _time_cg(self):
         """Device time of one CG solve on a random right-hand side (after one
@@ -341,7 +350,7 @@ class CoarseSolver:
         (nnmg_coarse_direct_create_f32), half the bytes of the fp64 direct
         solve.  Built on first use where the direct path is allowed
         (direct=True / "auto") and predicted faster than the active solver."""
-        if self.dense or not self._direct_mode:
+        if self.dense or not self._direct_mode or self.share is not None:
             return None
         if self._h32 is None and not self._h32_tried:
             self._h32_tried = True
@@ -387,8 +396,12 @@ class CoarseSolver:
         inv = torch.cholesky_inverse(Lc)
         del Lc
         h = ctypes.c_void_p()
-        _lib.call("nnmg_coarse_direct_create_f32" if f32 else "nnmg_coarse_direct_create", self.op.handle,
-                  inv.data_ptr(), len(free), ctypes.byref(h))
+        if self.share is not None and not f32:
+            _lib.call("nnmg_coarse_direct_create_share", self.op.handle, inv.data_ptr(), len(free), self.share[0],
+                      self.share[1], ctypes.byref(h))
+        else:
+            _lib.call("nnmg_coarse_direct_create_f32" if f32 else "nnmg_coarse_direct_create", self.op.handle,
+                      inv.data_ptr(), len(free), ctypes.byref(h))
         torch.cuda.synchronize(self.device)
         del inv
         if f32:

@@ -134,3 +134,23 @@ def test_mixed_cycle_uses_fp32_tile_coarse_solve(pkg):
         chebyshev_degree=4, coarse_direct=False, vcycle_precision=32))
     Hp.v_cycle(b)
     assert Hp.coarse_solver._h32 is None and not Hp.coarse_solver.direct
+
+
+@pytest.mark.parametrize("n_shares", [2, 3, 8])
+def test_direct_tile_shares_add_up(pkg, oracle, n_shares):
+    """Cell-partitioned runs split the inverse tiles across ranks
+    (nnmg_coarse_direct_create_share): the shares' outputs add up to the full
+    solve (identity rows from share 0 only), in a fixed order per share."""
+    sp, op, A = level(pkg, oracle, (30, 30), 2)
+    full = pkg.solvers.CoarseSolver(op, dense_limit=0, direct=True)
+    parts = [pkg.solvers.CoarseSolver(op, dense_limit=0, direct=True, share=(i, n_shares)) for i in range(n_shares)]
+    assert all(p.partial for p in parts) and not full.partial
+    b = np.random.default_rng(3).standard_normal(sp.n_dofs)
+    want = full.solve(b)
+    got = sum(p.solve(b) for p in parts)
+    assert rel(got, want) <= 1e-14
+    assert rel(got, np.linalg.solve(A, b)) <= 1e-10
+    cd = np.asarray(sp.constraints.dofs)
+    assert np.array_equal(parts[0].solve(b)[cd], b[cd]) and not parts[1].solve(b)[cd].any()
+    with pytest.raises(ValueError):
+        pkg.solvers.CoarseSolver(op, dense_limit=0, direct=True, share=(2, 2))
