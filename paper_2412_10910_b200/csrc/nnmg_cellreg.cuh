@@ -126,6 +126,9 @@ struct CellReg {
   static constexpr int SLICE_Q = DIM == 3 ? N1 * N1 : NLOC;
   static constexpr unsigned SLICE_BYTES = unsigned(SLICE_Q) * NG * CB * sizeof(double);
   static constexpr size_t WARP_SMEM = 2 * size_t(SLICE_BYTES) + 16;
+  // GEO 4: the whole fp32 chunk of a warp's 32 cells plus its mbarrier
+  static constexpr unsigned CHUNK32_BYTES = unsigned(NLOC) * NG * CB * sizeof(float);
+  static constexpr size_t WARP_SMEM32 = size_t(CHUNK32_BYTES) + 16;
 
   // TD / TG: storage types of dst and of the stored geometry (double, or
   // float in the mixed-precision V-cycle); TA: the arithmetic type (double;
@@ -139,10 +142,14 @@ struct CellReg {
                                                int64_t blk, int lane, const double* __restrict__ edges = nullptr,
                                                double* wsm = nullptr, double* __restrict__ cellout = nullptr) {
     static_assert(GEO != 3 || sizeof(TG) == sizeof(double), "TMA slice staging is fp64");
-    static_assert(GEO == 0 || sizeof(TA) == sizeof(double), "recomputed / staged geometry is fp64 arithmetic");
+    static_assert(GEO != 4 || (kPairedGeo<TG> && DIM == 3), "whole-chunk staging: paired fp32 geometry");
+    static_assert(GEO == 0 || GEO == 4 || sizeof(TA) == sizeof(double),
+                  "recomputed / slice-staged geometry is fp64 arithmetic");
     static_assert(!kEnergy || sizeof(TA) == sizeof(double), "cell energies are fp64");
     double* gbuf = wsm;
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(wsm + 2 * SLICE_Q * NG * CB);
+    unsigned long long* mbar4 =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(wsm) + CHUNK32_BYTES);  // GEO 4
     const TG* gchunk = geo + blk * (int64_t)NLOC * NG * CB;
     if constexpr (GEO == 3) {
       static_assert(DIM == 3, "slice staging is 3D");
@@ -155,6 +162,19 @@ struct CellReg {
           mbar_expect_tx(&mbar[s], SLICE_BYTES);
           tma_load_1d(gbuf + s * SLICE_Q * NG * CB, gchunk + s * SLICE_Q * NG * CB, SLICE_BYTES, &mbar[s]);
         }
+      }
+      __syncwarp();
+    }
+    if constexpr (GEO == 4) {
+      // GEO 4 (fp32 geometry, 3D): the warp's whole chunk (NLOC x NG x CB
+      // floats, 20.7 KB for Q2) by ONE TMA bulk copy issued before the gather:
+      // every geometry byte is in flight while the gathers and the sweeps
+      // run, and the point loop reads shared memory
+      if (lane == 0) {
+        mbar_init(mbar4, 1);
+        fence_proxy_async();
+        mbar_expect_tx(mbar4, CHUNK32_BYTES);
+        tma_load_1d(wsm, gchunk, CHUNK32_BYTES, mbar4);
       }
       __syncwarp();
     }
@@ -281,6 +301,9 @@ struct CellReg {
             mbar_wait(&mbar[qz & 1], (qz >> 1) & 1);
           }
         }
+        if constexpr (GEO == 4) {
+          if (q == 0) mbar_wait(mbar4, 0);
+        }
         point(qx, qy, qz, [&](TA gx, TA gy, TA gz, TA& fx, TA& fy, TA& fz) {
           TA gg[NG];
           if constexpr (GEO == 1) {
@@ -289,6 +312,14 @@ struct CellReg {
             const double* G = gbuf + ((qz & 1) * SLICE_Q + q % SLICE_Q) * NG * CB + lane;
 #pragma unroll
             for (int k = 0; k < NG; ++k) gg[k] = G[k * CB];
+          } else if constexpr (GEO == 4) {
+            const float2* G2 = reinterpret_cast<const float2*>(wsm) + q * (NG / 2) * CB + lane;
+#pragma unroll
+            for (int k = 0; k < NG / 2; ++k) {
+              const float2 t = G2[k * CB];
+              gg[2 * k] = TA(t.x);
+              gg[2 * k + 1] = TA(t.y);
+            }
           } else if constexpr (kPairedGeo<TG>) {
             // fp32 geometry of the 3D levels is stored in pairs [q][k/2][CB][2]:
             // 8-byte loads, 256 bytes per warp instruction like the fp64 stream

@@ -552,6 +552,22 @@ __global__ void __launch_bounds__(128, 1) k_apply_reg_tma(Tables tab, const doub
                                                    nullptr, wsm);
 }
 
+// fp32 geometry, the warp's whole chunk staged in shared memory by one TMA bulk copy (3D, GEO 4)
+template <int D, int P>
+__global__ void __launch_bounds__(128, 2) k_apply_reg_tma32(Tables tab, const float* __restrict__ src,
+                                                           float* __restrict__ dst, const int* __restrict__ idx,
+                                                           const float* __restrict__ geo, int64_t b0, int64_t b1,
+                                                           const int* __restrict__ cd, int64_t ncd) {
+  extern __shared__ __align__(128) unsigned char dsm_raw[];
+  if (ncd) constrained_rows<true>(cd, ncd, src, dst);
+  const int warp = threadIdx.x >> 5;
+  const int64_t blk = b0 + blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  if (blk >= b1) return;
+  double* wsm = reinterpret_cast<double*>(dsm_raw + warp * ((CellReg<D, P>::WARP_SMEM32 + 127) / 128 * 128));
+  CellReg<D, P>::template run<true, false, true, 4, float>(tab, PlainSrcT<float>{src}, dst, idx, geo, blk,
+                                                           threadIdx.x & 31, nullptr, wsm);
+}
+
 // all blocks recompute G from edge vectors, sum-factorised along z-pencils (3D)
 template <int D, int P, bool NEG>
 __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const double* __restrict__ src,
@@ -627,6 +643,24 @@ struct ApplyLaunchT {
         const int64_t nb = b1 - b0;
         constexpr int kWarpsPerCta = 4;
         const unsigned g = static_cast<unsigned>((nb + kWarpsPerCta - 1) / kWarpsPerCta);
+        if constexpr (D == 3) {
+          if (L.mixed_arith32 && L.reg_tma) {
+            constexpr size_t wsmem = (CellReg<D, P>::WARP_SMEM32 + 127) / 128 * 128;
+            constexpr size_t smem = kWarpsPerCta * wsmem;
+            static bool attr = false;
+            if (!attr) {
+              NNMG_CUDA_TRY(cudaFuncSetAttribute(k_apply_reg_tma32<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+              attr = true;
+            }
+            k_apply_reg_tma32<D, P><<<g, 32 * kWarpsPerCta, smem, s>>>(L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1,
+                                                                      cd, ncd);
+            fused = true;
+            NNMG_CHECK_LAUNCH();
+            count_launch();
+            return;
+          }
+        }
         // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
         auto kr = L.mixed_arith32 ? (L.reg_minb == 4 ? k_apply_reg<D, P, 4, true, false, float, float, float> : (L.reg_minb == 2 ? k_apply_reg<D, P, 2, true, false, float, float, float> : k_apply_reg<D, P, 3, true, false, float, float, float>))
                                   : k_apply_reg<D, P, 1, true, false, float, float, double>;

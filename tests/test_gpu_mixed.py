@@ -69,6 +69,19 @@ def test_mixed_precision_iterations_match_reference(pkg, monkeypatch, tag, arith
     assert np.linalg.norm(r) <= 1.01e-8 * np.linalg.norm(b)
 
 
+def test_mixed_precision_tma_staged_geometry(pkg, monkeypatch):
+    # NNMG_REG_TMA=1: the fp32 register apply stages each warp's geometry chunk by one TMA bulk copy
+    monkeypatch.setenv("NNMG_REG_TMA", "1")
+    g, H, b = _hierarchy(pkg, "C3_s8", 32)
+    z32 = H.v_cycle(b)
+    H.set_precision(64)
+    z64 = H.v_cycle(b)
+    assert 0 < rel(z32, z64) <= 2e-4
+    H.set_precision(32)
+    res = pkg.solvers.cg_solve(H.finest.operator, b, precond=H.precondition, target_reduction=1e-8)
+    assert res.converged and abs(res.iterations - int(g["iterations"])) <= 1
+
+
 def test_mixed_precision_graph_replay_and_errors(pkg):
     g, H, b = _hierarchy(pkg, "C2_s8", 32)
     f = torch.from_numpy(b).cuda()
