@@ -49,7 +49,7 @@ static void smoother_sweep_f32(Level& L, double lam_max, double lam_min, int deg
                                float* x, float* work, cudaStream_t s, bool residual_out, const float* t) {
   const int64_t n = L.n_dofs;
   float* r = work;
-  float* d = work + n;
+  float* d = work + ((n + 3) & ~int64_t(3));  // 16-byte aligned: the float4 vector kernels
   const float* idg = L.inv_diag32.ptr;
   const double theta = (lam_max + lam_min) / 2.0;
   const double delta = (lam_max - lam_min) / 2.0;
@@ -239,7 +239,7 @@ void vcycle_set_precision(VCycle& V, int bits) {
       level_enable_f32(*V.levels[l], 0);
       transfer_enable_f32(*V.transfers[l - 1], 0);
       V.r32[l].alloc(n);
-      V.work32[l].alloc(3 * n);
+      V.work32[l].alloc(3 * ((n + 3) & ~int64_t(3)));
     }
   }
   V.cf.alloc(V.levels[0]->n_dofs);

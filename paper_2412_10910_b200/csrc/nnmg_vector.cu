@@ -50,6 +50,114 @@ __global__ void k_cheb_step(int64_t n, const double* __restrict__ ad, const doub
   x[i] += di;
 }
 
+// fp32 vectors, four entries per thread (16-byte loads / stores; one entry
+// per thread moves 128 bytes per warp instruction and measured 4.7 TB/s on
+// C3 against 6.9 TB/s for the fp64 kernel).  Single-precision arithmetic.
+// Thread i < n4 handles entries 4 i .. 4 i + 3, the first n - 4 n4 threads
+// also one tail entry.  All pointers 16-byte aligned (checked by the caller).
+__device__ __forceinline__ float4 ld4(const float* p, int64_t i) { return reinterpret_cast<const float4*>(p)[i]; }
+__device__ __forceinline__ void st4(float* p, int64_t i, float4 v) { reinterpret_cast<float4*>(p)[i] = v; }
+
+__global__ void k_cheb_update_f4(int64_t n4, int64_t n, const float* __restrict__ inv_diag, float c1, float c2,
+                                 const float* __restrict__ r, float* __restrict__ d, float* __restrict__ x,
+                                 int x_is_d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  auto one = [&](float di_old, float id, float ri, float xi, float& dn, float& xn) {
+    dn = c1 * di_old + c2 * (id * ri);
+    xn = (x_is_d ? di_old : xi) + dn;
+  };
+  if (i < n4) {
+    const float4 id = ld4(inv_diag, i), rr = ld4(r, i), dd = ld4(d, i);
+    float4 xx = x_is_d ? dd : ld4(x, i);
+    float4 dn, xn;
+    one(dd.x, id.x, rr.x, xx.x, dn.x, xn.x);
+    one(dd.y, id.y, rr.y, xx.y, dn.y, xn.y);
+    one(dd.z, id.z, rr.z, xx.z, dn.z, xn.z);
+    one(dd.w, id.w, rr.w, xx.w, dn.w, xn.w);
+    st4(d, i, dn);
+    st4(x, i, xn);
+  }
+  const int64_t j = 4 * n4 + i;
+  if (i < n - 4 * n4) {
+    const float dold = d[j];
+    float dn, xn;
+    one(dold, inv_diag[j], r[j], x_is_d ? dold : x[j], dn, xn);
+    d[j] = dn;
+    x[j] = xn;
+  }
+}
+
+// x0 == nullptr: r = b, d = inv_diag b / theta, x = d (if x); else r holds b - A x0: d = inv_diag r / theta, x = x0 + d
+__global__ void k_cheb_init_f4(int64_t n4, int64_t n, const float* __restrict__ b, const float* x0,
+                               const float* __restrict__ inv_diag, float rtheta, float* __restrict__ r,
+                               float* __restrict__ d, float* x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n4) {
+    const float4 id = ld4(inv_diag, i);
+    float4 ri;
+    if (x0) {
+      ri = ld4(r, i);
+    } else {
+      ri = ld4(b, i);
+      st4(r, i, ri);
+    }
+    const float4 di = make_float4(id.x * ri.x * rtheta, id.y * ri.y * rtheta, id.z * ri.z * rtheta,
+                                  id.w * ri.w * rtheta);
+    st4(d, i, di);
+    if (x) {
+      if (x0) {
+        const float4 xo = ld4(x0, i);
+        st4(x, i, make_float4(xo.x + di.x, xo.y + di.y, xo.z + di.z, xo.w + di.w));
+      } else {
+        st4(x, i, di);
+      }
+    }
+  }
+  const int64_t j = 4 * n4 + i;
+  if (i < n - 4 * n4) {
+    float ri;
+    if (x0) {
+      ri = r[j];
+    } else {
+      ri = b[j];
+      r[j] = ri;
+    }
+    const float di = inv_diag[j] * ri * rtheta;
+    d[j] = di;
+    if (x) x[j] = x0 ? x0[j] + di : di;
+  }
+}
+
+// r holds f - A (x + t): d = inv_diag r / theta, x = (x + t) + d
+__global__ void k_cheb_init_add_f4(int64_t n4, int64_t n, const float* __restrict__ t,
+                                   const float* __restrict__ inv_diag, float rtheta, const float* __restrict__ r,
+                                   float* __restrict__ d, float* __restrict__ x) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n4) {
+    const float4 id = ld4(inv_diag, i), ri = ld4(r, i), tt = ld4(t, i), xx = ld4(x, i);
+    const float4 di = make_float4(id.x * ri.x * rtheta, id.y * ri.y * rtheta, id.z * ri.z * rtheta,
+                                  id.w * ri.w * rtheta);
+    st4(d, i, di);
+    st4(x, i, make_float4((xx.x + tt.x) + di.x, (xx.y + tt.y) + di.y, (xx.z + tt.z) + di.z, (xx.w + tt.w) + di.w));
+  }
+  const int64_t j = 4 * n4 + i;
+  if (i < n - 4 * n4) {
+    const float di = inv_diag[j] * r[j] * rtheta;
+    d[j] = di;
+    x[j] = (x[j] + t[j]) + di;
+  }
+}
+
+static inline bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// NNMG_MIXED_ARITH=64 keeps the scalar kernels (fp64 arithmetic on the fp32 storage)
+static bool vec_f32() {
+  static const bool on = [] {
+    const char* e = getenv("NNMG_MIXED_ARITH");
+    return !(e && atoi(e) == 64);
+  }();
+  return on;
+}
+
 // In-place residual form: the apply scatters -A d straight into r.
 // x0 == nullptr: r = b, d = inv_diag*b/theta, x = d
 // otherwise r already holds b - A x0: d = inv_diag*r/theta, x = x0 + d
@@ -102,6 +210,13 @@ void cheb_init_add(int64_t n, const double* t, const double* inv_diag, double th
 }
 void cheb_init_add(int64_t n, const float* t, const float* inv_diag, double theta, const float* r, float* d,
                    float* x, cudaStream_t s) {
+  if (n && vec_f32() && aligned16(t) && aligned16(inv_diag) && aligned16(r) && aligned16(d) && aligned16(x)) {
+    const int64_t n4 = n / 4;
+    k_cheb_init_add_f4<<<grid_for(n4 + 1), kBS, 0, s>>>(n4, n, t, inv_diag, float(1.0 / theta), r, d, x);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
   cheb_init_add_t(n, t, inv_diag, theta, r, d, x, s);
 }
 
@@ -133,6 +248,14 @@ void cheb_init(int64_t n, const double* b, const double* x0, const double* inv_d
 }
 void cheb_init(int64_t n, const float* b, const float* x0, const float* inv_diag, double theta, float* r, float* d,
                float* x, cudaStream_t s) {
+  if (n && vec_f32() && aligned16(b) && aligned16(x0) && aligned16(inv_diag) && aligned16(r) && aligned16(d) &&
+      aligned16(x)) {
+    const int64_t n4 = n / 4;
+    k_cheb_init_f4<<<grid_for(n4 + 1), kBS, 0, s>>>(n4, n, b, x0, inv_diag, float(1.0 / theta), r, d, x);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
   cheb_init_t(n, b, x0, inv_diag, theta, r, d, x, s);
 }
 
@@ -150,6 +273,13 @@ void cheb_update(int64_t n, const double* inv_diag, double c1, double c2, const 
 }
 void cheb_update(int64_t n, const float* inv_diag, double c1, double c2, const float* r, float* d, float* x,
                  cudaStream_t s, bool x_is_d) {
+  if (n && vec_f32() && aligned16(inv_diag) && aligned16(r) && aligned16(d) && aligned16(x)) {
+    const int64_t n4 = n / 4;
+    k_cheb_update_f4<<<grid_for(n4 + 1), kBS, 0, s>>>(n4, n, inv_diag, float(c1), float(c2), r, d, x, x_is_d ? 1 : 0);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
   cheb_update_t(n, inv_diag, c1, c2, r, d, x, s, x_is_d);
 }
 
@@ -197,8 +327,42 @@ void convert_t(int64_t n, const A* a, B* b, cudaStream_t s) {
   NNMG_CHECK_LAUNCH();
   count_launch();
 }
-void convert(int64_t n, const double* a, float* b, cudaStream_t s) { convert_t(n, a, b, s); }
-void convert(int64_t n, const float* a, double* b, cudaStream_t s) { convert_t(n, a, b, s); }
+// four entries per thread (16-byte accesses on the fp32 side, 2 x 16 on the fp64 side)
+__global__ void k_convert_d2f4(int64_t n4, int64_t n, const double* __restrict__ a, float* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n4) {
+    const double2 lo = reinterpret_cast<const double2*>(a)[2 * i], hi = reinterpret_cast<const double2*>(a)[2 * i + 1];
+    reinterpret_cast<float4*>(b)[i] = make_float4(float(lo.x), float(lo.y), float(hi.x), float(hi.y));
+  }
+  if (i < n - 4 * n4) b[4 * n4 + i] = float(a[4 * n4 + i]);
+}
+__global__ void k_convert_f2d4(int64_t n4, int64_t n, const float* __restrict__ a, double* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n4) {
+    const float4 v = reinterpret_cast<const float4*>(a)[i];
+    reinterpret_cast<double2*>(b)[2 * i] = make_double2(double(v.x), double(v.y));
+    reinterpret_cast<double2*>(b)[2 * i + 1] = make_double2(double(v.z), double(v.w));
+  }
+  if (i < n - 4 * n4) b[4 * n4 + i] = double(a[4 * n4 + i]);
+}
+void convert(int64_t n, const double* a, float* b, cudaStream_t s) {
+  if (n && aligned16(a) && aligned16(b)) {
+    k_convert_d2f4<<<grid_for(n / 4 + 1), kBS, 0, s>>>(n / 4, n, a, b);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
+  convert_t(n, a, b, s);
+}
+void convert(int64_t n, const float* a, double* b, cudaStream_t s) {
+  if (n && aligned16(a) && aligned16(b)) {
+    k_convert_f2d4<<<grid_for(n / 4 + 1), kBS, 0, s>>>(n / 4, n, a, b);
+    NNMG_CHECK_LAUNCH();
+    count_launch();
+    return;
+  }
+  convert_t(n, a, b, s);
+}
 
 // y = alpha*x + beta*y  (general axpby; beta==0 ignores y's content)
 __global__ void k_axpby(int64_t n, double alpha, const double* __restrict__ x, double beta, double* __restrict__ y) {
