@@ -135,8 +135,17 @@ struct CellReg {
   // float = the paper's single-precision V-cycle: with fp64
   // arithmetic on fp32 storage the kernel is bound by its DFMAs and its
   // 248 registers, 543 us against 597 us for fp64 storage on C3)
-  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class TA = double, class Src, class TD,
-            class TG>
+  // XNB (warp-neighbour faces): lane c and lane c + 1 hold x-adjacent cells on
+  // structured rows, so the last x-node of every line of cell c IS the first
+  // x-node of cell c + 1.  Checked per line and lane pair at run time (index
+  // comparison through one shuffle, no setup tables, any mesh): where it
+  // holds the first node's value comes from the left neighbour's register
+  // (no gather) and the last node's contribution is handed to the right
+  // neighbour's first node before the scatter (no atomic): N1^(d-1) of the
+  // N1^d gathers and atomics of a cell disappear (9 of 27 for 3D Q2).  The
+  // L2 atomic units see 57M fp32 REDs per C3 apply otherwise.
+  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class TA = double, bool XNB = false,
+            class Src, class TD, class TG>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, TD* __restrict__ dst,
                                                const int* __restrict__ idx, const TG* __restrict__ geo,
                                                int64_t blk, int lane, const double* __restrict__ edges = nullptr,
@@ -191,10 +200,41 @@ struct CellReg {
     }
     TA v[NLOC];
     const int* ib = idx + blk * NLOC * CB + lane;
+    constexpr int NLINE = NLOC / N1;
+    unsigned share_r = 0;  // XNB bit per line: my last x-node is the right neighbour's first
+    if constexpr (XNB) {
+      constexpr unsigned kFull = 0xffffffffu;
+      // phases, so that every load of a phase is in flight together: all
+      // indices, the match bits (shuffles of indices), all values, then the
+      // shuffles of the shared values
+      int gi[NLOC];
 #pragma unroll
-    for (int l = 0; l < NLOC; ++l) {
-      const int g = ld_geo<kStream>(ib + l * CB);
-      v[l] = g >= 0 ? TA(src((int64_t)g)) : TA(0);
+      for (int l = 0; l < NLOC; ++l) gi[l] = ld_geo<kStream>(ib + l * CB);
+      unsigned share_l = 0;
+#pragma unroll
+      for (int line = 0; line < NLINE; ++line) {
+        const int gf = gi[line * N1], gl = gi[line * N1 + N1 - 1];
+        const int nbf = __shfl_down_sync(kFull, gf, 1);
+        share_r |= ((lane < 31 && gl >= 0 && nbf == gl) ? 1u : 0u) << line;
+      }
+      share_l = __shfl_up_sync(kFull, share_r, 1);  // every lane takes part in the shuffle
+      if (lane == 0) share_l = 0u;
+#pragma unroll
+      for (int l = 0; l < NLOC; ++l) {
+        const bool from_left = l % N1 == 0 && ((share_l >> (l / N1)) & 1u);
+        v[l] = (gi[l] >= 0 && !from_left) ? TA(src((int64_t)gi[l])) : TA(0);
+      }
+#pragma unroll
+      for (int line = 0; line < NLINE; ++line) {
+        const TA recv = __shfl_up_sync(kFull, v[line * N1 + N1 - 1], 1);
+        if ((share_l >> line) & 1u) v[line * N1] = recv;
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < NLOC; ++l) {
+        const int g = ld_geo<kStream>(ib + l * CB);
+        v[l] = g >= 0 ? TA(src((int64_t)g)) : TA(0);
+      }
     }
     TA u0[kEnergy ? NLOC : 1];
     if constexpr (kEnergy) {
@@ -364,10 +404,39 @@ struct CellReg {
     sweep_axis<1, true, TA>(tS, w);
     sweep_axis<0, true, TA>(tS, w);
     double energy = 0.0;
+    if constexpr (XNB) {
+      static_assert(!kEnergy, "warp-neighbour sharing is for the plain apply");
+      // hand the last-node contributions of shared faces to the right neighbour
+      constexpr unsigned kFull = 0xffffffffu;
+      if (cellout) share_r = 0;  // deterministic mode keeps every slot: no hand-over (warp-uniform)
+      const unsigned share_l = __shfl_up_sync(kFull, share_r, 1);
+#pragma unroll
+      for (int line = 0; line < NLINE; ++line) {
+        const int lf = line * N1, ll = line * N1 + N1 - 1;
+        const bool mr = (share_r >> line) & 1u;
+        const TA recv = __shfl_up_sync(kFull, mr ? w[ll] : TA(0), 1);
+        if (lane > 0 && ((share_l >> line) & 1u)) w[lf] += recv;
+      }
+    }
+    // the index table is re-read (L1/L2 hit) rather than kept live across the
+    // sweeps; XNB reads it as one batch (its lane-dependent skips otherwise
+    // serialise the reloads: 918 vs 625 us measured) and marks the shared
+    // last nodes, which were handed over, as skipped
+    int gs[XNB ? NLOC : 1];
+    if constexpr (XNB) {
+#pragma unroll
+      for (int l = 0; l < NLOC; ++l) gs[l] = kStream ? __ldg(ib + l * CB) : ib[l * CB];
+#pragma unroll
+      for (int line = 0; line < NLINE; ++line)
+        if ((share_r >> line) & 1u) gs[line * N1 + N1 - 1] = -1;
+    }
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) {
-      // the index table is re-read (L1/L2 hit) rather than kept live
-      const int g = kStream ? __ldg(ib + l * CB) : ib[l * CB];
+      int g;
+      if constexpr (XNB)
+        g = gs[l];
+      else
+        g = kStream ? __ldg(ib + l * CB) : ib[l * CB];
       if (g >= 0) {
         // deterministic mode: the cell's result goes to the cell buffer in
         // the idx layout (coalesced), a fixed-order gather sums it later

@@ -338,6 +338,14 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       const char* ex = getenv("NNMG_ELAST_XCH");
       // measured on B200 (C5 fine apply): 257 -> 222 us
       L->elast_xch = ex ? atoi(ex) != 0 : true;
+      // warp-neighbour face sharing in the register Laplace apply.  Measured on
+      // B200: fp32 arithmetic (mixed cycle) C3 4.66 -> 4.39 ms, C2 0.329 ->
+      // 0.314 ms; fp64 2D (C2) apply 23.6 -> 21.5 us; fp64 3D (C3) apply 626
+      // -> 677 us (DRAM-bound already: the extra shuffle phases only cost).
+      // Default: on for the fp32 kernels and for 2D fp64, off for 3D fp64.
+      const char* xn = getenv("NNMG_REG_XNB");
+      L->reg_xnb32 = xn ? atoi(xn) != 0 : true;
+      L->reg_xnb = xn ? atoi(xn) != 0 : dim == 2;
       const char* mb = getenv("NNMG_APPLY_MINB");
       L->apply_minb = mb ? atoi(mb) : 0;
       const char* ma = getenv("NNMG_MIXED_ARITH");
@@ -513,7 +521,8 @@ __device__ __forceinline__ void constrained_rows(const int* __restrict__ cd, int
 // hybrids 0.67-0.74 ms (1/4 .. 3/4 of the blocks recomputing).  Blocks with
 // blk % rmod < rnum take the recompute path.  HYB is an opt-in instantiation
 // (NNMG_RECOMPUTE_MOD / NNMG_RECOMPUTE_NUM) so the default kernel stays lean.
-template <int D, int P, int MINB, bool NEG, bool HYB, class TV = double, class TG = double, class TA = double>
+template <int D, int P, int MINB, bool NEG, bool HYB, class TV = double, class TG = double, class TA = double,
+          bool XNB = false>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* __restrict__ src, TV* __restrict__ dst,
                                                    const int* __restrict__ idx, const TG* __restrict__ geo,
                                                    int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod,
@@ -533,8 +542,8 @@ __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* _
         continue;
       }
     }
-    CellReg<D, P>::template run<true, false, NEG, 0, TA>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk,
-                                                         threadIdx.x & 31, nullptr, nullptr, cellout);
+    CellReg<D, P>::template run<true, false, NEG, 0, TA, XNB>(tab, PlainSrcT<TV>{src}, dst, idx, geo, blk,
+                                                              threadIdx.x & 31, nullptr, nullptr, cellout);
   }
 }
 
@@ -662,6 +671,14 @@ struct ApplyLaunchT {
           }
         }
         // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
+        if (L.mixed_arith32 && L.reg_xnb32) {
+          k_apply_reg<D, P, 3, true, false, float, float, float, true><<<g, 32 * kWarpsPerCta, 0, s>>>(
+              L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, nullptr, 0, 1, cd, ncd, nullptr);
+          fused = true;
+          NNMG_CHECK_LAUNCH();
+          count_launch();
+          return;
+        }
         auto kr = L.mixed_arith32 ? (L.reg_minb == 4 ? k_apply_reg<D, P, 4, true, false, float, float, float> : (L.reg_minb == 2 ? k_apply_reg<D, P, 2, true, false, float, float, float> : k_apply_reg<D, P, 3, true, false, float, float, float>))
                                   : k_apply_reg<D, P, 1, true, false, float, float, double>;
         kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, nullptr, 0, 1, cd, ncd,
@@ -710,6 +727,16 @@ struct ApplyLaunchT {
             count_launch();
             return;
           }
+        }
+        if (L.reg_xnb && !(L.edges.ptr && L.recompute_mod > 0)) {
+          auto kx = neg ? k_apply_reg<D, P, 1, true, false, double, double, double, true>
+                        : k_apply_reg<D, P, 1, false, false, double, double, double, true>;
+          kx<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, nullptr, 0, 1, cd, ncd,
+                                              nullptr);
+          fused = true;
+          NNMG_CHECK_LAUNCH();
+          count_launch();
+          return;
         }
         const bool hyb = L.edges.ptr && L.recompute_mod > 0;
         auto kr = hyb ? (neg ? k_apply_reg<D, P, 1, true, true> : k_apply_reg<D, P, 1, false, true>)

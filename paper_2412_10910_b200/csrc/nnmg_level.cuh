@@ -39,6 +39,8 @@ struct Level {
   DevBuf<unsigned> bln_slot;      // [nblk][(nloc+1)/2][cb] staging positions (CellRegElast::bln_phys) of two local points per word, 0xFFFF = constrained / padding
   bool elast_tma = false;       // elasticity register apply: geometry slices staged in shared memory by TMA
   bool elast_xch = true;        // elasticity register apply: node-major gather/scatter via shared memory
+  bool reg_xnb = false;         // fp64 register apply: x-adjacent cells of a warp share their face nodes (shuffles instead of gathers / atomics)
+  bool reg_xnb32 = true;        // the same in the fp32-arithmetic apply of the mixed-precision cycle
   bool reg_tma = false;         // register apply (3D): G streamed through shared memory by TMA bulk copies
   bool fuse_constrained = true;  // register kernels handle the constrained rows in their prologue
   int reg_minb = 1;        // min CTAs/SM launch bound of that kernel (4 caps registers at 128: spills)

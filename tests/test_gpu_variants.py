@@ -73,6 +73,16 @@ APPLY_VARIANTS = [
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "4"}),
     ("op_3d_q4", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "8"}),
     ("op_3d_q3", {"NNMG_APPLY_RECOMPUTE": "0", "NNMG_APPLY_GEOS": "1", "NNMG_APPLY_SPLIT": "4"}),
+    # x-adjacent cells of a warp share their face nodes (shuffles instead of gathers / atomics)
+    ("op_3d_q2", {"NNMG_REG_XNB": "1"}),
+    ("op_3d_q1", {"NNMG_REG_XNB": "1"}),
+    ("op_2d_q2", {"NNMG_REG_XNB": "1"}),
+    ("op_2d_q1", {"NNMG_REG_XNB": "1"}),
+    ("op_2d_q3", {"NNMG_REG_XNB": "1"}),
+    ("op_3d_q2_neumann", {"NNMG_REG_XNB": "1"}),
+    ("op_ref_lshape_q2", {"NNMG_REG_XNB": "1"}),
+    ("op_2d_q2", {"NNMG_REG_XNB": "0"}),
+    ("op_2d_q1", {"NNMG_REG_XNB": "0"}),
     # constrained rows by the separate copy / subtract kernels instead of the cell kernels' prologue
     ("op_3d_q2", {"NNMG_FUSE_CONSTRAINED": "0"}),
     ("op_2d_q2", {"NNMG_FUSE_CONSTRAINED": "0"}),
