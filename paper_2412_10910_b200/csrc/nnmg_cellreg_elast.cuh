@@ -130,8 +130,14 @@ struct CellRegElast {
   // TA: the arithmetic type (double; float = single-precision arithmetic of
   // the mixed-precision V-cycle: registers, the exchange buffers and with
   // them the L1 wavefronts of the three phases halve)
+  // XNB (with XCH): x-adjacent cells of the block share the last x-node of
+  // every line with the next cell's first one where the index tables say so
+  // (checked per line and cell pair, any mesh): the shared value is read from
+  // the left neighbour's exchange slot instead of gathered, and the shared
+  // contribution is added into the right neighbour's first node instead of
+  // scattered: N1^2 of the N1^3 gathers and atomics per cell and component.
   template <bool kNeg, int GEO = 0, class TV, class TG, bool XCH = false, bool GSM = false, bool BLN = false,
-            class TA = double>
+            class TA = double, bool XNB = false>
   __device__ __forceinline__ static void run(const Tables& tab, const TV* __restrict__ src, TV* __restrict__ dst,
                                              const int* __restrict__ idx, const TG* __restrict__ geo, int64_t blk,
                                              double lam, double mu, double* sm, double* __restrict__ cellout = nullptr,
@@ -225,6 +231,40 @@ struct CellRegElast {
       for (int l = 0; l < NLOC; ++l) {
         const unsigned k = (l & 1) ? kk[l / 2] >> 16 : kk[l / 2] & 0xFFFFu;
         v[l] = k != 0xFFFFu ? sm[w * KS + k] : 0.0;
+      }
+      __syncthreads();  // phase A reuses the buffer
+    } else if constexpr (XCH && XNB) {
+      static_assert(!BLN && !GSM, "warp-neighbour sharing extends the plain node-major exchange");
+      constexpr int NLINE = NLOC / N1;
+      const int* xb = idx + blk * NLOC * CB + xc;
+      {
+        // node-major thread (cell xc, component xw): all indices first, then the values
+        int g[NLOC], gleft[NLINE];
+#pragma unroll
+        for (int l = 0; l < NLOC; ++l) g[l] = __ldg(xb + l * CB);
+#pragma unroll
+        for (int q = 0; q < NLINE; ++q) gleft[q] = xc > 0 ? __ldg(xb + (q * N1 + N1 - 1) * CB - 1) : -2;
+#pragma unroll
+        for (int l = 0; l < NLOC; ++l) {
+          const bool shared = l % N1 == 0 && g[l] >= 0 && gleft[l / N1] == g[l];
+          smt[(l * 3 + xw) * XS + xc] =
+              (g[l] >= 0 && !shared) ? TA(__ldg(src + (int64_t)g[l] * 3 + xw)) : TA(0);
+        }
+      }
+      __syncthreads();
+      {
+        // component thread (w, cell lane): the first node of a shared line comes from the left cell's last node
+        int gf[NLINE], gleft[NLINE];
+#pragma unroll
+        for (int q = 0; q < NLINE; ++q) {
+          gf[q] = __ldg(ib + (q * N1) * CB);
+          gleft[q] = lane > 0 ? __ldg(ib + (q * N1 + N1 - 1) * CB - 1) : -2;
+        }
+#pragma unroll
+        for (int l = 0; l < NLOC; ++l) {
+          const bool shared = l % N1 == 0 && gf[l / N1] >= 0 && gleft[l / N1] == gf[l / N1];
+          v[l] = shared ? smt[((l + N1 - 1) * 3 + w) * XS + lane - 1] : smt[(l * 3 + w) * XS + lane];
+        }
       }
       __syncthreads();  // phase A reuses the buffer
     } else if constexpr (XCH) {
@@ -459,6 +499,25 @@ struct CellRegElast {
         for (int l = 0; l < NLOC; ++l) smt[(l * 3 + w) * XS + lane] = acc[l];
         __syncthreads();
         const int* xb = idx + blk * NLOC * CB + xc;
+        if constexpr (XNB) {
+          constexpr int NLINE = NLOC / N1;
+          int g[NLOC], gleft[NLINE], gright[NLINE];
+#pragma unroll
+          for (int l = 0; l < NLOC; ++l) g[l] = __ldg(xb + l * CB);
+#pragma unroll
+          for (int q = 0; q < NLINE; ++q) {
+            gleft[q] = xc > 0 ? __ldg(xb + (q * N1 + N1 - 1) * CB - 1) : -2;
+            gright[q] = xc < CB - 1 ? __ldg(xb + (q * N1) * CB + 1) : -2;
+          }
+#pragma unroll
+          for (int l = 0; l < NLOC; ++l) {
+            TA a = smt[(l * 3 + xw) * XS + xc];
+            if (l % N1 == 0 && g[l] >= 0 && gleft[l / N1] == g[l]) a += smt[((l + N1 - 1) * 3 + xw) * XS + xc - 1];
+            const bool handed = l % N1 == N1 - 1 && gright[l / N1] == g[l];  // the right cell adds and scatters it
+            if (g[l] >= 0 && !handed) atomicAdd(dst + (int64_t)g[l] * 3 + xw, TV(kNeg ? -a : a));
+          }
+          return;
+        }
 #pragma unroll
         for (int l = 0; l < NLOC; ++l) {
           const int g = __ldg(xb + l * CB);

@@ -343,6 +343,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       // 0.314 ms; fp64 2D (C2) apply 23.6 -> 21.5 us; fp64 3D (C3) apply 626
       // -> 677 us (DRAM-bound already: the extra shuffle phases only cost).
       // Default: on for the fp32 kernels and for 2D fp64, off for 3D fp64.
+      const char* en = getenv("NNMG_ELAST_XNB");
+      L->elast_xnb = en ? atoi(en) != 0 : false;
       const char* xn = getenv("NNMG_REG_XNB");
       L->reg_xnb32 = xn ? atoi(xn) != 0 : true;
       L->reg_xnb = xn ? atoi(xn) != 0 : dim == 2;
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(128, 1) k_apply_reg_rc(Tables tab, const doubl
 
 // 3D elasticity, one thread per (cell, component): nnmg_cellreg_elast.cuh
 template <int P, bool NEG, int GEO = 0, class TV = double, class TG = double, bool XCH = false, bool GSM = false,
-          bool BLN = false, class TA = double>
+          bool BLN = false, class TA = double, bool XNB = false>
 __global__ void __launch_bounds__(96, sizeof(TA) == sizeof(float) ? 5 : 4) k_apply_reg_elast(Tables tab, const TV* __restrict__ src,
                                                         TV* __restrict__ dst, const int* __restrict__ idx,
                                                         const TG* __restrict__ geo, int64_t b0, int64_t b1,
@@ -603,8 +605,8 @@ __global__ void __launch_bounds__(96, sizeof(TA) == sizeof(float) ? 5 : 4) k_app
   if (ncd) constrained_rows<NEG>(cd, ncd, src, dst);
   const int64_t blk = b0 + blockIdx.x;
   if (blk >= b1) return;
-  CellRegElast<P>::template run<NEG, GEO, TV, TG, XCH, GSM, BLN, TA>(tab, src, dst, idx, geo, blk, lam, mu, sm,
-                                                                     cellout, bln);
+  CellRegElast<P>::template run<NEG, GEO, TV, TG, XCH, GSM, BLN, TA, XNB>(tab, src, dst, idx, geo, blk, lam, mu, sm,
+                                                                          cellout, bln);
 }
 
 // per-cell edge vectors in the blocked layout [blk][(b*2^(d-1)+k)*d + a][CB]
@@ -754,7 +756,8 @@ struct ApplyLaunchT {
     if constexpr (PH == kElasticity && D == 3 && NC == 3 && CellRegElast<P>::kSupported && !kF64) {
       if (L.reg_kernel) {
         // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
-        auto kr = L.mixed_arith32 ? k_apply_reg_elast<P, true, 0, float, float, true, false, false, float>
+        auto kr = L.mixed_arith32 ? (L.elast_xnb ? k_apply_reg_elast<P, true, 0, float, float, true, false, false, float, true>
+                                                 : k_apply_reg_elast<P, true, 0, float, float, true, false, false, float>)
                                   : k_apply_reg_elast<P, true, 0, float, float, true, false, false, double>;
         kr<<<static_cast<unsigned>(b1 - b0), 96, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, L.lam, L.mu,
                                                           cd, ncd, nullptr, BlnTables{});
@@ -784,6 +787,9 @@ struct ApplyLaunchT {
         if (L.elast_tma && L.elast_xch)
           kr = neg ? k_apply_reg_elast<P, true, 0, double, double, true, true>
                    : k_apply_reg_elast<P, false, 0, double, double, true, true>;
+        else if (L.elast_xnb && L.elast_xch && !cellout)
+          kr = neg ? k_apply_reg_elast<P, true, 0, double, double, true, false, false, double, true>
+                   : k_apply_reg_elast<P, false, 0, double, double, true, false, false, double, true>;
         BlnTables bln{};
         if (L.elast_bln && L.bln_node.ptr && !cellout) {
           bln = BlnTables{L.bln_node.ptr, L.bln_cnt.ptr, L.bln_slot.ptr, L.bln_kp};

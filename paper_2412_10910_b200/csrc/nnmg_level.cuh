@@ -37,6 +37,7 @@ struct Level {
   int bln_kp = 0;                 // padded node-list length per block
   DevBuf<int> bln_node, bln_cnt;  // [nblk][kp] global scalar node (-1 pad), [nblk] count
   DevBuf<unsigned> bln_slot;      // [nblk][(nloc+1)/2][cb] staging positions (CellRegElast::bln_phys) of two local points per word, 0xFFFF = constrained / padding
+  bool elast_xnb = false;       // elasticity register apply: x-adjacent cells share their face nodes (with elast_xch)
   bool elast_tma = false;       // elasticity register apply: geometry slices staged in shared memory by TMA
   bool elast_xch = true;        // elasticity register apply: node-major gather/scatter via shared memory
   bool reg_xnb = false;         // fp64 register apply: x-adjacent cells of a warp share their face nodes (shuffles instead of gathers / atomics)

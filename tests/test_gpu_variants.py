@@ -53,6 +53,10 @@ APPLY_VARIANTS = [
     ("op_3d_el_q2", {"NNMG_ELAST_TMA": "0"}),
     ("op_ref_cube3d_el", {"NNMG_ELAST_TMA": "1"}),
     ("op_3d_el_q1", {"NNMG_ELAST_TMA": "1"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_XNB": "1"}),
+    ("op_3d_el_q1", {"NNMG_ELAST_XNB": "1"}),
+    ("op_ref_cube3d_el", {"NNMG_ELAST_XNB": "1"}),
+    ("op_3d_el_q2", {"NNMG_ELAST_XNB": "0"}),
     ("op_3d_el_q2", {"NNMG_ELAST_BLN": "1"}),
     ("op_3d_el_q2", {"NNMG_ELAST_BLN": "1", "NNMG_ELAST_TMA": "1"}),
     ("op_3d_el_q1", {"NNMG_ELAST_BLN": "1"}),
