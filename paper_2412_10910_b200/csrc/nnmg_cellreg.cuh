@@ -144,7 +144,7 @@ struct CellReg {
   // neighbour's first node before the scatter (no atomic): N1^(d-1) of the
   // N1^d gathers and atomics of a cell disappear (9 of 27 for 3D Q2).  The
   // L2 atomic units see 57M fp32 REDs per C3 apply otherwise.
-  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class TA = double, bool XNB = false,
+  template <bool kStream, bool kEnergy, bool kNeg = false, int GEO = 0, class TA = double, int XNB = 0,
             class Src, class TD, class TG>
   __device__ __forceinline__ static double run(const Tables& tab, const Src& src, TD* __restrict__ dst,
                                                const int* __restrict__ idx, const TG* __restrict__ geo,
@@ -202,7 +202,7 @@ struct CellReg {
     const int* ib = idx + blk * NLOC * CB + lane;
     constexpr int NLINE = NLOC / N1;
     unsigned share_r = 0;  // XNB bit per line: my last x-node is the right neighbour's first
-    if constexpr (XNB) {
+    if constexpr (XNB == 1) {
       constexpr unsigned kFull = 0xffffffffu;
       // phases, so that every load of a phase is in flight together: all
       // indices, the match bits (shuffles of indices), all values, then the
@@ -404,10 +404,20 @@ struct CellReg {
     sweep_axis<1, true, TA>(tS, w);
     sweep_axis<0, true, TA>(tS, w);
     double energy = 0.0;
-    if constexpr (XNB) {
+    if constexpr (XNB != 0) {
       static_assert(!kEnergy, "warp-neighbour sharing is for the plain apply");
-      // hand the last-node contributions of shared faces to the right neighbour
       constexpr unsigned kFull = 0xffffffffu;
+      if constexpr (XNB == 2) {
+        // scatter-only sharing: the match bits from the first / last indices of every line
+#pragma unroll
+        for (int line = 0; line < NLINE; ++line) {
+          const int gf = kStream ? __ldg(ib + (line * N1) * CB) : ib[(line * N1) * CB];
+          const int gl = kStream ? __ldg(ib + (line * N1 + N1 - 1) * CB) : ib[(line * N1 + N1 - 1) * CB];
+          const int nbf = __shfl_down_sync(kFull, gf, 1);
+          share_r |= ((lane < 31 && gl >= 0 && nbf == gl) ? 1u : 0u) << line;
+        }
+      }
+      // hand the last-node contributions of shared faces to the right neighbour
       if (cellout) share_r = 0;  // deterministic mode keeps every slot: no hand-over (warp-uniform)
       const unsigned share_l = __shfl_up_sync(kFull, share_r, 1);
 #pragma unroll
@@ -423,7 +433,7 @@ struct CellReg {
     // serialise the reloads: 918 vs 625 us measured) and marks the shared
     // last nodes, which were handed over, as skipped
     int gs[XNB ? NLOC : 1];
-    if constexpr (XNB) {
+    if constexpr (XNB != 0) {
 #pragma unroll
       for (int l = 0; l < NLOC; ++l) gs[l] = kStream ? __ldg(ib + l * CB) : ib[l * CB];
 #pragma unroll
@@ -433,7 +443,7 @@ struct CellReg {
 #pragma unroll
     for (int l = 0; l < NLOC; ++l) {
       int g;
-      if constexpr (XNB)
+      if constexpr (XNB != 0)
         g = gs[l];
       else
         g = kStream ? __ldg(ib + l * CB) : ib[l * CB];

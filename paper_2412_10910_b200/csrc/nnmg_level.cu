@@ -348,6 +348,7 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       const char* xn = getenv("NNMG_REG_XNB");
       L->reg_xnb32 = xn ? atoi(xn) != 0 : true;
       L->reg_xnb = xn ? atoi(xn) != 0 : dim == 2;
+      L->reg_xnb_mode = xn ? atoi(xn) : 1;  // 2: sharing in the scatter only (fp64)
       const char* mb = getenv("NNMG_APPLY_MINB");
       L->apply_minb = mb ? atoi(mb) : 0;
       const char* ma = getenv("NNMG_MIXED_ARITH");
@@ -524,7 +525,7 @@ __device__ __forceinline__ void constrained_rows(const int* __restrict__ cd, int
 // blk % rmod < rnum take the recompute path.  HYB is an opt-in instantiation
 // (NNMG_RECOMPUTE_MOD / NNMG_RECOMPUTE_NUM) so the default kernel stays lean.
 template <int D, int P, int MINB, bool NEG, bool HYB, class TV = double, class TG = double, class TA = double,
-          bool XNB = false>
+          int XNB = 0>
 __global__ void __launch_bounds__(128, MINB) k_apply_reg(Tables tab, const TV* __restrict__ src, TV* __restrict__ dst,
                                                    const int* __restrict__ idx, const TG* __restrict__ geo,
                                                    int64_t b0, int64_t b1, const double* __restrict__ edges, int rmod,
@@ -674,7 +675,7 @@ struct ApplyLaunchT {
         }
         // single-precision arithmetic (the paper's fp32 V-cycle) unless NNMG_MIXED_ARITH=64
         if (L.mixed_arith32 && L.reg_xnb32) {
-          k_apply_reg<D, P, 3, true, false, float, float, float, true><<<g, 32 * kWarpsPerCta, 0, s>>>(
+          k_apply_reg<D, P, 3, true, false, float, float, float, 1><<<g, 32 * kWarpsPerCta, 0, s>>>(
               L.tab, src, dst, L.idx.ptr, L.geo32.ptr, b0, b1, nullptr, 0, 1, cd, ncd, nullptr);
           fused = true;
           NNMG_CHECK_LAUNCH();
@@ -731,8 +732,11 @@ struct ApplyLaunchT {
           }
         }
         if (L.reg_xnb && !(L.edges.ptr && L.recompute_mod > 0)) {
-          auto kx = neg ? k_apply_reg<D, P, 1, true, false, double, double, double, true>
-                        : k_apply_reg<D, P, 1, false, false, double, double, double, true>;
+          auto kx = neg ? k_apply_reg<D, P, 1, true, false, double, double, double, 1>
+                        : k_apply_reg<D, P, 1, false, false, double, double, double, 1>;
+          if (L.reg_xnb_mode == 2)
+            kx = neg ? k_apply_reg<D, P, 1, true, false, double, double, double, 2>
+                     : k_apply_reg<D, P, 1, false, false, double, double, double, 2>;
           kx<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, nullptr, 0, 1, cd, ncd,
                                               nullptr);
           fused = true;

@@ -85,6 +85,9 @@ APPLY_VARIANTS = [
     ("op_2d_q3", {"NNMG_REG_XNB": "1"}),
     ("op_3d_q2_neumann", {"NNMG_REG_XNB": "1"}),
     ("op_ref_lshape_q2", {"NNMG_REG_XNB": "1"}),
+    ("op_3d_q2", {"NNMG_REG_XNB": "2"}),
+    ("op_3d_q2_neumann", {"NNMG_REG_XNB": "2"}),
+    ("op_2d_q2", {"NNMG_REG_XNB": "2"}),
     ("op_2d_q2", {"NNMG_REG_XNB": "0"}),
     ("op_2d_q1", {"NNMG_REG_XNB": "0"}),
     # constrained rows by the separate copy / subtract kernels instead of the cell kernels' prologue
