@@ -343,6 +343,8 @@ Level* level_create(int device, int dim, int degree, int ncomp, int physics, int
       // 0.314 ms; fp64 2D (C2) apply 23.6 -> 21.5 us; fp64 3D (C3) apply 626
       // -> 677 us (DRAM-bound already: the extra shuffle phases only cost).
       // Default: on for the fp32 kernels and for 2D fp64, off for 3D fp64.
+      const char* rw = getenv("NNMG_REG_WARPS");
+      L->reg_warps = rw ? atoi(rw) : 0;  // 0: default by dimension
       const char* en = getenv("NNMG_ELAST_XNB");
       L->elast_xnb = en ? atoi(en) != 0 : false;
       const char* xn = getenv("NNMG_REG_XNB");
@@ -749,8 +751,13 @@ struct ApplyLaunchT {
                       : (neg ? (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, true, false> : k_apply_reg<D, P, 1, true, false>)
                              : (L.reg_minb >= 3 ? k_apply_reg<D, P, 3, false, false>
                                                 : k_apply_reg<D, P, 1, false, false>));
-        kr<<<g, 32 * kWarpsPerCta, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
-                                            hyb ? L.recompute_mod : 0, L.recompute_num, cd, ncd, nullptr);
+        // warps (cell blocks) per CTA (NNMG_REG_WARPS): one-warp CTAs retire independently (no CTA
+        // waits for its slowest warp); measured on B200: C3 apply 626.9 -> 619.4 us, cycle 7.24 ->
+        // 7.16 ms with 1 instead of 4; C2 (2D) neutral.  Default 1 in 3D, 4 in 2D.
+        const int wpc = (L.reg_warps == 1 || L.reg_warps == 2 || L.reg_warps == 4) ? L.reg_warps : (D == 3 ? 1 : 4);
+        const unsigned gw = static_cast<unsigned>((nb + wpc - 1) / wpc);
+        kr<<<gw, 32 * wpc, 0, s>>>(L.tab, src, dst, L.idx.ptr, L.geo.ptr, b0, b1, L.edges.ptr,
+                                    hyb ? L.recompute_mod : 0, L.recompute_num, cd, ncd, nullptr);
         fused = true;
         NNMG_CHECK_LAUNCH();
         count_launch();
