@@ -42,6 +42,7 @@ struct Level {
   bool elast_xch = true;        // elasticity register apply: node-major gather/scatter via shared memory
   bool reg_xnb = false;         // fp64 register apply: x-adjacent cells of a warp share their face nodes (shuffles instead of gathers / atomics)
   int reg_warps = 0;            // fp64 register apply: warps (cell blocks) per CTA (0: 1 in 3D, 4 in 2D)
+  int reg_warps32 = 0;          // the same for the fp32-arithmetic apply (0: 1 in 3D, 4 in 2D)
   int reg_xnb_mode = 1;         // 1: gather and scatter, 2: scatter only
   bool reg_xnb32 = true;        // the same in the fp32-arithmetic apply of the mixed-precision cycle
   bool reg_tma = false;         // register apply (3D): G streamed through shared memory by TMA bulk copies
