@@ -29,7 +29,13 @@ struct TransferDispatchT {
   void operator()() {
     constexpr int CBC = cells_per_block<D, P, NC>();
     const Level& C = *T.coarse;
-    const unsigned g = grid_for(T.nitems, kWarps);
+    // warps (work items / cell chunks) per CTA of the prolongation and the lane restriction
+    // (independent warps: one-warp CTAs retire on their own; measured on B200: C3 prolongation
+    // 151.0 -> 147.5 us, restriction 176.4 -> 173.6 us; C2 (2D) prolongation 18.5 -> 24.6 us, so
+    // the default is 1 in 3D and 4 in 2D; NNMG_TRANSFER_WARPS overrides)
+    const int tw = (T.transfer_warps == 1 || T.transfer_warps == 2 || T.transfer_warps == 4) ? T.transfer_warps
+                                                                                             : (D == 3 ? 1 : kWarps);
+    const unsigned g = grid_for(T.nitems, tw);
     const TV* const xh = [&] {
       if constexpr (kF64)
         return T.xhat.ptr;
@@ -44,7 +50,7 @@ struct TransferDispatchT {
       // fp32 levels: single-precision arithmetic unless NNMG_MIXED_ARITH=64
       if constexpr (!kF64)
         if (T.mixed_arith32) kp = k_prolongate<D, P, NC, CBC, PPL, TV, TV, float>;
-      kp<<<g, kWarps * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.nitems == T.ncc ? nullptr : T.item_cell.ptr,
+      kp<<<g, tw * 32, 0, s>>>(C.tab, in, out, mode, C.idx.ptr, T.nitems == T.ncc ? nullptr : T.item_cell.ptr,
                                    T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems);
       NNMG_CHECK_LAUNCH();
       count_launch();
@@ -63,21 +69,25 @@ struct TransferDispatchT {
           auto kl = D == 3 ? k_restrict_lane<D, P, NC, 3, TV, TV> : k_restrict_lane<D, P, NC, 1, TV, TV>;
           if (T.mixed_arith32)
             kl = D == 3 ? k_restrict_lane<D, P, NC, 3, TV, TV, float> : k_restrict_lane<D, P, NC, 1, TV, TV, float>;
-          kl<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch,
-                                                             T.cellbuf.ptr);
+          const size_t sm = tw * (T.mixed_arith32 ? restrict_lane_smem_per_warp<D, P, NC, float>()
+                                                   : restrict_lane_smem_per_warp<D, P, NC, double>());
+          kl<<<grid_for(nwarps, tw), tw * 32, sm, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch,
+                                                      T.cellbuf.ptr);
         } else if (rk != 2) {
           auto k = rk == 0 ? k_restrict_lane<D, P, NC, 1>
                    : rk == 3 ? k_restrict_lane<D, P, NC, 3>
                              : k_restrict_lane<D, P, NC, 2>;
-          k<<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh,
-                                                            T.nitems, ch, T.cellbuf.ptr);
+          k<<<grid_for(nwarps, tw), tw * 32, tw * restrict_lane_smem_per_warp<D, P, NC, double>(), s>>>(
+              C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         } else {
           k_restrict_staged<D, P, NC><<<grid_for(nwarps, W), W * 32, 0, s>>>(
               C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         }
       } else if constexpr (ipow(P + 1, D) * NC <= 81 && kF64) {
         if (T.restrict_wide) {
-          k_restrict_lane<D, P, NC, 1><<<grid_for(nwarps, kWarps), kWarps * 32, 0, s>>>(
+          // (81 outputs: three 32-output tiles, 32 x 33 doubles per warp)
+          k_restrict_lane<D, P, NC, 1><<<grid_for(nwarps, tw), tw * 32,
+                                        tw * restrict_lane_smem_per_warp<D, P, NC, double>(), s>>>(
               C.tab, in, T.item_pt.ptr, T.pt_dof.ptr, xh, T.nitems, ch, T.cellbuf.ptr);
         } else if (T.restrict_pl == 2 && kPl2) {
           if constexpr (kPl2) {
@@ -233,6 +243,8 @@ Transfer* transfer_create(Level* coarse, Level* fine, int64_t npts, const int64_
       T->restrict_pl = pl ? atoi(pl) : 1;
       const char* ma = getenv("NNMG_MIXED_ARITH");
       T->mixed_arith32 = ma ? atoi(ma) != 64 : true;
+      const char* twp = getenv("NNMG_TRANSFER_WARPS");
+      T->transfer_warps = twp ? atoi(twp) : 0;  // 0: default by dimension
     }
     // fine scalar DoFs without a transfer point: zeroed by the plain prolongation
     std::vector<uint8_t> has(fine->n_scalar, 0);

@@ -15,6 +15,7 @@ struct Transfer {
   int chunk = 1;            // coarse cells per warp in the restriction
   int restrict_kernel = -1;  // variant for NLOC*NCOMP <= 32 (see transfer_create; -1: by dimension)
   int restrict_wide = 0;    // 32 < NLOC*NCOMP <= 81: lane-owned local vector instead of staged groups
+  int transfer_warps = 0;   // warps (work items / cell chunks) per CTA of the prolongation and the lane restriction (0: 1 in 3D, 4 in 2D)
   bool mixed_arith32 = true;  // fp32 vectors: single-precision arithmetic in the transfer kernels
   int restrict_pl = 1;      // staged restriction: planes of the outermost axis per lane (1, 2)
   int prolong_ppl = 1;      // 2: two points per lane also where one is the default

@@ -119,8 +119,9 @@ __global__ void __launch_bounds__(kTransferWarps * 32, PPL > 1 && (PC >= 3 || NC
   constexpr int N1 = PC + 1;
   constexpr int NLOC = ipow(N1, DIM);
   __shared__ TA su[kTransferWarps][NCOMP * NLOC];
+  // blockDim.x / 32 <= kTransferWarps warps per CTA (independent: one work item each)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t item = blockIdx.x * (int64_t)kTransferWarps + warp;
+  const int64_t item = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
   if (item >= nitems) return;
   // item_cell == nullptr: one item per cell (saves a dependent load)
   const int64_t cell = item_cell ? (int64_t)item_cell[item] : item;
@@ -293,6 +294,14 @@ __device__ __forceinline__ void stream_rounds(const CellRounds& R, const int* __
   }
 }
 
+// dynamic shared memory of k_restrict_lane per warp
+template <int DIM, int PC, int NCOMP, class TA>
+constexpr size_t restrict_lane_smem_per_warp() {
+  constexpr int NOUT = ipow(PC + 1, DIM) * NCOMP;
+  constexpr int TW = NOUT < 32 ? NOUT : 32;
+  return size_t(32) * (TW | 1) * sizeof(TA);
+}
+
 // A lane owns a point and the full local vector in registers (NLOC*NCOMP <=
 // 32: Q1/Q2 scalar, 2D vector; up to 81 with NNMG_RESTRICT_WIDE: 3D Q2
 // elasticity, Q3 scalar); a cell's lanes are combined through shared memory
@@ -306,8 +315,10 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
   constexpr int NLOC = ipow(N1, DIM);
   constexpr int NOUT = NLOC * NCOMP;
   static_assert(NOUT <= 81, "lane-owned local vector");
+  // blockDim.x / 32 <= kTransferWarps independent warps per CTA; the reduction
+  // buffer is dynamic shared memory, 32 * RS elements per warp (lane_smem_bytes)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t c0 = (blockIdx.x * (int64_t)kTransferWarps + warp) * chunk;
+  const int64_t c0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + warp) * chunk;
   if (c0 >= ncc) return;
   const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
   const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
@@ -320,8 +331,8 @@ __global__ void __launch_bounds__(kTransferWarps * 32)
   // flush is conditional).
   constexpr int TW = NOUT < 32 ? NOUT : 32;
   constexpr int RS = TW | 1;
-  __shared__ TA red[kTransferWarps][32 * RS];
-  TA* rw = red[warp];
+  extern __shared__ __align__(16) unsigned char lane_smem[];
+  TA* rw = reinterpret_cast<TA*>(lane_smem) + warp * (32 * RS);
   TA acc[NOUT];
 #pragma unroll
   for (int o = 0; o < NOUT; ++o) acc[o] = 0;
