@@ -429,8 +429,20 @@ struct StagedRestrict {
   static constexpr int OV = OZ + N1;
   static constexpr int REC0 = OV + NCOMP;
   static constexpr int REC = ((REC0 - 2 + 15) / 16) * 16 + 2;
-  // per-warp buffer in elements of the arithmetic type (even: keeps the 2-element alignment)
-  static constexpr int WARP_DOUBLES = (2 * P * REC + SLOTS * N1 * PLANE + 1) & ~1;
+  // per-warp buffer in elements of the arithmetic type (even: keeps the
+  // 2-element alignment).  The cell-end reduction buffer [SLOTS][N1][PLANE]
+  // aliases the two staging buffers: at a cell end both are dead (the round's
+  // sub-rounds are over, the next round has not staged yet), so a warp needs
+  // max(staging, reduction) instead of their sum (C5: 15.1 -> 8.6 KB) and more
+  // warps fit per SM.
+  static constexpr int STAGE_ELEMS = 2 * P * REC;
+  static constexpr int RED_ELEMS = SLOTS * N1 * PLANE;
+  // measured on B200: C5 (vector Q2, latency-bound) restriction 68.0 -> 65.8 us with the alias,
+  // C4 (scalar Q4, bound by its table reads) 437 -> 442 us: aliased for vector fields only
+  static constexpr bool kAlias = NCOMP > 1;
+  static constexpr int WARP_DOUBLES =
+      ((kAlias ? (STAGE_ELEMS > RED_ELEMS ? STAGE_ELEMS : RED_ELEMS) : STAGE_ELEMS + RED_ELEMS) + 1) & ~1;
+  // (a launch bound of 5 CTAs per SM on top, 96 registers with spills: C4 437 -> 584 us, C5 68 -> 89 us)
   static constexpr int WARP_BYTES = WARP_DOUBLES * int(sizeof(TA));
   static constexpr int WARPS = (48 * 1024) / WARP_BYTES >= kTransferWarps
                                    ? kTransferWarps
@@ -463,8 +475,8 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL, TA>::WARPS 
   const int64_t c0 = (blockIdx.x * (int64_t)K::WARPS + warp) * chunk;
   if (c0 >= ncc) return;
   const int nch = (int)(ncc - c0 < chunk ? ncc - c0 : chunk);
-  TA* stage = smem[warp];                // [2][P][REC]
-  TA* red = smem[warp] + 2 * P * REC;    // [SLOTS][N1][PLANE]
+  TA* stage = smem[warp];  // [2][P][REC]
+  TA* red = smem[warp] + (K::kAlias ? 0 : K::STAGE_ELEMS);  // [SLOTS][N1][PLANE]; kAlias: over the staging buffers
   const CellRounds R{cell_start[c0 + min(lane, nch)], nch};
   zero_empty_cells(R, c0, NOUT, lane, cellbuf);
   const int slot = lane / G, g = lane % G;
@@ -542,6 +554,7 @@ __global__ void __launch_bounds__(StagedRestrict<DIM, PC, NCOMP, PL, TA>::WARPS 
         buf ^= 1;  // the next round writes the other buffer: one barrier per round
       },
       [&](int ci) {
+        if constexpr (K::kAlias) __syncwarp();  // every lane is done with the staged round: its buffers become the reduction buffer
         if (grp) {
 #pragma unroll
           for (int p = 0; p < PL; ++p)
